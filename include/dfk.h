@@ -1,0 +1,241 @@
+/*
+ * dfk.h — C ABI of the B200-native fused SwiGLU-MLP path (DeepFusionKernel,
+ * arXiv 2602.11808).
+ *
+ * This is the drop-in boundary for the reference's C++ operator API
+ * (/root/reference/proj/include/deepfusion/{fused,swiglu,tp,tuner}.hpp).
+ * Plain pointers and sizes only; no C++ or torch types cross it; no
+ * exceptions cross it.  Every entry point returns a dfk_status (0 = OK) and
+ * leaves a thread-local message in dfk_last_error() on failure.
+ *
+ * Mapping of the reference interface (file:line under
+ * /root/reference/proj/) to the entry points that replace it:
+ *
+ *   run_fused_stage1   include/deepfusion/fused.hpp:61-63     -> dfk_stage1
+ *   run_fused          include/deepfusion/fused.hpp:66-67     -> dfk_forward
+ *   down_projection    include/deepfusion/swiglu.hpp:90-91    -> dfk_down
+ *   run_stage1         include/deepfusion/fused.hpp:82-84     -> dfk_stage1
+ *                                                               (cfg.variant)
+ *   run_variant        include/deepfusion/fused.hpp:87-89     -> dfk_forward
+ *                                                               (cfg.variant)
+ *   run_four_kernel / run_two_kernel  swiglu.hpp:64-76        -> dfk_forward
+ *                                       (DFK_VARIANT_FOUR/TWO_KERNEL)
+ *   MlpWeights (+validate)  swiglu.hpp:49-57, swiglu.cpp:26-39 -> dfk_weights_create
+ *   make_plan / run_tp_mlp  tp.hpp:54-79                      -> dfk_tp_init*,
+ *                                                               dfk_tp_forward,
+ *                                                               dfk_weights_create
+ *                                                               (ff_begin/ff_end)
+ *   balanced_ranges         tp.hpp:36, tp.cpp:8-29            -> dfk_balanced_range
+ *   profile / select / Tuner::get_or_tune  tuner.hpp:103-137  -> dfk_tune
+ *   cache_store / cache_lookup  tuner.hpp:102-113              -> dfk_tune (cache_path)
+ *   default_candidates      tuner.hpp:55                      -> dfk_candidates
+ *   default_fingerprint     tuner.hpp:116                     -> dfk_fingerprint
+ *   predict_traffic         traffic.hpp:60-71 (fused, single tile)
+ *                                                             -> dfk_block_bytes
+ *
+ * Error classes mirror the reference's exceptions: ShapeError
+ * (tensor.hpp:21-23) -> DFK_ERR_SHAPE; std::invalid_argument (unknown
+ * variant, scheme mismatch) -> DFK_ERR_INVALID; "every candidate
+ * disqualified" (tuner.cpp:185-188) -> DFK_ERR_GATE; CacheError
+ * (tuner.hpp:97-99) -> DFK_ERR_CACHE.
+ *
+ * Data: activations are bf16 row-major on the device (X [B x d_model],
+ * A2 [B x d_ff_shard]); Y is fp32 or bf16 [B x d_model].  Weights are
+ * registered once in the reference layout (W_gate, W_up [d_model x d_ff],
+ * W_down [d_ff x d_model], row-major; fp64 / fp32 / bf16; host or device)
+ * and prepacked into the streaming layout.  All compute calls are
+ * asynchronous on the context's stream; the caller synchronises.  One
+ * context per GPU per host thread.
+ */
+#ifndef DFK_H_
+#define DFK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFK_API __attribute__((visibility("default")))
+
+typedef enum dfk_status {
+  DFK_OK = 0,
+  DFK_ERR_SHAPE = 1,       /* reference ShapeError */
+  DFK_ERR_INVALID = 2,     /* reference std::invalid_argument */
+  DFK_ERR_CUDA = 3,
+  DFK_ERR_NCCL = 4,
+  DFK_ERR_NOMEM = 5,
+  DFK_ERR_UNSUPPORTED = 6,
+  DFK_ERR_GATE = 7,        /* every scheduler candidate failed the gate */
+  DFK_ERR_CACHE = 8        /* reference CacheError */
+} dfk_status;
+
+typedef enum dfk_dtype { DFK_F64 = 0, DFK_F32 = 1, DFK_BF16 = 2 } dfk_dtype;
+typedef enum dfk_memory { DFK_HOST = 0, DFK_DEVICE = 1 } dfk_memory;
+
+/* Execution layout of the block (reference VariantTag, swiglu.hpp:16). */
+typedef enum dfk_variant {
+  DFK_VARIANT_FUSED = 0,       /* fused stage 1 + down (the product)        */
+  DFK_VARIANT_TWO_KERNEL = 1,  /* cuBLASLt [W_gate|W_up] GEMM + silu_mul +
+                                  cuBLASLt down: the unfused comparator     */
+  DFK_VARIANT_FOUR_KERNEL = 2  /* 2 GEMMs + silu + mul + down               */
+} dfk_variant;
+
+/* Kernel family of a fused stage (0 = let the library choose). */
+typedef enum dfk_family {
+  DFK_FAMILY_AUTO = 0,
+  DFK_FAMILY_TC = 1,    /* tcgen05 / TMEM tensor-core kernel ("F2")       */
+  DFK_FAMILY_GEMV = 2   /* CUDA-core warp GEMV, batch <= 8 ("F1")         */
+} dfk_family;
+
+/* One scheduler candidate / launch configuration (the GPU counterpart of
+ * KernelConfig + TileConfig, fused.hpp:25-47).  Zero-initialised fields mean
+ * "library default". */
+typedef struct dfk_config {
+  int32_t variant;      /* dfk_variant                                     */
+  int32_t s1_family;    /* dfk_family for the fused stage 1                */
+  int32_t s1_stages;    /* smem pipeline depth (0 = deepest that fits)     */
+  int32_t s1_ctas;      /* persistent CTAs (0 = one per SM)                */
+  int32_t s1_split_k;   /* CTAs sharing one stage-1 tile (1 = none)        */
+  int32_t down_family;  /* dfk_family for the down projection              */
+  int32_t down_stages;
+  int32_t down_ctas;    /* stream-K CTAs (0 = one per SM)                  */
+  int32_t pdl;          /* 1 = programmatic dependent launch between the
+                           two kernels (and across calls); 0 = plain       */
+  int32_t mutant;       /* negative controls, tests only (0 = none)        */
+  int32_t reserved[6];
+  char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
+} dfk_config;
+
+typedef struct dfk_context_s* dfk_context;
+typedef struct dfk_weights_s* dfk_weights;
+
+/* --- library / context ------------------------------------------------- */
+DFK_API const char* dfk_last_error(void);
+DFK_API const char* dfk_version(void);
+DFK_API int dfk_device_count(int* n);
+/* stream: a cudaStream_t to run on, or NULL for a context-owned stream. */
+DFK_API int dfk_context_create(int device, void* stream, dfk_context* out);
+DFK_API int dfk_context_destroy(dfk_context ctx);
+DFK_API int dfk_context_sync(dfk_context ctx);
+DFK_API int dfk_context_stream(dfk_context ctx, void** stream);
+/* Free-text device descriptor used as the tuning-cache fingerprint
+ * (the GPU counterpart of default_fingerprint, tuner.cpp:392-406). */
+DFK_API int dfk_fingerprint(dfk_context ctx, char* buf, size_t len);
+DFK_API int dfk_sm_count(dfk_context ctx, int* n);
+
+/* --- weights --------------------------------------------------------- */
+/* Registers one block's weights in the reference layout and prepacks them.
+ * [ff_begin, ff_end) selects a tensor-parallel shard of d_ff (pass 0, d_ff
+ * for the whole block): W_gate/W_up columns and W_down rows of that range
+ * (tp.cpp:140-167).  Errors: DFK_ERR_SHAPE for dims < 1 or an empty /
+ * out-of-range shard. */
+DFK_API int dfk_weights_create(dfk_context ctx, const void* w_gate,
+                               const void* w_up, const void* w_down,
+                               int64_t d_model, int64_t d_ff, int32_t dtype,
+                               int32_t memory, int64_t ff_begin,
+                               int64_t ff_end, dfk_weights* out);
+DFK_API int dfk_weights_destroy(dfk_weights w);
+DFK_API int dfk_weights_shape(dfk_weights w, int64_t* d_model,
+                              int64_t* d_ff_shard, int64_t* ff_begin);
+/* Bytes of packed weights resident in HBM for this handle. */
+DFK_API int dfk_weights_bytes(dfk_weights w, int64_t* bytes);
+
+/* --- the hot path (device pointers, asynchronous) ---------------------- */
+/* A2 = (X W_up) * silu(X W_gate): X bf16 [B x d_model], A2 bf16
+ * [B x d_ff_shard].  cfg NULL = scheduler's choice for B. */
+DFK_API int dfk_stage1(dfk_context ctx, dfk_weights w, const void* x,
+                       int64_t batch, void* a2, const dfk_config* cfg);
+/* Y = A2 W_down: A2 bf16 [B x d_ff_shard], Y (y_dtype F32/BF16)
+ * [B x d_model]. */
+DFK_API int dfk_down(dfk_context ctx, dfk_weights w, const void* a2,
+                     int64_t batch, void* y, int32_t y_dtype,
+                     const dfk_config* cfg);
+/* Whole block: Y = stage-2(stage-1(X)); A2 lives in context scratch. */
+DFK_API int dfk_forward(dfk_context ctx, dfk_weights w, const void* x,
+                        int64_t batch, void* y, int32_t y_dtype,
+                        const dfk_config* cfg);
+/* Reference-facing call with HOST buffers (synchronous): converts X
+ * (x_dtype F64/F32/BF16) to bf16, copies it in, runs dfk_forward (or
+ * dfk_tp_forward when the context has a TP communicator), copies Y out and
+ * converts it to y_dtype. */
+DFK_API int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
+                             int32_t x_dtype, int64_t batch, void* y,
+                             int32_t y_dtype, const dfk_config* cfg);
+
+/* --- scheduler (tuner.cpp semantics) ----------------------------------- */
+/* Candidate grid for (weights, B): fills up to `cap` configs, returns the
+ * count in *n (default_candidates, tuner.cpp:59-88). */
+DFK_API int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
+                           dfk_config* out, int32_t cap, int32_t* n);
+/* Profiles every candidate on the context's GPU (CUDA-event timing: one
+ * gate run, `warmup` >= 1 untimed runs, `runs` >= 3 timed runs, lower
+ * median), disqualifies those deviating from the unfused cuBLASLt reference
+ * by more than the bf16 gate (max|dY| / max|Y_ref| > 1e-2), selects by
+ * (median, fusion preference, label), stores it for later NULL-cfg calls,
+ * and persists it in the JSON cache at cache_path (NULL/"" = memory only;
+ * format_version 1, flock-guarded, keyed by (B, d_model, d_ff, TP degree,
+ * GPU fingerprint)).  A cache hit skips profiling.  *from_cache is set to
+ * 1 on a hit.  results_json (optional) receives the ScheduleEntry as JSON. */
+DFK_API int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
+                     const char* cache_path, int32_t warmup, int32_t runs,
+                     dfk_config* chosen, int32_t* from_cache,
+                     char* results_json, size_t results_len);
+/* The configuration a NULL-cfg call with this B would use. */
+DFK_API int dfk_select_config(dfk_context ctx, dfk_weights w, int64_t batch,
+                              dfk_config* out);
+
+/* --- tensor parallelism over NCCL -------------------------------------- */
+/* ncclUniqueId is 128 bytes. */
+DFK_API int dfk_tp_unique_id(void* id128);
+/* Multi-process (one rank per GPU): every rank calls with the same id. */
+DFK_API int dfk_tp_init(dfk_context ctx, const void* id128, int rank,
+                        int nranks);
+/* Single process driving `n` contexts on n devices (ncclCommInitAll). */
+DFK_API int dfk_tp_init_all(dfk_context* ctxs, int n);
+DFK_API int dfk_tp_rank(dfk_context ctx, int* rank, int* nranks);
+/* Fused stage 1 + down on this rank's shard into fp32 partial Y, then one
+ * in-place ncclAllReduce(sum) of B x d_model on the context stream (the one
+ * collective of the compound scheme, tp.cpp:140-167). */
+DFK_API int dfk_tp_forward(dfk_context ctx, dfk_weights w, const void* x,
+                           int64_t batch, float* y, const dfk_config* cfg);
+/* balanced_ranges(extent, parts)[index] (tp.cpp:8-29). */
+DFK_API int dfk_balanced_range(int64_t extent, int64_t parts, int64_t index,
+                               int64_t* begin, int64_t* end);
+
+/* --- traffic model ------------------------------------------------------ */
+/* Algorithmic bytes of one fused block call at 2 B/element: the reference's
+ * fused single-tile model, stage 1 + stage 2 (traffic.cpp:70-76, 82-94),
+ * with d_ff the (shard) width. */
+DFK_API int dfk_block_bytes(int64_t batch, int64_t d_model, int64_t d_ff,
+                            int64_t* stage1, int64_t* stage2);
+
+/* --- device memory / timing plumbing ----------------------------------- */
+DFK_API int dfk_malloc(dfk_context ctx, size_t bytes, void** p);
+DFK_API int dfk_free(dfk_context ctx, void* p);
+DFK_API int dfk_host_alloc(size_t bytes, void** p); /* pinned */
+DFK_API int dfk_host_free(void* p);
+DFK_API int dfk_memcpy_h2d(dfk_context ctx, void* dst, const void* src,
+                           size_t bytes);
+DFK_API int dfk_memcpy_d2h(dfk_context ctx, void* dst, const void* src,
+                           size_t bytes);
+DFK_API int dfk_memset(dfk_context ctx, void* p, int value, size_t bytes);
+/* Fills a device bf16 buffer with uniform values in [lo, hi) (synthetic
+ * bench inputs; counter-based hash, seed-deterministic). */
+DFK_API int dfk_fill_uniform_bf16(dfk_context ctx, void* p, int64_t n,
+                                  uint64_t seed, float lo, float hi);
+DFK_API int dfk_event_create(void** ev);
+DFK_API int dfk_event_destroy(void* ev);
+DFK_API int dfk_event_record(dfk_context ctx, void* ev);
+DFK_API int dfk_event_elapsed_ms(void* start, void* stop, float* ms);
+/* Writes `bytes` of junk to a scratch buffer larger than L2 (flush). */
+DFK_API int dfk_flush_l2(dfk_context ctx);
+/* Number of hot-path kernel launches issued by this context so far. */
+DFK_API int dfk_launch_count(dfk_context ctx, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFK_H_ */

@@ -1,0 +1,925 @@
+// api.cu — the C ABI (include/dfk.h): contexts, weight registration +
+// prepack, the fused forward path and its unfused cuBLASLt comparators,
+// host-buffer forward, and the memory / timing plumbing.
+//
+// Reference behaviour mirrored here (paths under /root/reference/proj):
+//   shape validation & ShapeError       src/fused.cpp:49-68, swiglu.cpp:26-39
+//   run_fused = stage 1 then down       src/fused.cpp:209-216
+//   two-kernel layout (gate cols first) src/swiglu.cpp:130-166, 194-212
+//   four-kernel layout                  src/swiglu.cpp:170-192
+//   down_projection                     src/swiglu.cpp:214-226
+//   balanced_ranges                     src/tp.cpp:8-29
+//   fused traffic model                 src/traffic.cpp:70-76, 82-94
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "internal.h"
+#include "layout.cuh"
+#include "stream_kernels.cuh"
+
+namespace dfk {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(int status, const std::string& msg) {
+  (void)status;
+  g_last_error = msg;
+}
+
+int fail(int status, const std::string& msg) {
+  set_error(status, msg);
+  return status;
+}
+
+int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return DFK_OK;
+  if (b.p) {
+    cudaStreamSynchronize(s);
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    return fail(DFK_ERR_NOMEM, std::string("cudaMalloc(") +
+                                   std::to_string(bytes) +
+                                   "): " + cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  if (zero) DFK_CUDA(cudaMemsetAsync(b.p, 0, bytes, s));
+  return DFK_OK;
+}
+
+std::string config_label(const dfk_config& c) {
+  if (c.label[0]) return c.label;
+  std::ostringstream o;
+  if (c.variant == DFK_VARIANT_TWO_KERNEL) return "two_kernel_cublaslt";
+  if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
+  o << "fused_s1" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
+    << c.s1_stages << "_c" << c.s1_ctas << "_dn"
+    << (c.down_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
+    << c.down_stages << "_c" << c.down_ctas << (c.pdl ? "_pdl" : "");
+  return o.str();
+}
+
+namespace {
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// ---------------------------------------------------------------------------
+// TMA descriptors (driver entry point fetched through the runtime so the
+// library does not link libcuda directly).
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [rows x inner] with row stride `ld` elements; box
+// 64 (inner) x box_rows, 128B swizzle; out-of-bounds reads are zero.
+int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
+             int64_t ld, int box_rows, CUtensorMap* out) {
+  auto key = std::make_tuple(reinterpret_cast<uintptr_t>(ptr), inner, rows, ld,
+                             box_rows);
+  auto it = ctx->tmaps.find(key);
+  if (it != ctx->tmaps.end()) {
+    *out = it->second;
+    return DFK_OK;
+  }
+  auto enc = tmap_encoder();
+  if (!enc) return fail(DFK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner),
+                        static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    return fail(DFK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" +
+                                  std::to_string(static_cast<int>(r)) + ")");
+  }
+  if (ctx->tmaps.size() > 4096) ctx->tmaps.clear();
+  ctx->tmaps.emplace(key, m);
+  *out = m;
+  return DFK_OK;
+}
+
+int max_stages(dfk_context_s* ctx, int n_pad) {
+  const int avail = ctx->max_smem_optin - 1024 - 1024;
+  int s = avail / stream_stage_bytes(n_pad);
+  return std::max(2, std::min(s, 32));
+}
+
+int gemv_nb(int64_t b) {
+  if (b <= 1) return 1;
+  if (b <= 2) return 2;
+  if (b <= 4) return 4;
+  return 8;
+}
+
+// Makes an activation operand TMA-legal (16-byte aligned base, row stride a
+// multiple of 16 bytes); copies into `pad` when it is not.
+int tma_operand(dfk_context_s* ctx, const void* p, int64_t rows, int64_t cols,
+                int64_t ld, DeviceBuf& pad, const void** out, int64_t* out_ld) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld % 8) == 0) {
+    *out = p;
+    *out_ld = ld;
+    return DFK_OK;
+  }
+  const int64_t ld2 = round_up(cols, 8);
+  DFK_TRY(ensure_buf(pad, static_cast<size_t>(rows * ld2 * 2), false,
+                     ctx->stream));
+  DFK_CUDA(launch_pad_rows(static_cast<const __nv_bfloat16*>(p), rows, cols,
+                           ld, static_cast<__nv_bfloat16*>(pad.p), ld2,
+                           ctx->stream));
+  ctx->launches++;
+  *out = pad.p;
+  *out_ld = ld2;
+  return DFK_OK;
+}
+
+int check_batch(int64_t B) {
+  if (B < 1) {
+    return fail(DFK_ERR_SHAPE, "batch must be >= 1, got " + std::to_string(B));
+  }
+  return DFK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused stage 1 / down launchers.
+// ---------------------------------------------------------------------------
+int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
+                 int64_t B, __nv_bfloat16* a2, int64_t a2_ld,
+                 const dfk_config& cfg) {
+  const bool tc = cfg.s1_family != DFK_FAMILY_GEMV;
+  if (!tc && B > 8) {
+    // GEMV family handles up to 8 rows per launch; chunk larger batches.
+  }
+  const void* xp;
+  int64_t x_ld;
+  DFK_TRY(tma_operand(ctx, x, B, w->d_model, w->d_model, ctx->xpad, &xp, &x_ld));
+  const int64_t chunk = tc ? 256 : 8;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t nb = std::min(chunk, B - b0);
+    const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
+    CUtensorMap tm;
+    DFK_TRY(get_tmap(ctx,
+                     static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
+                     w->d_model, nb, x_ld, n_pad, &tm));
+    StreamArgs a = {};
+    a.wpack = w->s1_pack;
+    a.tiles = w->s1_tiles;
+    a.kblocks = w->s1_kblocks;
+    a.B = static_cast<int>(nb);
+    a.n_pad = n_pad;
+    a.stages = cfg.s1_stages > 0 ? std::min(cfg.s1_stages, max_stages(ctx, n_pad))
+                                 : max_stages(ctx, n_pad);
+    a.split_k = 1;
+    a.a2 = a2 + b0 * a2_ld;
+    a.a2_ld = a2_ld;
+    a.cols_valid = static_cast<int>(w->d_ff);
+    a.mutant = cfg.mutant;
+    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : ctx->sm_count;
+    grid = std::max(1, std::min(grid, w->s1_tiles));
+    cudaError_t e = launch_stream(kModeStage1, tc, gemv_nb(nb), tm, a, grid,
+                                  cfg.pdl != 0, ctx->stream);
+    if (e != cudaSuccess)
+      return fail(DFK_ERR_CUDA, std::string("stage-1 launch: ") +
+                                    cudaGetErrorString(e));
+    ctx->launches++;
+  }
+  return DFK_OK;
+}
+
+int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
+               int64_t a2_ld, int64_t B, void* y, int64_t y_ld, bool y_bf16,
+               const dfk_config& cfg) {
+  const bool tc = cfg.down_family != DFK_FAMILY_GEMV;
+  const void* ap;
+  int64_t a_ld;
+  DFK_TRY(tma_operand(ctx, a2, B, w->d_ff, a2_ld, ctx->a2pad, &ap, &a_ld));
+  const int64_t chunk = tc ? 256 : 8;
+  const int yacc_ld = w->dn_tiles * kDownCols;
+  DFK_TRY(ensure_buf(ctx->yacc,
+                     static_cast<size_t>(std::min<int64_t>(chunk, B)) *
+                         yacc_ld * sizeof(float),
+                     true, ctx->stream));
+  DFK_TRY(ensure_buf(ctx->counters, static_cast<size_t>(w->dn_tiles) * 4, true,
+                     ctx->stream));
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t nb = std::min(chunk, B - b0);
+    const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
+    CUtensorMap tm;
+    DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
+                     w->d_ff, nb, a_ld, n_pad, &tm));
+    StreamArgs a = {};
+    a.wpack = w->dn_pack;
+    a.tiles = w->dn_tiles;
+    a.kblocks = w->dn_kblocks;
+    a.B = static_cast<int>(nb);
+    a.n_pad = n_pad;
+    a.stages = cfg.down_stages > 0
+                   ? std::min(cfg.down_stages, max_stages(ctx, n_pad))
+                   : max_stages(ctx, n_pad);
+    a.split_k = 1;
+    a.yacc = static_cast<float*>(ctx->yacc.p);
+    a.yacc_ld = yacc_ld;
+    a.counters = static_cast<int*>(ctx->counters.p);
+    a.y = y_bf16 ? static_cast<void*>(static_cast<__nv_bfloat16*>(y) + b0 * y_ld)
+                 : static_cast<void*>(static_cast<float*>(y) + b0 * y_ld);
+    a.y_ld = y_ld;
+    a.y_bf16 = y_bf16 ? 1 : 0;
+    a.out_cols = static_cast<int>(w->d_model);
+    const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
+    int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count;
+    grid = std::max<int64_t>(1, std::min<int64_t>(grid, U));
+    cudaError_t e = launch_stream(kModeDown, tc, gemv_nb(nb), tm, a,
+                                  static_cast<int>(grid), cfg.pdl != 0,
+                                  ctx->stream);
+    if (e != cudaSuccess)
+      return fail(DFK_ERR_CUDA,
+                  std::string("down launch: ") + cudaGetErrorString(e));
+    ctx->launches++;
+  }
+  return DFK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Unfused comparators on cuBLASLt (bf16 in, fp32 accumulate).
+// ---------------------------------------------------------------------------
+int ensure_unfused_weights(dfk_context_s* ctx, dfk_weights_s* w) {
+  if (w->cat_t && w->down_t) return DFK_OK;
+  const size_t cat_bytes = static_cast<size_t>(2 * w->d_ff * w->d_model) * 2;
+  const size_t down_bytes = static_cast<size_t>(w->d_ff * w->d_model) * 2;
+  if (cudaMalloc(&w->cat_t, cat_bytes) != cudaSuccess ||
+      cudaMalloc(&w->down_t, down_bytes) != cudaSuccess) {
+    return fail(DFK_ERR_NOMEM, "unfused comparator weights");
+  }
+  DFK_CUDA(launch_unpack_stage1(w->s1_pack, w->d_model, w->d_ff, w->s1_tiles,
+                                w->s1_kblocks, w->cat_t, ctx->stream));
+  DFK_CUDA(launch_unpack_down(w->dn_pack, w->d_model, w->d_ff, w->dn_tiles,
+                              w->dn_kblocks, w->down_t, ctx->stream));
+  return DFK_OK;
+}
+
+// C[n x m] (row-major, ldc) = B[n x k] (row-major, ldb) * A[m x k]^T where A
+// is K-major [m x k] (lda).  In cuBLAS column-major terms: C_cm[m x n] =
+// op_T(A_cm[k x m]) * B_cm[k x n].
+int lt_gemm(dfk_context_s* ctx, const __nv_bfloat16* A, int64_t lda,
+            const __nv_bfloat16* Bm, int64_t ldb, void* C, int64_t ldc,
+            bool c_bf16, int64_t m, int64_t n, int64_t k) {
+  if (!ctx->lt) {
+    if (cublasLtCreate(&ctx->lt) != CUBLAS_STATUS_SUCCESS)
+      return fail(DFK_ERR_CUDA, "cublasLtCreate");
+  }
+  const size_t ws_bytes = 32u << 20;
+  DFK_TRY(ensure_buf(ctx->lt_ws, ws_bytes, false, ctx->stream));
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  const cudaDataType_t ct = c_bf16 ? CUDA_R_16BF : CUDA_R_32F;
+  cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F);
+  cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+  cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
+  cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
+  cublasLtMatrixLayoutCreate(&la, CUDA_R_16BF, k, m, lda);
+  cublasLtMatrixLayoutCreate(&lb, CUDA_R_16BF, k, n, ldb);
+  cublasLtMatrixLayoutCreate(&lc, ct, m, n, ldc);
+  auto key = std::make_tuple(m, n, k, c_bf16 ? 1 : 0);
+  auto it = ctx->lt_algos.find(key);
+  cublasLtMatmulAlgo_t algo;
+  if (it == ctx->lt_algos.end()) {
+    cublasLtMatmulPreference_t pref = nullptr;
+    cublasLtMatmulPreferenceCreate(&pref);
+    size_t wsb = ws_bytes;
+    cublasLtMatmulPreferenceSetAttribute(
+        pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb));
+    cublasLtMatmulHeuristicResult_t res[4];
+    int got = 0;
+    cublasStatus_t st = cublasLtMatmulAlgoGetHeuristic(
+        ctx->lt, op, la, lb, lc, lc, pref, 4, res, &got);
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (st != CUBLAS_STATUS_SUCCESS || got == 0) {
+      cublasLtMatmulDescDestroy(op);
+      cublasLtMatrixLayoutDestroy(la);
+      cublasLtMatrixLayoutDestroy(lb);
+      cublasLtMatrixLayoutDestroy(lc);
+      return fail(DFK_ERR_CUDA, "cuBLASLt: no algorithm for the unfused GEMM");
+    }
+    algo = res[0].algo;
+    ctx->lt_algos.emplace(key, algo);
+  } else {
+    algo = it->second;
+  }
+  const float alpha = 1.f, beta = 0.f;
+  cublasStatus_t st =
+      cublasLtMatmul(ctx->lt, op, &alpha, A, la, Bm, lb, &beta, C, lc, C, lc,
+                     &algo, ctx->lt_ws.p, ws_bytes, ctx->stream);
+  cublasLtMatmulDescDestroy(op);
+  cublasLtMatrixLayoutDestroy(la);
+  cublasLtMatrixLayoutDestroy(lb);
+  cublasLtMatrixLayoutDestroy(lc);
+  if (st != CUBLAS_STATUS_SUCCESS)
+    return fail(DFK_ERR_CUDA, "cublasLtMatmul failed (" +
+                                  std::to_string(static_cast<int>(st)) + ")");
+  ctx->launches++;
+  return DFK_OK;
+}
+
+// Stage 1 of the unfused layouts into a2 (ld = d_ff).
+int stage1_unfused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
+                   int64_t B, __nv_bfloat16* a2, int64_t a2_ld, int variant) {
+  DFK_TRY(ensure_unfused_weights(ctx, w));
+  const int64_t df = w->d_ff, dm = w->d_model;
+  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+  if (variant == DFK_VARIANT_TWO_KERNEL) {
+    // Grouped GEMM into [A_gate | A_1] (gate columns first), then silu-mul.
+    DFK_TRY(ensure_buf(ctx->concat, static_cast<size_t>(B * 2 * df) * 2, false,
+                       ctx->stream));
+    auto* cc = static_cast<__nv_bfloat16*>(ctx->concat.p);
+    DFK_TRY(lt_gemm(ctx, w->cat_t, dm, xb, dm, cc, 2 * df, true, 2 * df, B, dm));
+    DFK_CUDA(launch_silu_mul(cc, 2 * df, cc + df, 2 * df, a2, B, df,
+                             ctx->stream));
+    ctx->launches++;
+    (void)a2_ld;
+    return DFK_OK;
+  }
+  // Four-kernel: A_gate, A_1, A_silu materialised.
+  const size_t bytes = static_cast<size_t>(B * df) * 2;
+  DFK_TRY(ensure_buf(ctx->concat, bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx->tmp1, bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx->tmp2, bytes, false, ctx->stream));
+  auto* agate = static_cast<__nv_bfloat16*>(ctx->concat.p);
+  auto* a1 = static_cast<__nv_bfloat16*>(ctx->tmp1.p);
+  auto* asilu = static_cast<__nv_bfloat16*>(ctx->tmp2.p);
+  DFK_TRY(lt_gemm(ctx, w->cat_t, dm, xb, dm, agate, df, true, df, B, dm));
+  DFK_TRY(lt_gemm(ctx, w->cat_t + df * dm, dm, xb, dm, a1, df, true, df, B, dm));
+  DFK_CUDA(launch_silu(agate, asilu, B * df, ctx->stream));
+  DFK_CUDA(launch_mul(a1, asilu, a2, B * df, ctx->stream));
+  ctx->launches += 2;
+  return DFK_OK;
+}
+
+int down_unfused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
+                 int64_t B, void* y, bool y_bf16) {
+  DFK_TRY(ensure_unfused_weights(ctx, w));
+  return lt_gemm(ctx, w->down_t, w->d_ff, static_cast<const __nv_bfloat16*>(a2),
+                 w->d_ff, y, w->d_model, y_bf16, w->d_model, B, w->d_ff);
+}
+
+int check_handles(dfk_context_s* ctx, dfk_weights_s* w) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  if (!w) return fail(DFK_ERR_INVALID, "null weights");
+  if (w->ctx != ctx)
+    return fail(DFK_ERR_INVALID, "weights belong to another context");
+  return DFK_OK;
+}
+
+uint16_t f32_to_bf16_bits(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu))
+    return static_cast<uint16_t>((u >> 16) | 0x40u);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+
+size_t dtype_size(int dt) { return dt == DFK_F64 ? 8 : dt == DFK_F32 ? 4 : 2; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Config resolution.
+// ---------------------------------------------------------------------------
+void default_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
+                    dfk_config* out) {
+  (void)ctx;
+  (void)w;
+  std::memset(out, 0, sizeof(*out));
+  out->variant = DFK_VARIANT_FUSED;
+  out->s1_family = DFK_FAMILY_TC;
+  out->down_family = DFK_FAMILY_TC;
+  out->s1_split_k = 1;
+  out->pdl = 1;
+  (void)B;
+  std::snprintf(out->label, sizeof(out->label), "%s",
+                config_label(*out).c_str());
+}
+
+int resolve_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
+                   const dfk_config* in, dfk_config* out) {
+  if (in) {
+    *out = *in;
+  } else {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto it = ctx->chosen.find(std::make_tuple(B, w->d_model, w->d_ff));
+    if (it != ctx->chosen.end()) {
+      *out = it->second;
+    } else {
+      default_config(ctx, w, B, out);
+    }
+  }
+  if (out->variant < 0 || out->variant > 2)
+    return fail(DFK_ERR_INVALID,
+                "unknown variant " + std::to_string(out->variant));
+  if (out->s1_family == DFK_FAMILY_AUTO) out->s1_family = DFK_FAMILY_TC;
+  if (out->down_family == DFK_FAMILY_AUTO) out->down_family = DFK_FAMILY_TC;
+  if (out->s1_family < 0 || out->s1_family > 2 || out->down_family < 0 ||
+      out->down_family > 2)
+    return fail(DFK_ERR_INVALID, "unknown kernel family");
+  if (out->s1_split_k < 1) out->s1_split_k = 1;
+  if (out->s1_stages < 0 || out->down_stages < 0 || out->s1_ctas < 0 ||
+      out->down_ctas < 0)
+    return fail(DFK_ERR_INVALID, "negative launch parameter");
+  return DFK_OK;
+}
+
+int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
+                 int64_t B, void* y, int y_dtype, const dfk_config* cfg_in) {
+  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_batch(B));
+  if (!x || !y) return fail(DFK_ERR_INVALID, "null activation pointer");
+  if (y_dtype != DFK_F32 && y_dtype != DFK_BF16)
+    return fail(DFK_ERR_INVALID, "y_dtype must be F32 or BF16");
+  dfk_config cfg;
+  DFK_TRY(resolve_config(ctx, w, B, cfg_in, &cfg));
+  const int64_t a2_ld = round_up(w->d_ff, 8);
+  DFK_TRY(ensure_buf(ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
+                     ctx->stream));
+  auto* a2 = static_cast<__nv_bfloat16*>(ctx->a2.p);
+  if (cfg.variant == DFK_VARIANT_FUSED) {
+    DFK_TRY(stage1_fused(ctx, w, x, B, a2, a2_ld, cfg));
+    return down_fused(ctx, w, a2, a2_ld, B, y, w->d_model, y_dtype == DFK_BF16,
+                      cfg);
+  }
+  // Unfused comparators want a dense X (ld = d_model) and dense A2.
+  DFK_TRY(stage1_unfused(ctx, w, x, B, a2, w->d_ff, cfg.variant));
+  return down_unfused(ctx, w, a2, B, y, y_dtype == DFK_BF16);
+}
+
+}  // namespace dfk
+
+using namespace dfk;
+
+// ===========================================================================
+// extern "C"
+// ===========================================================================
+extern "C" {
+
+const char* dfk_last_error(void) { return g_last_error.c_str(); }
+
+const char* dfk_version(void) { return "dfk-b200 0.1.0 (sm_100a)"; }
+
+int dfk_device_count(int* n) {
+  DFK_CUDA(cudaGetDeviceCount(n));
+  return DFK_OK;
+}
+
+int dfk_context_create(int device, void* stream, dfk_context* out) {
+  if (!out) return fail(DFK_ERR_INVALID, "null out");
+  *out = nullptr;
+  int n = 0;
+  DFK_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n)
+    return fail(DFK_ERR_INVALID, "device " + std::to_string(device) +
+                                     " out of range (" + std::to_string(n) +
+                                     " visible)");
+  DFK_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  DFK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0) {
+    return fail(DFK_ERR_UNSUPPORTED,
+                std::string("this library is built for sm_100a (B200); device "
+                            "is ") +
+                    prop.name + " sm_" + std::to_string(prop.major) +
+                    std::to_string(prop.minor));
+  }
+  auto* ctx = new dfk_context_s();
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  ctx->max_smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+  ctx->l2_bytes = prop.l2CacheSize;
+  ctx->name = prop.name;
+  ctx->cc_major = prop.major;
+  ctx->cc_minor = prop.minor;
+  cudaDriverGetVersion(&ctx->driver_version);
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete ctx;
+      return fail(DFK_ERR_CUDA, cudaGetErrorString(e));
+    }
+    ctx->own_stream = true;
+  }
+  *out = ctx;
+  return DFK_OK;
+}
+
+int dfk_context_destroy(dfk_context ctx) {
+  if (!ctx) return DFK_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc,
+                       &ctx->counters, &ctx->concat, &ctx->tmp1, &ctx->tmp2,
+                       &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev}) {
+    if (b->p) cudaFree(b->p);
+  }
+  if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
+  if (ctx->hy_pinned) cudaFreeHost(ctx->hy_pinned);
+  if (ctx->lt) cublasLtDestroy(ctx->lt);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return DFK_OK;
+}
+
+int dfk_context_sync(dfk_context ctx) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_context_stream(dfk_context ctx, void** stream) {
+  if (!ctx || !stream) return fail(DFK_ERR_INVALID, "null argument");
+  *stream = ctx->stream;
+  return DFK_OK;
+}
+
+int dfk_fingerprint(dfk_context ctx, char* buf, size_t len) {
+  if (!ctx || !buf) return fail(DFK_ERR_INVALID, "null argument");
+  int mem_clock = 0;
+  cudaDeviceGetAttribute(&mem_clock, cudaDevAttrMemoryClockRate, ctx->device);
+  std::ostringstream o;
+  o << ctx->name << "|sm_" << ctx->cc_major << ctx->cc_minor << "|" << ctx->sm_count
+    << "SM|memclk" << mem_clock << "|drv" << ctx->driver_version << "|tp"
+    << ctx->nranks;
+  std::snprintf(buf, len, "%s", o.str().c_str());
+  return DFK_OK;
+}
+
+int dfk_sm_count(dfk_context ctx, int* n) {
+  if (!ctx || !n) return fail(DFK_ERR_INVALID, "null argument");
+  *n = ctx->sm_count;
+  return DFK_OK;
+}
+
+int dfk_weights_create(dfk_context ctx, const void* w_gate, const void* w_up,
+                       const void* w_down, int64_t d_model, int64_t d_ff,
+                       int32_t dtype, int32_t memory, int64_t ff_begin,
+                       int64_t ff_end, dfk_weights* out) {
+  if (!ctx || !out) return fail(DFK_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (d_model < 1 || d_ff < 1) {
+    return fail(DFK_ERR_SHAPE, "MlpWeights: dimensions must be >= 1, got d_model=" +
+                                   std::to_string(d_model) +
+                                   " d_ff=" + std::to_string(d_ff));
+  }
+  if (ff_begin < 0 || ff_end > d_ff || ff_begin >= ff_end) {
+    return fail(DFK_ERR_SHAPE, "shard [" + std::to_string(ff_begin) + ", " +
+                                   std::to_string(ff_end) +
+                                   ") is empty or outside [0, " +
+                                   std::to_string(d_ff) + ")");
+  }
+  if (!w_gate || !w_up || !w_down) return fail(DFK_ERR_INVALID, "null weight");
+  if (dtype != DFK_F64 && dtype != DFK_F32 && dtype != DFK_BF16)
+    return fail(DFK_ERR_INVALID, "unknown dtype");
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  auto* w = new dfk_weights_s();
+  w->ctx = ctx;
+  w->d_model = d_model;
+  w->d_ff = ff_end - ff_begin;
+  w->ff_begin = ff_begin;
+  w->d_ff_total = d_ff;
+  w->s1_tiles = static_cast<int>(ceil_div64(w->d_ff, kS1Cols));
+  w->s1_kblocks = static_cast<int>(ceil_div64(d_model, kBlockK));
+  w->dn_tiles = static_cast<int>(ceil_div64(d_model, kDownCols));
+  w->dn_kblocks = static_cast<int>(ceil_div64(w->d_ff, kBlockK));
+  const size_t s1_bytes =
+      static_cast<size_t>(w->s1_tiles) * w->s1_kblocks * kBlockBytes;
+  const size_t dn_bytes =
+      static_cast<size_t>(w->dn_tiles) * w->dn_kblocks * kBlockBytes;
+  if (cudaMalloc(&w->s1_pack, s1_bytes) != cudaSuccess ||
+      cudaMalloc(&w->dn_pack, dn_bytes) != cudaSuccess) {
+    cudaFree(w->s1_pack);
+    delete w;
+    return fail(DFK_ERR_NOMEM, "weight pack allocation");
+  }
+  const void* g = w_gate;
+  const void* u = w_up;
+  const void* d = w_down;
+  void* staging[3] = {nullptr, nullptr, nullptr};
+  const size_t esz = dtype_size(dtype);
+  if (memory == DFK_HOST) {
+    const size_t n1 = static_cast<size_t>(d_model * d_ff) * esz;
+    const void* srcs[3] = {w_gate, w_up, w_down};
+    for (int i = 0; i < 3; ++i) {
+      if (cudaMalloc(&staging[i], n1) != cudaSuccess) {
+        for (void* p : staging) cudaFree(p);
+        cudaFree(w->s1_pack);
+        cudaFree(w->dn_pack);
+        delete w;
+        return fail(DFK_ERR_NOMEM, "weight staging allocation");
+      }
+      DFK_CUDA(cudaMemcpyAsync(staging[i], srcs[i], n1, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    }
+    g = staging[0];
+    u = staging[1];
+    d = staging[2];
+  }
+  cudaError_t e1 = launch_pack_stage1(g, u, dtype, d_model, d_ff, ff_begin,
+                                      w->d_ff, w->s1_tiles, w->s1_kblocks,
+                                      w->s1_pack, ctx->stream);
+  cudaError_t e2 = launch_pack_down(d, dtype, d_model, ff_begin, w->d_ff,
+                                    w->dn_tiles, w->dn_kblocks, w->dn_pack,
+                                    ctx->stream);
+  cudaError_t e3 = cudaStreamSynchronize(ctx->stream);
+  for (void* p : staging)
+    if (p) cudaFree(p);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+    cudaFree(w->s1_pack);
+    cudaFree(w->dn_pack);
+    delete w;
+    return fail(DFK_ERR_CUDA,
+                std::string("weight prepack: ") +
+                    cudaGetErrorString(e1 != cudaSuccess   ? e1
+                                       : e2 != cudaSuccess ? e2
+                                                           : e3));
+  }
+  *out = w;
+  return DFK_OK;
+}
+
+int dfk_weights_destroy(dfk_weights w) {
+  if (!w) return DFK_OK;
+  cudaSetDevice(w->ctx->device);
+  cudaStreamSynchronize(w->ctx->stream);
+  cudaFree(w->s1_pack);
+  cudaFree(w->dn_pack);
+  if (w->cat_t) cudaFree(w->cat_t);
+  if (w->down_t) cudaFree(w->down_t);
+  {
+    std::lock_guard<std::mutex> lk(w->ctx->mu);
+    w->ctx->tmaps.clear();
+  }
+  delete w;
+  return DFK_OK;
+}
+
+int dfk_weights_shape(dfk_weights w, int64_t* d_model, int64_t* d_ff_shard,
+                      int64_t* ff_begin) {
+  if (!w) return fail(DFK_ERR_INVALID, "null weights");
+  if (d_model) *d_model = w->d_model;
+  if (d_ff_shard) *d_ff_shard = w->d_ff;
+  if (ff_begin) *ff_begin = w->ff_begin;
+  return DFK_OK;
+}
+
+int dfk_weights_bytes(dfk_weights w, int64_t* bytes) {
+  if (!w || !bytes) return fail(DFK_ERR_INVALID, "null argument");
+  *bytes = (static_cast<int64_t>(w->s1_tiles) * w->s1_kblocks +
+            static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks) *
+           kBlockBytes;
+  return DFK_OK;
+}
+
+int dfk_stage1(dfk_context ctx, dfk_weights w, const void* x, int64_t batch,
+               void* a2, const dfk_config* cfg_in) {
+  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_batch(batch));
+  if (!x || !a2) return fail(DFK_ERR_INVALID, "null activation pointer");
+  dfk_config cfg;
+  DFK_TRY(resolve_config(ctx, w, batch, cfg_in, &cfg));
+  auto* out = static_cast<__nv_bfloat16*>(a2);
+  if (cfg.variant == DFK_VARIANT_FUSED)
+    return stage1_fused(ctx, w, x, batch, out, w->d_ff, cfg);
+  return stage1_unfused(ctx, w, x, batch, out, w->d_ff, cfg.variant);
+}
+
+int dfk_down(dfk_context ctx, dfk_weights w, const void* a2, int64_t batch,
+             void* y, int32_t y_dtype, const dfk_config* cfg_in) {
+  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_batch(batch));
+  if (!a2 || !y) return fail(DFK_ERR_INVALID, "null activation pointer");
+  if (y_dtype != DFK_F32 && y_dtype != DFK_BF16)
+    return fail(DFK_ERR_INVALID, "y_dtype must be F32 or BF16");
+  dfk_config cfg;
+  DFK_TRY(resolve_config(ctx, w, batch, cfg_in, &cfg));
+  if (cfg.variant == DFK_VARIANT_FUSED)
+    return down_fused(ctx, w, a2, w->d_ff, batch, y, w->d_model,
+                      y_dtype == DFK_BF16, cfg);
+  return down_unfused(ctx, w, a2, batch, y, y_dtype == DFK_BF16);
+}
+
+int dfk_forward(dfk_context ctx, dfk_weights w, const void* x, int64_t batch,
+                void* y, int32_t y_dtype, const dfk_config* cfg) {
+  return forward_impl(ctx, w, x, batch, y, y_dtype, cfg);
+}
+
+int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
+                     int32_t x_dtype, int64_t batch, void* y, int32_t y_dtype,
+                     const dfk_config* cfg) {
+  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_batch(batch));
+  if (!x || !y) return fail(DFK_ERR_INVALID, "null host pointer");
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  const int64_t dm = w->d_model;
+  const size_t xn = static_cast<size_t>(batch * dm);
+  const size_t xb = xn * 2;
+  const size_t yb = xn * 4;
+  if (ctx->hx_pinned_bytes < xb) {
+    if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
+    DFK_CUDA(cudaMallocHost(&ctx->hx_pinned, xb));
+    ctx->hx_pinned_bytes = xb;
+  }
+  if (ctx->hy_pinned_bytes < yb) {
+    if (ctx->hy_pinned) cudaFreeHost(ctx->hy_pinned);
+    DFK_CUDA(cudaMallocHost(&ctx->hy_pinned, yb));
+    ctx->hy_pinned_bytes = yb;
+  }
+  auto* hx = static_cast<uint16_t*>(ctx->hx_pinned);
+  if (x_dtype == DFK_BF16) {
+    std::memcpy(hx, x, xb);
+  } else if (x_dtype == DFK_F32) {
+    const float* xf = static_cast<const float*>(x);
+    for (size_t i = 0; i < xn; ++i) hx[i] = f32_to_bf16_bits(xf[i]);
+  } else if (x_dtype == DFK_F64) {
+    const double* xd = static_cast<const double*>(x);
+    for (size_t i = 0; i < xn; ++i)
+      hx[i] = f32_to_bf16_bits(static_cast<float>(xd[i]));
+  } else {
+    return fail(DFK_ERR_INVALID, "unknown x dtype");
+  }
+  DFK_TRY(ensure_buf(ctx->hx_dev, xb, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx->hy_dev, yb, false, ctx->stream));
+  DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, hx, xb, cudaMemcpyHostToDevice,
+                           ctx->stream));
+  if (ctx->comm) {
+    DFK_TRY(dfk_tp_forward(ctx, w, ctx->hx_dev.p, batch,
+                           static_cast<float*>(ctx->hy_dev.p), cfg));
+  } else {
+    DFK_TRY(forward_impl(ctx, w, ctx->hx_dev.p, batch, ctx->hy_dev.p, DFK_F32,
+                         cfg));
+  }
+  DFK_CUDA(cudaMemcpyAsync(ctx->hy_pinned, ctx->hy_dev.p, yb,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+  const float* hy = static_cast<const float*>(ctx->hy_pinned);
+  if (y_dtype == DFK_F32) {
+    std::memcpy(y, hy, yb);
+  } else if (y_dtype == DFK_F64) {
+    double* yd = static_cast<double*>(y);
+    for (size_t i = 0; i < xn; ++i) yd[i] = hy[i];
+  } else if (y_dtype == DFK_BF16) {
+    uint16_t* yh = static_cast<uint16_t*>(y);
+    for (size_t i = 0; i < xn; ++i) yh[i] = f32_to_bf16_bits(hy[i]);
+  } else {
+    return fail(DFK_ERR_INVALID, "unknown y dtype");
+  }
+  return DFK_OK;
+}
+
+int dfk_balanced_range(int64_t extent, int64_t parts, int64_t index,
+                       int64_t* begin, int64_t* end) {
+  if (parts < 1) return fail(DFK_ERR_SHAPE, "balanced_ranges: parts must be >= 1");
+  if (parts > extent)
+    return fail(DFK_ERR_SHAPE, "balanced_ranges: cannot split extent " +
+                                   std::to_string(extent) + " into " +
+                                   std::to_string(parts) + " non-empty ranges");
+  if (index < 0 || index >= parts) return fail(DFK_ERR_INVALID, "index out of range");
+  const int64_t base = extent / parts, rem = extent % parts;
+  const int64_t b = index * base + std::min(index, rem);
+  *begin = b;
+  *end = b + base + (index < rem ? 1 : 0);
+  return DFK_OK;
+}
+
+int dfk_block_bytes(int64_t batch, int64_t d_model, int64_t d_ff,
+                    int64_t* stage1, int64_t* stage2) {
+  if (batch < 1 || d_model < 1 || d_ff < 1)
+    return fail(DFK_ERR_SHAPE, "dims must be >= 1");
+  // Fused single covering tile: X once, both weights once, A2 written once;
+  // stage 2: A2 read once, W_down once, Y written once; 2 bytes/element.
+  if (stage1) *stage1 = 2 * (batch * d_model + 2 * d_model * d_ff + batch * d_ff);
+  if (stage2) *stage2 = 2 * (batch * d_ff + d_ff * d_model + batch * d_model);
+  return DFK_OK;
+}
+
+int dfk_malloc(dfk_context ctx, size_t bytes, void** p) {
+  if (!ctx || !p) return fail(DFK_ERR_INVALID, "null argument");
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+  if (e != cudaSuccess) return fail(DFK_ERR_NOMEM, cudaGetErrorString(e));
+  return DFK_OK;
+}
+
+int dfk_free(dfk_context ctx, void* p) {
+  if (ctx) cudaSetDevice(ctx->device);
+  if (p) DFK_CUDA(cudaFree(p));
+  return DFK_OK;
+}
+
+int dfk_host_alloc(size_t bytes, void** p) {
+  DFK_CUDA(cudaMallocHost(p, bytes ? bytes : 16));
+  return DFK_OK;
+}
+
+int dfk_host_free(void* p) {
+  if (p) DFK_CUDA(cudaFreeHost(p));
+  return DFK_OK;
+}
+
+int dfk_memcpy_h2d(dfk_context ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_memcpy_d2h(dfk_context ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_memset(dfk_context ctx, void* p, int value, size_t bytes) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_CUDA(cudaMemsetAsync(p, value, bytes, ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_fill_uniform_bf16(dfk_context ctx, void* p, int64_t n, uint64_t seed,
+                          float lo, float hi) {
+  if (!ctx || !p) return fail(DFK_ERR_INVALID, "null argument");
+  DFK_CUDA(launch_fill_uniform_bf16(static_cast<__nv_bfloat16*>(p), n, seed, lo,
+                                    hi, ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_event_create(void** ev) {
+  cudaEvent_t e;
+  DFK_CUDA(cudaEventCreate(&e));
+  *ev = e;
+  return DFK_OK;
+}
+
+int dfk_event_destroy(void* ev) {
+  if (ev) DFK_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+  return DFK_OK;
+}
+
+int dfk_event_record(dfk_context ctx, void* ev) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_event_elapsed_ms(void* start, void* stop, float* ms) {
+  DFK_CUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(stop)));
+  DFK_CUDA(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start),
+                                static_cast<cudaEvent_t>(stop)));
+  return DFK_OK;
+}
+
+int dfk_flush_l2(dfk_context ctx) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  const size_t bytes = static_cast<size_t>(std::max(ctx->l2_bytes, 1 << 20)) * 2;
+  DFK_TRY(ensure_buf(ctx->flush, bytes, false, ctx->stream));
+  DFK_CUDA(launch_flush(ctx->flush.p, bytes, ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_launch_count(dfk_context ctx, int64_t* n) {
+  if (!ctx || !n) return fail(DFK_ERR_INVALID, "null argument");
+  *n = ctx->launches;
+  return DFK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// internal.h — library-private state behind the dfk.h handles.
+#pragma once
+
+#include <cublasLt.h>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "dfk.h"
+
+namespace dfk {
+
+// Error plumbing: thread-local message + status, no exceptions across the
+// ABI.
+struct Error {
+  int status;
+  std::string msg;
+};
+void set_error(int status, const std::string& msg);
+int fail(int status, const std::string& msg);
+
+#define DFK_CUDA(call)                                                     \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess)                                                 \
+      return ::dfk::fail(DFK_ERR_CUDA, std::string(#call) + ": " +         \
+                                           cudaGetErrorString(e_));        \
+  } while (0)
+
+#define DFK_TRY(call)             \
+  do {                            \
+    int s_ = (call);              \
+    if (s_ != DFK_OK) return s_;  \
+  } while (0)
+
+struct DeviceBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace dfk
+
+struct dfk_context_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 0;
+  int max_smem_optin = 0;
+  int l2_bytes = 0;
+  std::string name;
+  int cc_major = 0, cc_minor = 0;
+  int driver_version = 0;
+  int64_t launches = 0;
+
+  // Scratch (grown on demand, never shrunk).
+  dfk::DeviceBuf a2;       // internal A2 of dfk_forward
+  dfk::DeviceBuf xpad;     // padded activations for unaligned shapes
+  dfk::DeviceBuf a2pad;    // padded A2 for dfk_down with unaligned d_ff
+  dfk::DeviceBuf yacc;     // fp32 down accumulator (kept all-zero)
+  dfk::DeviceBuf counters; // per-tile down arrival counters (kept zero)
+  dfk::DeviceBuf concat;   // unfused comparator intermediates
+  dfk::DeviceBuf tmp1, tmp2;
+  dfk::DeviceBuf lt_ws;    // cuBLASLt workspace
+  dfk::DeviceBuf flush;    // L2 flush buffer
+  dfk::DeviceBuf hx_dev, hy_dev;  // forward_host device staging
+  void* hx_pinned = nullptr;
+  size_t hx_pinned_bytes = 0;
+  void* hy_pinned = nullptr;
+  size_t hy_pinned_bytes = 0;
+
+  cublasLtHandle_t lt = nullptr;
+  std::map<std::tuple<int64_t, int64_t, int64_t, int>, cublasLtMatmulAlgo_t>
+      lt_algos;
+
+  // TMA descriptors keyed by (ptr, inner extent, rows, row stride, box rows).
+  std::map<std::tuple<uintptr_t, int64_t, int64_t, int64_t, int>, CUtensorMap>
+      tmaps;
+
+  // NCCL tensor parallelism.
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+
+  // Scheduler decisions: (batch, d_model, d_ff shard) -> config.
+  std::map<std::tuple<int64_t, int64_t, int64_t>, dfk_config> chosen;
+  std::mutex mu;
+};
+
+struct dfk_weights_s {
+  dfk_context_s* ctx = nullptr;
+  int64_t d_model = 0, d_ff = 0, ff_begin = 0, d_ff_total = 0;
+  // Stage 1: tiles of 64 A2 columns, K blocks over d_model.
+  int s1_tiles = 0, s1_kblocks = 0;
+  uint8_t* s1_pack = nullptr;
+  // Down: tiles of 128 Y columns, K blocks over d_ff.
+  int dn_tiles = 0, dn_kblocks = 0;
+  uint8_t* dn_pack = nullptr;
+  // Unfused comparator (built lazily from the packs): K-major bf16
+  // W_cat^T [2 d_ff x d_model] (gate rows first) and W_down^T
+  // [d_model x d_ff].
+  __nv_bfloat16* cat_t = nullptr;
+  __nv_bfloat16* down_t = nullptr;
+};
+
+namespace dfk {
+
+// Kernels in aux_kernels.cu.
+cudaError_t launch_pack_stage1(const void* w_gate, const void* w_up, int dtype,
+                               int64_t d_model, int64_t d_ff_total,
+                               int64_t ff_begin, int64_t d_ff, int tiles,
+                               int kblocks, uint8_t* dst, cudaStream_t s);
+cudaError_t launch_pack_down(const void* w_down, int dtype, int64_t d_model,
+                             int64_t ff_begin, int64_t d_ff, int tiles,
+                             int kblocks, uint8_t* dst, cudaStream_t s);
+cudaError_t launch_unpack_stage1(const uint8_t* pack, int64_t d_model,
+                                 int64_t d_ff, int tiles, int kblocks,
+                                 __nv_bfloat16* cat_t, cudaStream_t s);
+cudaError_t launch_unpack_down(const uint8_t* pack, int64_t d_model,
+                               int64_t d_ff, int tiles, int kblocks,
+                               __nv_bfloat16* down_t, cudaStream_t s);
+cudaError_t launch_pad_rows(const __nv_bfloat16* src, int64_t rows,
+                            int64_t cols, int64_t ld_src, __nv_bfloat16* dst,
+                            int64_t ld_dst, cudaStream_t s);
+cudaError_t launch_silu_mul(const __nv_bfloat16* gate, int64_t ld_gate,
+                            const __nv_bfloat16* up, int64_t ld_up,
+                            __nv_bfloat16* out, int64_t rows, int64_t cols,
+                            cudaStream_t s);
+cudaError_t launch_silu(const __nv_bfloat16* in, __nv_bfloat16* out,
+                        int64_t n, cudaStream_t s);
+cudaError_t launch_mul(const __nv_bfloat16* a, const __nv_bfloat16* b,
+                       __nv_bfloat16* out, int64_t n, cudaStream_t s);
+cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* p, int64_t n,
+                                     uint64_t seed, float lo, float hi,
+                                     cudaStream_t s);
+cudaError_t launch_flush(void* p, size_t bytes, cudaStream_t s);
+cudaError_t launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n,
+                               cudaStream_t s);
+
+// api.cu helpers used by the scheduler / TP translation units.
+int resolve_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
+                   const dfk_config* in, dfk_config* out);
+void default_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
+                    dfk_config* out);
+int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
+                 int64_t B, void* y, int y_dtype, const dfk_config* cfg);
+int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s);
+std::string config_label(const dfk_config& c);
+
+}  // namespace dfk

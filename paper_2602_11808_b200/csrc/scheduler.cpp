@@ -1,0 +1,451 @@
+// scheduler.cpp — the profile-driven kernel scheduler (paper §3.3; the
+// reference's tuner, /root/reference/proj/src/tuner.cpp), re-done for the
+// GPU: candidates are (kernel family, pipeline depth, CTA count, PDL) per
+// stage plus the unfused cuBLASLt layouts; timing is CUDA events on the
+// context stream; the correctness gate compares against the two-kernel
+// cuBLASLt output at the bf16 tolerance; selection and the JSON cache keep
+// the reference's semantics:
+//   candidate grid, labels unique           tuner.cpp:59-88
+//   gate run, warmup >= 1, runs >= 3        tuner.cpp:106-162
+//   lower median                            tuner.cpp:32-35
+//   select: (median, fusion pref, label)    tuner.cpp:170-190, 23-30
+//   all disqualified -> error               tuner.cpp:185-188
+//   cache format_version 1, flock, replace  tuner.cpp:196-390
+//   get_or_tune (hit skips profiling)       tuner.cpp:408-424
+// One "run" is the mean of kRepsPerRun back-to-back calls (a single µs-scale
+// launch is below event resolution); samples are stored in ns per call.
+#include <cuda_runtime.h>
+#include <sys/file.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <ctime>
+#include <filesystem>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <json.hpp>
+
+#include "internal.h"
+
+using namespace dfk;
+using nlohmann::json;
+
+namespace {
+
+constexpr int kCacheFormatVersion = 1;
+constexpr double kGateTolerance = 1e-2;  // max|dY| / max|Y_ref|, bf16 path
+constexpr int kRepsPerRun = 8;
+
+struct Result {
+  std::string label;
+  dfk_config cfg;
+  std::vector<int64_t> samples_ns;
+  int64_t median_ns = 0;
+  int warmup_runs = 0;
+  int measured_runs = 0;
+  bool disqualified = false;
+  std::string reason;
+  double gate_error = 0.0;
+};
+
+int variant_preference(int v) {
+  return v == DFK_VARIANT_FUSED ? 0 : v == DFK_VARIANT_TWO_KERNEL ? 1 : 2;
+}
+
+int64_t lower_median(std::vector<int64_t> s) {
+  std::sort(s.begin(), s.end());
+  return s[(s.size() - 1) / 2];
+}
+
+std::string now_iso8601() {
+  const std::time_t now =
+      std::chrono::system_clock::to_time_t(std::chrono::system_clock::now());
+  std::tm tm_utc{};
+  gmtime_r(&now, &tm_utc);
+  char buf[32];
+  std::strftime(buf, sizeof(buf), "%Y-%m-%dT%H:%M:%SZ", &tm_utc);
+  return buf;
+}
+
+dfk_config make_cfg(int variant, int s1f, int s1st, int dnf, int dnst,
+                    int pdl) {
+  dfk_config c;
+  std::memset(&c, 0, sizeof(c));
+  c.variant = variant;
+  c.s1_family = s1f;
+  c.s1_stages = s1st;
+  c.s1_split_k = 1;
+  c.down_family = dnf;
+  c.down_stages = dnst;
+  c.pdl = pdl;
+  std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+  return c;
+}
+
+std::vector<dfk_config> candidates(int64_t B) {
+  std::vector<dfk_config> out;
+  out.push_back(make_cfg(DFK_VARIANT_FOUR_KERNEL, 0, 0, 0, 0, 0));
+  out.push_back(make_cfg(DFK_VARIANT_TWO_KERNEL, 0, 0, 0, 0, 0));
+  std::vector<int> fams = {DFK_FAMILY_TC};
+  if (B <= 8) fams.push_back(DFK_FAMILY_GEMV);
+  std::set<std::string> seen;
+  for (int s1f : fams)
+    for (int dnf : fams)
+      for (int st : {0, 4})
+        for (int pdl : {1, 0}) {
+          if (pdl == 0 && st != 0) continue;  // keep the grid small
+          dfk_config c = make_cfg(DFK_VARIANT_FUSED, s1f, st, dnf, st, pdl);
+          if (seen.insert(c.label).second) out.push_back(c);
+        }
+  return out;
+}
+
+json cfg_to_json(const dfk_config& c) {
+  return json{{"variant", c.variant},         {"s1_family", c.s1_family},
+              {"s1_stages", c.s1_stages},     {"s1_ctas", c.s1_ctas},
+              {"s1_split_k", c.s1_split_k},   {"down_family", c.down_family},
+              {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
+              {"pdl", c.pdl},                 {"label", std::string(c.label)}};
+}
+
+template <typename T>
+T get_field(const json& j, const char* f) {
+  if (!j.contains(f))
+    throw std::runtime_error(std::string("cache entry missing field '") + f + "'");
+  try {
+    return j.at(f).get<T>();
+  } catch (const json::exception& e) {
+    throw std::runtime_error(std::string("cache field '") + f +
+                             "' has the wrong type: " + e.what());
+  }
+}
+
+dfk_config cfg_from_json(const json& j) {
+  dfk_config c;
+  std::memset(&c, 0, sizeof(c));
+  c.variant = get_field<int>(j, "variant");
+  c.s1_family = get_field<int>(j, "s1_family");
+  c.s1_stages = get_field<int>(j, "s1_stages");
+  c.s1_ctas = get_field<int>(j, "s1_ctas");
+  c.s1_split_k = get_field<int>(j, "s1_split_k");
+  c.down_family = get_field<int>(j, "down_family");
+  c.down_stages = get_field<int>(j, "down_stages");
+  c.down_ctas = get_field<int>(j, "down_ctas");
+  c.pdl = get_field<int>(j, "pdl");
+  std::snprintf(c.label, sizeof(c.label), "%s",
+                get_field<std::string>(j, "label").c_str());
+  return c;
+}
+
+json entry_json(int64_t B, int64_t dm, int64_t df, const std::string& fp,
+                const Result& chosen, const std::vector<Result>& all) {
+  json results = json::array();
+  for (const Result& r : all) {
+    json j{{"label", r.label},
+           {"variant", r.cfg.variant == DFK_VARIANT_FUSED        ? "fused"
+                       : r.cfg.variant == DFK_VARIANT_TWO_KERNEL ? "two_kernel"
+                                                                 : "four_kernel"},
+           {"samples_ns", r.samples_ns},
+           {"median_ns", r.median_ns},
+           {"warmup_runs", r.warmup_runs},
+           {"measured_runs", r.measured_runs},
+           {"gate_error", r.gate_error},
+           {"config", cfg_to_json(r.cfg)}};
+    if (r.disqualified) j["disqualified"] = r.reason;
+    results.push_back(j);
+  }
+  return json{{"shape", {{"batch", B}, {"d_model", dm}, {"d_ff", df}}},
+              {"fingerprint", fp},
+              {"chosen", chosen.label},
+              {"chosen_config", cfg_to_json(chosen.cfg)},
+              {"created_at", now_iso8601()},
+              {"results", results}};
+}
+
+// Stream + flock released together (tuner.cpp:270-288 semantics).
+class LockedFile {
+ public:
+  LockedFile(const std::string& path, const char* mode, int op)
+      : f_(std::fopen(path.c_str(), mode)) {
+    if (f_) flock(fileno(f_), op);
+  }
+  ~LockedFile() {
+    if (f_) std::fclose(f_);
+  }
+  std::FILE* get() const { return f_; }
+  explicit operator bool() const { return f_ != nullptr; }
+
+ private:
+  std::FILE* f_;
+};
+
+std::string read_all(std::FILE* f) {
+  std::string text;
+  char buf[4096];
+  size_t got;
+  std::fseek(f, 0, SEEK_SET);
+  while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) text.append(buf, got);
+  return text;
+}
+
+json parse_cache(const std::string& text, const std::string& path) {
+  json doc;
+  try {
+    doc = json::parse(text);
+  } catch (const json::parse_error& e) {
+    throw std::runtime_error("cache file " + path + " is corrupt: " + e.what());
+  }
+  const int v = get_field<int>(doc, "format_version");
+  if (v != kCacheFormatVersion)
+    throw std::runtime_error("cache file " + path + " has format version " +
+                             std::to_string(v) + "; this build reads version " +
+                             std::to_string(kCacheFormatVersion));
+  return doc;
+}
+
+bool key_matches(const json& e, int64_t B, int64_t dm, int64_t df,
+                 const std::string& fp) {
+  const json s = get_field<json>(e, "shape");
+  return get_field<int64_t>(s, "batch") == B &&
+         get_field<int64_t>(s, "d_model") == dm &&
+         get_field<int64_t>(s, "d_ff") == df &&
+         get_field<std::string>(e, "fingerprint") == fp;
+}
+
+bool cache_lookup(const std::string& path, int64_t B, int64_t dm, int64_t df,
+                  const std::string& fp, json* hit) {
+  std::string text;
+  {
+    LockedFile f(path, "r", LOCK_SH);
+    if (!f) return false;
+    text = read_all(f.get());
+  }
+  if (text.empty()) return false;
+  const json doc = parse_cache(text, path);
+  for (const json& e : get_field<json>(doc, "entries")) {
+    if (key_matches(e, B, dm, df, fp)) {
+      *hit = e;
+      return true;
+    }
+  }
+  return false;
+}
+
+void cache_store(const std::string& path, const json& entry, int64_t B,
+                 int64_t dm, int64_t df, const std::string& fp) {
+  std::filesystem::path p(path);
+  if (p.has_parent_path()) std::filesystem::create_directories(p.parent_path());
+  LockedFile f(path, "a+", LOCK_EX);
+  if (!f) throw std::runtime_error("cache file " + path + " is not writable");
+  const std::string text = read_all(f.get());
+  json doc = text.empty() ? json{{"format_version", kCacheFormatVersion},
+                                 {"entries", json::array()}}
+                          : parse_cache(text, path);
+  json& entries = doc["entries"];
+  bool replaced = false;
+  for (json& e : entries) {
+    if (key_matches(e, B, dm, df, fp)) {
+      e = entry;
+      replaced = true;
+      break;
+    }
+  }
+  if (!replaced) entries.push_back(entry);
+  const std::string out = doc.dump(2) + "\n";
+  std::fseek(f.get(), 0, SEEK_SET);
+  if (ftruncate(fileno(f.get()), 0) != 0)
+    throw std::runtime_error("cache file " + path + ": truncate failed");
+  if (std::fwrite(out.data(), 1, out.size(), f.get()) != out.size() ||
+      std::fflush(f.get()) != 0)
+    throw std::runtime_error("cache file " + path + ": write failed");
+}
+
+// max|a-b| / max|b| over n floats.
+double rel_inf_error(const std::vector<float>& a, const std::vector<float>& b) {
+  double num = 0.0, den = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    const double d = std::fabs(static_cast<double>(a[i]) - b[i]);
+    if (!(d <= num)) num = std::isnan(d) ? INFINITY : std::max(num, d);
+    den = std::max(den, std::fabs(static_cast<double>(b[i])));
+  }
+  return den > 0 ? num / den : num;
+}
+
+void write_json(const json& j, char* buf, size_t len) {
+  if (!buf || len == 0) return;
+  const std::string s = j.dump();
+  std::snprintf(buf, len, "%s", s.c_str());
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
+                   dfk_config* out, int32_t cap, int32_t* n) {
+  if (!ctx || !w || !n) return fail(DFK_ERR_INVALID, "null argument");
+  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
+  const auto c = candidates(batch);
+  *n = static_cast<int32_t>(c.size());
+  for (int32_t i = 0; i < std::min<int32_t>(cap, *n); ++i) out[i] = c[i];
+  return DFK_OK;
+}
+
+int dfk_select_config(dfk_context ctx, dfk_weights w, int64_t batch,
+                      dfk_config* out) {
+  if (!ctx || !w || !out) return fail(DFK_ERR_INVALID, "null argument");
+  return resolve_config(ctx, w, batch, nullptr, out);
+}
+
+int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
+             const char* cache_path, int32_t warmup, int32_t runs,
+             dfk_config* chosen, int32_t* from_cache, char* results_json,
+             size_t results_len) {
+  if (!ctx || !w) return fail(DFK_ERR_INVALID, "null handle");
+  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
+  if (warmup < 1) return fail(DFK_ERR_INVALID, "profile: warmup must be >= 1");
+  if (runs < 3) return fail(DFK_ERR_INVALID, "profile: runs must be >= 3");
+  if (from_cache) *from_cache = 0;
+  int64_t dm = w->d_model, df = w->d_ff;
+  char fpbuf[256];
+  dfk_fingerprint(ctx, fpbuf, sizeof(fpbuf));
+  const std::string fp = fpbuf;
+  const std::string path = cache_path ? cache_path : "";
+  const auto key = std::make_tuple(batch, dm, df);
+
+  try {
+    if (!path.empty()) {
+      json hit;
+      if (cache_lookup(path, batch, dm, df, fp, &hit)) {
+        const dfk_config c = cfg_from_json(get_field<json>(hit, "chosen_config"));
+        {
+          std::lock_guard<std::mutex> lk(ctx->mu);
+          ctx->chosen[key] = c;
+        }
+        if (chosen) *chosen = c;
+        if (from_cache) *from_cache = 1;
+        write_json(hit, results_json, results_len);
+        return DFK_OK;
+      }
+    }
+  } catch (const std::exception& e) {
+    return fail(DFK_ERR_CACHE, e.what());
+  }
+
+  // Seeded input, identical across candidates (tuner.cpp:117-120).
+  cudaSetDevice(ctx->device);
+  void *x = nullptr, *y = nullptr, *yref = nullptr;
+  const size_t xb = static_cast<size_t>(batch * dm) * 2;
+  const size_t yb = static_cast<size_t>(batch * dm) * 4;
+  if (cudaMalloc(&x, xb) != cudaSuccess || cudaMalloc(&y, yb) != cudaSuccess ||
+      cudaMalloc(&yref, yb) != cudaSuccess) {
+    cudaFree(x);
+    cudaFree(y);
+    return fail(DFK_ERR_NOMEM, "tune buffers");
+  }
+  auto cleanup = [&] {
+    cudaFree(x);
+    cudaFree(y);
+    cudaFree(yref);
+  };
+  dfk_fill_uniform_bf16(ctx, x, batch * dm, 0, -1.f, 1.f);
+  const dfk_config refcfg = make_cfg(DFK_VARIANT_TWO_KERNEL, 0, 0, 0, 0, 0);
+  int st = forward_impl(ctx, w, x, batch, yref, DFK_F32, &refcfg);
+  if (st != DFK_OK) {
+    cleanup();
+    return st;
+  }
+  std::vector<float> href(static_cast<size_t>(batch * dm)),
+      hy(static_cast<size_t>(batch * dm));
+  cudaMemcpyAsync(href.data(), yref, yb, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  std::vector<Result> results;
+  for (const dfk_config& c : candidates(batch)) {
+    Result r;
+    r.cfg = c;
+    r.label = c.label;
+    r.warmup_runs = warmup;
+    cudaMemsetAsync(y, 0xFF, yb, ctx->stream);  // NaN-fill: stale data fails
+    st = forward_impl(ctx, w, x, batch, y, DFK_F32, &c);
+    cudaError_t ce = cudaStreamSynchronize(ctx->stream);
+    if (st != DFK_OK || ce != cudaSuccess) {
+      r.disqualified = true;
+      r.reason = st != DFK_OK ? std::string("launch failed: ") + dfk_last_error()
+                              : std::string("CUDA error: ") + cudaGetErrorString(ce);
+      results.push_back(r);
+      if (ce != cudaSuccess) break;  // sticky error: stop profiling
+      continue;
+    }
+    cudaMemcpy(hy.data(), y, yb, cudaMemcpyDeviceToHost);
+    r.gate_error = rel_inf_error(hy, href);
+    if (!(r.gate_error <= kGateTolerance)) {
+      std::ostringstream o;
+      o << "output deviates from the two-kernel reference by " << r.gate_error
+        << " (gate " << kGateTolerance << ")";
+      r.disqualified = true;
+      r.reason = o.str();
+      results.push_back(r);
+      continue;
+    }
+    for (int i = 0; i < warmup; ++i)
+      forward_impl(ctx, w, x, batch, y, DFK_F32, &c);
+    for (int i = 0; i < runs; ++i) {
+      cudaEventRecord(e0, ctx->stream);
+      for (int k = 0; k < kRepsPerRun; ++k)
+        forward_impl(ctx, w, x, batch, y, DFK_F32, &c);
+      cudaEventRecord(e1, ctx->stream);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      r.samples_ns.push_back(
+          static_cast<int64_t>(std::llround(ms * 1e6 / kRepsPerRun)));
+    }
+    r.measured_runs = runs;
+    r.median_ns = lower_median(r.samples_ns);
+    results.push_back(r);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cleanup();
+
+  const Result* best = nullptr;
+  for (const Result& r : results) {
+    if (r.disqualified) continue;
+    auto k = [](const Result& q) {
+      return std::make_tuple(q.median_ns, variant_preference(q.cfg.variant),
+                             q.label);
+    };
+    if (!best || k(r) < k(*best)) best = &r;
+  }
+  if (!best)
+    return fail(DFK_ERR_GATE,
+                "select: every candidate was disqualified by the correctness gate");
+  const json entry = entry_json(batch, dm, df, fp, *best, results);
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->chosen[key] = best->cfg;
+  }
+  if (chosen) *chosen = best->cfg;
+  write_json(entry, results_json, results_len);
+  if (!path.empty()) {
+    try {
+      cache_store(path, entry, batch, dm, df, fp);
+    } catch (const std::exception& e) {
+      return fail(DFK_ERR_CACHE, e.what());
+    }
+  }
+  return DFK_OK;
+}
+
+}  // extern "C"

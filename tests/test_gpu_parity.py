@@ -1,0 +1,327 @@
+"""GPU parity tests: the sm_100a kernels (through the C ABI) vs the oracle.
+
+Tolerance (north star): bf16 inputs, fp32 accumulation, A2 stored in bf16;
+the gate is the infinity-norm relative error
+    max|Y_gpu - Y_ref| / max|Y_ref| <= 1e-2
+against the fp64 oracle run on the SAME bf16-exact inputs.  A2 is checked the
+same way.  Integer-exact properties (zero in -> zero out, config invariance
+of stage 1, workspace self-cleaning) are checked bit-exactly.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    den = np.abs(ref).max()
+    return float(np.abs(got - ref).max() / (den if den > 0 else 1.0))
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2602_11808_b200 import runtime
+    return runtime
+
+
+@pytest.fixture(scope="module")
+def ctx(rt):
+    c = rt.Context(0)
+    yield c
+    c.close()
+
+
+def configs(rt, B):
+    out = {
+        "fused_tc": rt.Config.make(s1_family=rt.FAMILY_TC, down_family=rt.FAMILY_TC),
+        "fused_tc_nopdl": rt.Config.make(pdl=0),
+        "two_kernel": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
+        "four_kernel": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
+    }
+    if B <= 8:
+        out["fused_gemv"] = rt.Config.make(s1_family=rt.FAMILY_GEMV,
+                                           down_family=rt.FAMILY_GEMV)
+        out["fused_gemv_tc"] = rt.Config.make(s1_family=rt.FAMILY_GEMV,
+                                              down_family=rt.FAMILY_TC)
+    return out
+
+
+def instance(oracle_lib, seed, B, dm, df, scale=None):
+    scale = scale if scale is not None else 1.0 / np.sqrt(dm)
+    x, wu, wg, wd = oracle_lib.make_instance(seed, B, dm, df, scale)
+    return tuple(oracle_lib.quantize_bf16(a)[0] for a in (x, wu, wg, wd))
+
+
+def run_gpu(rt, ctx, w, x, cfg, y_dtype=None):
+    B, dm = x.shape
+    xd = ctx.array((B, dm)).upload(x)
+    a2 = ctx.array((B, w.d_ff))
+    y = ctx.array((B, dm), y_dtype if y_dtype is not None else rt.F32)
+    ctx.stage1(w, xd, a2, cfg=cfg)
+    ctx.down(w, a2, y, cfg=cfg)
+    a2h = a2.download()
+    y1 = y.download()
+    yf = ctx.array((B, dm), rt.F32)
+    ctx.forward(w, xd, yf, cfg=cfg)
+    return a2h, y1, yf.download()
+
+
+# --- golden vectors ----------------------------------------------------------------
+def test_golden_vectors(rt, ctx, oracle_lib, golden):
+    for name in golden["names"]:
+        name = str(name)
+        seed, B, dm, df, q = (int(v) for v in golden[f"{name}/meta"])
+        scale = float(golden[f"{name}/scale"][0])
+        x, wu, wg, wd = oracle_lib.make_instance(seed, B, dm, df, scale)
+        xq, wuq, wgq, wdq = (oracle_lib.quantize_bf16(a)[0] for a in (x, wu, wg, wd))
+        if q:
+            a2_ref, y_ref = golden[f"{name}/a2"], golden[f"{name}/y"]
+        else:  # fp64 golden case: the oracle (pinned to it) on the bf16 inputs
+            a2_ref, y_ref = oracle_lib.forward(xq, wuq, wgq, wdq)
+        w = ctx.weights(wg, wu, wd)  # fp64 in, rounded to bf16 on device
+        for label, cfg in configs(rt, B).items():
+            a2, y1, y2 = run_gpu(rt, ctx, w, xq, cfg)
+            assert rel_err(a2, a2_ref) <= TOL, (name, label, "a2")
+            assert rel_err(y1, y_ref) <= TOL, (name, label, "y")
+            assert rel_err(y2, y_ref) <= TOL, (name, label, "y fwd")
+
+
+def test_scalar_known_answer(rt, ctx):
+    """x=2, W_up=3, W_gate=1, W_down=1 -> 6*silu(2) = 10.5696; with A2 in
+    bf16 the GPU gives 10.5625."""
+    one = np.ones((1, 1))
+    w = ctx.weights(one, 3 * one, one)
+    for label, cfg in configs(rt, 1).items():
+        y = ctx.forward_host(w, 2 * one, cfg=cfg)
+        assert abs(y[0, 0] - 10.5696) / 10.5696 < 2e-3, (label, y)
+
+
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 5, 8, 13, 16, 17, 32, 33, 64, 100])
+def test_batch_sweep_medium_shape(rt, ctx, oracle_lib, B):
+    dm, df = 512, 1536
+    x, wu, wg, wd = instance(oracle_lib, 100 + B, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    for label, cfg in configs(rt, B).items():
+        a2, y1, y2 = run_gpu(rt, ctx, w, x, cfg)
+        assert rel_err(a2, a2_ref) <= TOL, (B, label)
+        assert rel_err(y1, y_ref) <= TOL, (B, label)
+        assert rel_err(y2, y_ref) <= TOL, (B, label)
+
+
+@pytest.mark.parametrize("B,dm,df", [(1, 1, 1), (3, 5, 7), (5, 7, 11), (2, 4, 7),
+                                     (5, 13, 17), (3, 200, 300), (4, 72, 130),
+                                     (7, 1000, 3000), (2, 4096, 64), (1, 64, 4096)])
+def test_ragged_and_tiny_shapes(rt, ctx, oracle_lib, B, dm, df):
+    """No dimension a multiple of the tile (edge tiles, fused.cpp:74-168) and
+    unaligned d_model / d_ff (TMA padding path)."""
+    x, wu, wg, wd = instance(oracle_lib, B * 7 + dm, B, dm, df, 1.0)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    for label, cfg in configs(rt, B).items():
+        a2, y1, y2 = run_gpu(rt, ctx, w, x, cfg)
+        assert rel_err(a2, a2_ref) <= TOL, (label, "a2")
+        assert rel_err(y1, y_ref) <= TOL, (label, "y")
+        assert rel_err(y2, y_ref) <= TOL, (label, "y fwd")
+
+
+def test_zero_input_gives_exact_zero(rt, ctx, oracle_lib):
+    x, wu, wg, wd = instance(oracle_lib, 9, 4, 256, 448)
+    w = ctx.weights(wg, wu, wd)
+    for label, cfg in configs(rt, 4).items():
+        a2, y1, y2 = run_gpu(rt, ctx, w, np.zeros_like(x), cfg)
+        assert not a2.any() and not y1.any() and not y2.any(), label
+
+
+def test_zero_gate_switches_everything_off(rt, ctx, oracle_lib):
+    x, wu, wg, wd = instance(oracle_lib, 10, 3, 128, 192)
+    w = ctx.weights(np.zeros_like(wg), wu, wd)
+    for label, cfg in configs(rt, 3).items():
+        a2, y1, _ = run_gpu(rt, ctx, w, x, cfg)
+        assert not a2.any() and not y1.any(), label
+
+
+def test_stage1_bitwise_invariant_across_launch_configs(rt, ctx, oracle_lib):
+    """Stage 1 reduces each tile's full K inside one CTA, so A2 is
+    bit-identical for every pipeline depth / CTA count (the GPU form of
+    the reference's worker-count independence, test_fused.cpp:208-227)."""
+    B, dm, df = 8, 1024, 2048
+    x, wu, wg, wd = instance(oracle_lib, 11, B, dm, df)
+    w = ctx.weights(wg, wu, wd)
+    xd = ctx.array((B, dm)).upload(x)
+    outs = []
+    for fam in (rt.FAMILY_TC, rt.FAMILY_GEMV):
+        base = None
+        for stages in (2, 3, 5, 0):
+            for ctas in (1, 7, 148, 0):
+                a2 = ctx.array((B, df))
+                ctx.stage1(w, xd, a2, cfg=rt.Config.make(s1_family=fam, s1_stages=stages,
+                                                         s1_ctas=ctas))
+                bits = a2.download_bits()
+                if base is None:
+                    base = bits
+                assert np.array_equal(bits, base), (fam, stages, ctas)
+        outs.append(base)
+    a2_ref, _ = oracle_lib.forward(x, wu, wg, wd)
+    for bits in outs:
+        from paper_2602_11808_b200.runtime import bf16_bits_to_f32
+        assert rel_err(bf16_bits_to_f32(bits), a2_ref) <= TOL
+
+
+def test_down_workspace_self_cleans(rt, ctx, oracle_lib):
+    """The stream-K down kernel's fp32 workspace and tile counters are
+    re-zeroed by the finalising CTA: repeated calls with different grids and
+    batches agree with the oracle every time."""
+    dm, df = 640, 1280
+    x, wu, wg, wd = instance(oracle_lib, 12, 16, dm, df)
+    w = ctx.weights(wg, wu, wd)
+    for B in (16, 3, 16, 1, 9):
+        a2_ref, y_ref = oracle_lib.forward(x[:B], wu, wg, wd)
+        for ctas in (0, 5, 148, 333):
+            for fam in ((rt.FAMILY_TC, rt.FAMILY_GEMV) if B <= 8 else (rt.FAMILY_TC,)):
+                cfg = rt.Config.make(down_family=fam, down_ctas=ctas)
+                _, y1, y2 = run_gpu(rt, ctx, w, x[:B], cfg)
+                assert rel_err(y1, y_ref) <= TOL, (B, ctas, fam)
+                assert rel_err(y2, y_ref) <= TOL, (B, ctas, fam)
+
+
+def test_bf16_output_and_layer_chain(rt, ctx, oracle_lib):
+    """Multi-layer decode loop (bench.cpp:98-115): x <- Y (bf16) through 4
+    layers, vs the oracle chain fed the same bf16-rounded activations."""
+    B, dm, df, L = 4, 512, 1792, 4
+    layers = [instance(oracle_lib, 50 + l, B, dm, df)[1:] for l in range(L)]
+    x0 = instance(oracle_lib, 49, B, dm, df)[0]
+    ws = [ctx.weights(wg, wu, wd) for (wu, wg, wd) in layers]
+    bufs = [ctx.array((B, dm)).upload(x0), ctx.array((B, dm))]
+    for l, w in enumerate(ws):
+        ctx.forward(w, bufs[l % 2], bufs[(l + 1) % 2])
+    y_gpu = bufs[L % 2].download()
+    xr = x0
+    for (wu, wg, wd) in layers:
+        _, yr = oracle_lib.forward(xr, wu, wg, wd)
+        xr = oracle_lib.quantize_bf16(yr)[0]
+    assert rel_err(y_gpu, xr) <= 2 * TOL
+
+
+def test_forward_host_matches_device_path(rt, ctx, oracle_lib):
+    x, wu, wg, wd = instance(oracle_lib, 13, 6, 384, 1024)
+    w = ctx.weights(wg, wu, wd)
+    y_host = ctx.forward_host(w, x)
+    xd = ctx.array(x.shape).upload(x)
+    yd = ctx.array(x.shape, rt.F32)
+    ctx.forward(w, xd, yd)
+    assert np.array_equal(y_host.astype(np.float32), yd.download()) or \
+        rel_err(y_host, yd.download()) <= 1e-6
+
+
+def test_tp_shards_reconstruct_full_block(rt, ctx, oracle_lib):
+    """Compound TP scheme on one GPU: per-shard prepacked weights
+    (ff_begin/ff_end), fp32 partial Y, sum in device order == full block
+    (test_tp.cpp:74-112); stage-1 shards concatenate to the full A2."""
+    B, dm, df = 3, 256, 700
+    x, wu, wg, wd = instance(oracle_lib, 14, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    xd = ctx.array((B, dm)).upload(x)
+    for P in (1, 2, 3, 4, 8):
+        parts, shards = [], []
+        for p in range(P):
+            b, e = rt.balanced_range(df, P, p)
+            w = ctx.weights(wg, wu, wd, ff_range=(b, e))
+            a2 = ctx.array((B, e - b))
+            y = ctx.array((B, dm), rt.F32)
+            ctx.stage1(w, xd, a2)
+            ctx.down(w, a2, y)
+            shards.append(a2.download())
+            parts.append(y.download().astype(np.float64))
+        y_tp = oracle_lib.allreduce_in_order(np.stack(parts))
+        assert rel_err(y_tp, y_ref) <= TOL, P
+        assert rel_err(np.concatenate(shards, axis=1), a2_ref) <= TOL, P
+
+
+def test_error_classes(rt, ctx, oracle_lib):
+    x, wu, wg, wd = instance(oracle_lib, 15, 2, 64, 128)
+    with pytest.raises(rt.ShapeError):
+        ctx.weights(wg, wu, wd, ff_range=(100, 100))
+    w = ctx.weights(wg, wu, wd)
+    xd = ctx.array((2, 64)).upload(x)
+    a2 = ctx.array((2, 128))
+    with pytest.raises(rt.ShapeError):
+        ctx.stage1(w, xd, a2, batch=-1)
+    with pytest.raises(rt.InvalidArgument):
+        ctx.stage1(w, xd, a2, cfg=rt.Config.make(variant=7))
+
+
+def test_mirror_api_reads_like_reference(rt, oracle_lib):
+    """The deepfusion mirror: run_fused / run_variant / run_tp_mlp with the
+    reference's argument meaning."""
+    from paper_2602_11808_b200 import deepfusion as dfm
+    x, wu, wg, wd = instance(oracle_lib, 16, 3, 96, 320, 0.2)
+    _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = dfm.MlpWeights(wu, wg, wd, dfm.MlpShape(3, 96, 320))
+    assert rel_err(dfm.run_fused(x, w, dfm.TileConfig(1, 32, 32)), y_ref) <= TOL
+    for v in dfm.VariantTag:
+        assert rel_err(dfm.run_variant(dfm.KernelConfig(v), x, w), y_ref) <= TOL, v
+    a2 = np.zeros((3, 320))
+    dfm.run_fused_stage1(x, wu, wg, dfm.TileConfig(3, 320, 96), a2)
+    assert rel_err(dfm.down_projection(a2, wd), y_ref) <= TOL
+    r = dfm.run_tp_mlp(x, w, dfm.make_plan(320, 3), dfm.KernelConfig())
+    assert rel_err(r.output, y_ref) <= TOL
+    assert len(r.log.events) == 1 and r.log.events[0].payload_elements_per_device == 3 * 96
+    with pytest.raises(dfm.ShapeError):
+        dfm.run_fused_stage1(x, wu, wg, dfm.TileConfig(0, 1, 1), a2)
+    with pytest.raises(dfm.ShapeError):
+        dfm.down_projection(a2, wd[:5])
+
+
+def test_scheduler_gate_select_and_cache(rt, ctx, oracle_lib, tmp_path):
+    x, wu, wg, wd = instance(oracle_lib, 17, 4, 512, 1024)
+    w = ctx.weights(wg, wu, wd)
+    path = str(tmp_path / "cache.json")
+    cfg, hit, entry = ctx.tune(w, 4, path, warmup=1, runs=3)
+    assert not hit
+    assert entry["chosen"] == cfg.label.decode()
+    labels = [r["label"] for r in entry["results"]]
+    assert len(labels) == len(set(labels)) >= 6
+    for r in entry["results"]:
+        assert "disqualified" not in r, r
+        assert r["median_ns"] == sorted(r["samples_ns"])[(len(r["samples_ns"]) - 1) // 2]
+    best = min(entry["results"], key=lambda r: (r["median_ns"],
+                                                 0 if r["variant"] == "fused" else
+                                                 1 if r["variant"] == "two_kernel" else 2,
+                                                 r["label"]))
+    assert best["label"] == entry["chosen"]
+    import json
+    doc = json.load(open(path))
+    assert doc["format_version"] == 1 and len(doc["entries"]) == 1
+    cfg2, hit2, _ = ctx.tune(w, 4, path)
+    assert hit2 and cfg2.label == cfg.label
+    # a NULL-config call now uses the tuned choice
+    assert ctx.select_config(w, 4).label == cfg.label
+    open(path, "w").write("{not json")
+    with pytest.raises(rt.CacheError):
+        ctx.tune(w, 4, path)
+    json.dump({"format_version": 2, "entries": []}, open(path, "w"))
+    with pytest.raises(rt.CacheError):
+        ctx.tune(w, 4, path)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("B", [1, 16])
+def test_llama8b_full_shape_parity(rt, ctx, oracle_lib, B):
+    """Config 1/2: Llama-3.1-8B MLP, d_model=4096,
+    d_ff=14336, seed 20260809, vs the fp64 oracle on identical bf16 inputs."""
+    dm, df = 4096, 14336
+    x, wu, wg, wd = instance(oracle_lib, 20260809, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    for label, cfg in configs(rt, B).items():
+        a2, y1, y2 = run_gpu(rt, ctx, w, x, cfg)
+        assert rel_err(a2, a2_ref) <= TOL, (label, rel_err(a2, a2_ref))
+        assert rel_err(y1, y_ref) <= TOL, (label, rel_err(y1, y_ref))
+        assert rel_err(y2, y_ref) <= TOL, (label, rel_err(y2, y_ref))
