@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the fused SwiGLU-MLP decode path (BASELINE.json metric:
+"SwiGLU-MLP decode µs/call & achieved HBM GB/s vs ~8 TB/s roofline, batch
+1-64").
+
+Workload (configs[1]): Llama-3.1-8B MLP (d_model=4096, d_ff=14336), batch
+sweep B in {1,2,4,8,16,32,64} on one B200, scheduler-selected kernels.  A
+"step" is one fused block call at every B of the sweep (7 calls), each on the
+next of R rotating weight sets (every set is 352 MB >> 126 MB L2, so no call
+finds its weights in L2).  Synthetic bf16 data (uniform, device-generated).
+
+value      = algorithmic bytes of all calls / device time (GB/s, aggregate
+             over ranks); bytes per call follow the reference's fused traffic
+             model (traffic.cpp:70-76, 82-94) at 2 B/element.
+e2e        = the same metric through the host-buffer C-ABI call
+             (dfk_forward_host: bf16 H2D of X, forward, fp32 D2H of Y).
+roofline   = the fused stage-1 kernel (2/3 of the bytes) timed alone with
+             CUDA events on its stream, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline = the reference CPU path (oracle/_ref, the unmodified reference
+             compiled in place) on a bounded sample.
+
+N>1 (torchrun): tensor parallel over NCCL, one rank per GPU — every rank holds
+the balanced_ranges(d_ff, N) shard and the block ends in one ncclAllReduce.
+
+--impl reference: the reference's own CPU implementation of the path
+(oracle/_ref/libdeepfusion_ref.so: run_fused with a single covering
+column-major tile and all host threads) on rank 0, same metric/unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DM, DF = 4096, 14336
+SWEEP = [1, 2, 4, 8, 16, 32, 64]
+METRIC = "SwiGLU-MLP decode µs/call & achieved HBM GB/s vs ~8 TB/s roofline, batch 1–64"
+WORKLOAD = "Llama-3.1-8B MLP (d_model=4096, d_ff=14336) decode batch sweep 1/2/4/8/16/32/64"
+
+
+def block_bytes(B, dm, df, P=1):
+    """Per-GPU algorithmic bytes of one block call at TP degree P."""
+    return 2 * (3 * dm * df // P + 2 * B * dm + 2 * B * df // P)
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --- clocks sampling ---------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --- reference CPU arm -------------------------------------------------------
+class CpuReference:
+    """The reference CPU path (oracle/_ref: the unmodified reference compiled
+    in place) on a Llama-8B-shaped fp64 instance built once."""
+
+    def __init__(self, B=1):
+        import oracle
+        o = oracle.Oracle()
+        self.B = B
+        x, wu, wg, wd = o.make_instance(0, B, DM, DF, 1.0 / np.sqrt(DM))
+        self.inst = oracle.Reference().instance(x, wu, wg, wd)
+
+    def time(self, threads=1, budget_s=12.0, min_calls=3, max_calls=50):
+        """run_fused (fused.cpp:209-216, single covering column-major tile,
+        `threads` stage-1 workers); returns (GB/s of algorithmic bytes,
+        calls, median seconds per call)."""
+        tile = (self.B, -(-DF // threads) if threads > 1 else DF, DM)
+        self.inst.run_fused(tile=tile, num_workers=threads)  # warm-up
+        times = []
+        t_start = time.perf_counter()
+        while len(times) < max_calls and (len(times) < min_calls or
+                                          time.perf_counter() - t_start < budget_s):
+            t0 = time.perf_counter()
+            self.inst.run_fused(tile=tile, num_workers=threads)
+            times.append(time.perf_counter() - t0)
+        per_call = statistics.median(times)
+        return block_bytes(self.B, DM, DF) / per_call / 1e9, len(times), per_call
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    t_all = time.perf_counter()
+    ref = CpuReference(B=1)
+    vals = []
+    for step in range(args.warmup + args.steps):
+        gbs, n, per = ref.time(threads=threads, budget_s=0.0, min_calls=1, max_calls=1)
+        if step >= args.warmup:
+            vals.append((gbs, per))
+    gbs = statistics.median(v[0] for v in vals)
+    per = statistics.median(v[1] for v in vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(per * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (mt19937_64 uniform, reference generator)",
+        "config": {"workload": WORKLOAD, "sample": "one B=1 block per step",
+                   "parallelism": f"{threads} host threads (stage 1), down single-thread"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"reference run_fused, Llama-8B B=1, {threads} stage-1 "
+                                   f"workers, one call per step"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "us_per_call": {"1": round(per * 1e6, 1)},
+        "wall_s": round(time.perf_counter() - t_all, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --- GPU arm -----------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sets", type=int, default=4, help="rotating weight sets")
+    ap.add_argument("--no-tune", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", default=",".join(map(str, SWEEP)))
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    sweep = [int(b) for b in args.sweep.split(",")]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # plumbing only: rendezvous + max-reduce
+        dist.init_process_group("gloo")
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    from paper_2602_11808_b200 import runtime as rt
+
+    P = world
+    ctx = rt.Context(local_rank)
+    if P > 1:
+        uid = [rt.Context.tp_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.tp_init(uid[0], rank, P)
+    f0, f1 = rt.balanced_range(DF, P, rank)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # Weight sets: synthetic bf16 U[-1/sqrt(dm), 1/sqrt(dm)) generated on the
+    # device in the reference layout, then prepacked (sources freed).
+    scale = 1.0 / np.sqrt(DM)
+    sets = []
+    for s in range(args.sets):
+        g = ctx.array((DM, DF)).fill_uniform(1000 * s + 1, -scale, scale)
+        u = ctx.array((DM, DF)).fill_uniform(1000 * s + 2, -scale, scale)
+        d = ctx.array((DF, DM)).fill_uniform(1000 * s + 3, -scale, scale)
+        sets.append(ctx.weights(g, u, d, ff_range=(f0, f1)))
+        del g, u, d
+    ctx.sync()
+    bmax = max(sweep)
+    xs = {B: ctx.array((B, DM)).fill_uniform(7 + B) for B in sweep}
+    ys = {B: ctx.array((B, DM), rt.F32) for B in sweep}
+
+    # Scheduler: profile once per batch size (tuner.cpp get_or_tune).
+    chosen = {}
+    if not args.no_tune:
+        for B in sweep:
+            cfg, hit, entry = ctx.tune(sets[0], B, None, 1, 4)
+            chosen[B] = cfg.label.decode()
+    cfgs = {B: ctx.select_config(sets[0], B) for B in sweep}
+
+    def call(B, i, cfg=None):
+        w = sets[i % len(sets)]
+        if P > 1:
+            ctx.tp_forward(w, xs[B], ys[B], cfg=cfg)
+        else:
+            ctx.forward(w, xs[B], ys[B], cfg=cfg)
+
+    def step(k):
+        for j, B in enumerate(sweep):
+            call(B, k * len(sweep) + j, cfgs[B])
+
+    ev0, ev1 = rt.Event(), rt.Event()
+    for k in range(args.warmup):
+        step(k)
+    ctx.sync()
+
+    # ---- headline timed region ----
+    launches0 = ctx.launch_count()
+    barrier()
+    ctx.sync()
+    with ClockSampler(local_rank) as clk:
+        ev0.record(ctx)
+        for k in range(args.steps):
+            step(k)
+        ev1.record(ctx)
+        ctx.sync()
+    barrier()
+    ms_total = max_over_ranks(ev0.elapsed_ms(ev1))
+    launches = ctx.launch_count() - launches0
+    bytes_step = sum(block_bytes(B, DM, DF, P) for B in sweep) * P
+    value = bytes_step * args.steps / (ms_total * 1e-3) / 1e9
+    ms_per_step = ms_total / args.steps
+
+    # ---- per-batch µs/call (fused, scheduler pick) and the unfused comparator ----
+    def time_calls(B, cfg, n, fn=None):
+        for i in range(2):
+            (fn or call)(B, i, cfg)
+        barrier()
+        ctx.sync()
+        ev0.record(ctx)
+        for i in range(n):
+            (fn or call)(B, i, cfg)
+        ev1.record(ctx)
+        ctx.sync()
+        return max_over_ranks(ev0.elapsed_ms(ev1)) * 1e3 / n
+
+    n_rep = max(args.steps, 10)
+    us = {B: time_calls(B, cfgs[B], n_rep) for B in sweep}
+    two = rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)
+    us_unfused = {B: time_calls(B, two, n_rep) for B in sweep}
+
+    # ---- roofline: the fused stage-1 kernel alone ----
+    a2s = {B: ctx.array((B, f1 - f0)) for B in sweep}
+
+    def s1_call(B, i, cfg):
+        ctx.stage1(sets[i % len(sets)], xs[B], a2s[B], cfg=cfg)
+
+    s1_us = {B: time_calls(B, cfgs[B], n_rep, s1_call) for B in sweep}
+    s1_bytes = {B: 2 * (B * DM + 2 * DM * (f1 - f0) + B * (f1 - f0)) for B in sweep}
+    s1_achieved = sum(s1_bytes.values()) / (sum(s1_us.values()) * 1e-6) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "stage1_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch_sweep_mean")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the host-buffer C-ABI call ----
+    hx = {B: rt.PinnedHost((B, DM), np.uint16) for B in sweep}
+    hy = {B: rt.PinnedHost((B, DM), np.float32) for B in sweep}
+    for B in sweep:
+        hx[B].arr[...] = xs[B].download_bits()
+
+    def host_call(B, i, cfg):
+        ctx.forward_host_into(sets[i % len(sets)], hx[B].arr, hy[B].arr, cfg=cfg)
+
+    for k in range(2):
+        for B in sweep:
+            host_call(B, k, cfgs[B])
+    barrier()
+    ctx.sync()
+    e2e_steps = max(3, args.steps // 2)
+    t0 = time.perf_counter()
+    ev0.record(ctx)
+    for k in range(e2e_steps):
+        for j, B in enumerate(sweep):
+            host_call(B, k * len(sweep) + j, cfgs[B])
+    ev1.record(ctx)
+    ctx.sync()
+    wall = time.perf_counter() - t0
+    e2e_ms = max_over_ranks(max(ev0.elapsed_ms(ev1), wall * 1e3))
+    e2e = bytes_step * e2e_steps / (e2e_ms * 1e-3) / 1e9
+
+    # ---- CPU baseline: reference path, rank 0, N=1 only ----
+    cpu = None
+    if rank == 0 and P == 1 and not args.no_cpu:
+        try:
+            gbs, n, per = CpuReference(B=1).time(threads=1, budget_s=12.0)
+            cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+                   "sample": f"reference run_fused as shipped (1 worker, fused.cpp:252), "
+                             f"Llama-8B B=1, fp64, median of {n} calls "
+                             f"({per * 1e3:.1f} ms/call)"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": P,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "strong" if P > 1 else "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (uniform bf16, device-generated)",
+            "config": {"workload": WORKLOAD, "batch_sweep": sweep, "d_model": DM, "d_ff": DF,
+                       "parallelism": f"tp{P}" if P > 1 else "single-gpu",
+                       "weight_sets": args.sets,
+                       "l2": "inputs larger than L2: 352 MB per weight set, "
+                             f"{args.sets} sets rotated", "kernels": "scheduler-selected"},
+            "us_per_call": {str(B): round(us[B], 2) for B in sweep},
+            "tokens_per_s": {str(B): round(B / (us[B] * 1e-6), 1) for B in sweep},
+            "gbs_per_batch": {str(B): round(block_bytes(B, DM, DF, P) * P / (us[B] * 1e-6) / 1e9, 1)
+                              for B in sweep},
+            "unfused_us_per_call": {str(B): round(us_unfused[B], 2) for B in sweep},
+            "speedup_vs_unfused": {str(B): round(us_unfused[B] / us[B], 3) for B in sweep},
+            "chosen": chosen,
+            "roofline": {"bound": "hbm", "achieved": round(s1_achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(s1_achieved / peak, 4),
+                         "traffic": traffic, "kernel": "fused stage-1 (stream_kernel<S1>)",
+                         "peak_source": peak_src,
+                         "per_batch_us": {str(B): round(s1_us[B], 2) for B in sweep}},
+            "e2e": {"value": round(e2e, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": sum(B * DM * 2 for B in sweep),
+                    "d2h_bytes_per_step": sum(B * DM * 4 for B in sweep)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    barrier()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

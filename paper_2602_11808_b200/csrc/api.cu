@@ -42,6 +42,14 @@ int fail(int status, const std::string& msg) {
   return status;
 }
 
+void free_weights(dfk_weights_s* w) {
+  cudaFree(w->s1_pack);
+  cudaFree(w->dn_pack);
+  if (w->cat_t) cudaFree(w->cat_t);
+  if (w->down_t) cudaFree(w->down_t);
+  delete w;
+}
+
 int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return DFK_OK;
@@ -552,6 +560,8 @@ int dfk_context_destroy(dfk_context ctx) {
                        &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev}) {
     if (b->p) cudaFree(b->p);
   }
+  for (dfk_weights_s* w : ctx->weights) free_weights(w);
+  ctx->weights.clear();
   if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
   if (ctx->hy_pinned) cudaFreeHost(ctx->hy_pinned);
   if (ctx->lt) cublasLtDestroy(ctx->lt);
@@ -680,17 +690,14 @@ int dfk_weights_create(dfk_context ctx, const void* w_gate, const void* w_up,
 
 int dfk_weights_destroy(dfk_weights w) {
   if (!w) return DFK_OK;
-  cudaSetDevice(w->ctx->device);
-  cudaStreamSynchronize(w->ctx->stream);
-  cudaFree(w->s1_pack);
-  cudaFree(w->dn_pack);
-  if (w->cat_t) cudaFree(w->cat_t);
-  if (w->down_t) cudaFree(w->down_t);
+  dfk_context_s* ctx = w->ctx;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
   {
-    std::lock_guard<std::mutex> lk(w->ctx->mu);
-    w->ctx->tmaps.clear();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (!ctx->weights.erase(w)) return fail(DFK_ERR_INVALID, "unknown weights handle");
   }
-  delete w;
+  free_weights(w);
   return DFK_OK;
 }
 

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -87,6 +88,9 @@ struct dfk_context_s {
   // NCCL tensor parallelism.
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+
+  // Weight handles registered on this context (freed with it).
+  std::set<dfk_weights_s*> weights;
 
   // Scheduler decisions: (batch, d_model, d_ff shard) -> config.
   std::map<std::tuple<int64_t, int64_t, int64_t>, dfk_config> chosen;

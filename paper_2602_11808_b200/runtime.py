@@ -309,9 +309,11 @@ class Weights:
         self.ff_begin, self.d_ff = int(f0), int(f1 - f0)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        # The context frees every weight set it still owns when it is closed;
+        # only destroy explicitly while it is alive.
+        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
             lib.dfk_weights_destroy(self.h)
-            self.h = None
+        self.h = None
 
     @property
     def packed_bytes(self) -> int:
