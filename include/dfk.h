@@ -104,7 +104,12 @@ typedef struct dfk_config {
   int32_t pdl;          /* 1 = programmatic dependent launch between the
                            two kernels (and across calls); 0 = plain       */
   int32_t mutant;       /* negative controls, tests only (0 = none)        */
-  int32_t reserved[6];
+  int32_t block_kernel; /* 1 = the whole block (stage 1 + down) in ONE
+                           persistent kernel with per-tile A2 dependency
+                           flags (the paper's single deeply fused kernel);
+                           0 = two kernels (stage 1, then down)          */
+  int32_t kbs;          /* 16 KiB weight blocks per pipeline stage (0 = auto) */
+  int32_t reserved[4];
   char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
 } dfk_config;
 

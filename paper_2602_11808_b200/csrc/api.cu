@@ -75,10 +75,17 @@ std::string config_label(const dfk_config& c) {
   std::ostringstream o;
   if (c.variant == DFK_VARIANT_TWO_KERNEL) return "two_kernel_cublaslt";
   if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
+  if (c.block_kernel) {
+    o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
+      << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
+      << (c.pdl ? "_pdl" : "");
+    return o.str();
+  }
   o << "fused_s1" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
     << c.s1_stages << "_c" << c.s1_ctas << "_dn"
     << (c.down_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
-    << c.down_stages << "_c" << c.down_ctas << (c.pdl ? "_pdl" : "");
+    << c.down_stages << "_c" << c.down_ctas << "_kbs" << c.kbs
+    << (c.pdl ? "_pdl" : "");
   return o.str();
 }
 
@@ -138,10 +145,17 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
   return DFK_OK;
 }
 
-int max_stages(dfk_context_s* ctx, int n_pad) {
+int max_stages(dfk_context_s* ctx, int n_pad, int kbs) {
   const int avail = ctx->max_smem_optin - 1024 - 1024;
-  int s = avail / stream_stage_bytes(n_pad);
-  return std::max(2, std::min(s, 32));
+  int s = avail / stream_stage_bytes(n_pad, kbs);
+  return std::min(s, 32);
+}
+
+// 32 KiB ring stages stream fastest (tools/stream_probe.cu); fall back to
+// 16 KiB when a 32 KiB stage would leave fewer than 4 slots.
+int pick_kbs(dfk_context_s* ctx, int n_pad, int requested) {
+  if (requested > 0) return std::min(requested, 4);
+  return max_stages(ctx, n_pad, 2) >= 4 ? 2 : 1;
 }
 
 int gemv_nb(int64_t b) {
@@ -180,43 +194,77 @@ int check_batch(int64_t B) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused stage 1 / down launchers.
+// Fused launchers.
 // ---------------------------------------------------------------------------
+struct Launch {
+  bool tc;
+  int64_t chunk;  // batch rows per launch
+};
+
+Launch launch_shape(int family) {
+  const bool tc = family != DFK_FAMILY_GEMV;
+  return {tc, tc ? 256 : 8};
+}
+
+void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
+                 int stages_req, int kbs_req, StreamArgs* a) {
+  const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
+  a->w1 = w->s1_pack;
+  a->t1 = w->s1_tiles;
+  a->kb1 = w->s1_kblocks;
+  a->w2 = w->dn_pack;
+  a->t2 = w->dn_tiles;
+  a->kb2 = w->dn_kblocks;
+  a->B = static_cast<int>(nb);
+  a->n_pad = n_pad;
+  a->kbs = pick_kbs(ctx, n_pad, kbs_req);
+  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs));
+  a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
+}
+
+int ensure_down_workspace(dfk_context_s* ctx, dfk_weights_s* w, int64_t rows) {
+  DFK_TRY(ensure_buf(ctx->yacc,
+                     static_cast<size_t>(rows) * w->dn_tiles * kDownCols *
+                         sizeof(float),
+                     true, ctx->stream));
+  return ensure_buf(ctx->counters, static_cast<size_t>(w->dn_tiles) * 4, true,
+                    ctx->stream);
+}
+
+void fill_down(dfk_context_s* ctx, dfk_weights_s* w, void* y, int64_t b0,
+               int64_t y_ld, bool y_bf16, StreamArgs* a) {
+  a->yacc = static_cast<float*>(ctx->yacc.p);
+  a->yacc_ld = w->dn_tiles * kDownCols;
+  a->counters = static_cast<int*>(ctx->counters.p);
+  a->y = y_bf16 ? static_cast<void*>(static_cast<__nv_bfloat16*>(y) + b0 * y_ld)
+                : static_cast<void*>(static_cast<float*>(y) + b0 * y_ld);
+  a->y_ld = y_ld;
+  a->y_bf16 = y_bf16 ? 1 : 0;
+  a->out_cols = static_cast<int>(w->d_model);
+}
+
 int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
                  int64_t B, __nv_bfloat16* a2, int64_t a2_ld,
                  const dfk_config& cfg) {
-  const bool tc = cfg.s1_family != DFK_FAMILY_GEMV;
-  if (!tc && B > 8) {
-    // GEMV family handles up to 8 rows per launch; chunk larger batches.
-  }
+  const Launch L = launch_shape(cfg.s1_family);
   const void* xp;
   int64_t x_ld;
   DFK_TRY(tma_operand(ctx, x, B, w->d_model, w->d_model, ctx->xpad, &xp, &x_ld));
-  const int64_t chunk = tc ? 256 : 8;
-  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
-    const int64_t nb = std::min(chunk, B - b0);
-    const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
-    CUtensorMap tm;
-    DFK_TRY(get_tmap(ctx,
-                     static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
-                     w->d_model, nb, x_ld, n_pad, &tm));
+  for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
+    const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
-    a.wpack = w->s1_pack;
-    a.tiles = w->s1_tiles;
-    a.kblocks = w->s1_kblocks;
-    a.B = static_cast<int>(nb);
-    a.n_pad = n_pad;
-    a.stages = cfg.s1_stages > 0 ? std::min(cfg.s1_stages, max_stages(ctx, n_pad))
-                                 : max_stages(ctx, n_pad);
-    a.split_k = 1;
+    fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg.kbs, &a);
+    CUtensorMap tm;
+    DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
+                     w->d_model, nb, x_ld, a.n_pad, &tm));
     a.a2 = a2 + b0 * a2_ld;
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     a.mutant = cfg.mutant;
     int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : ctx->sm_count;
     grid = std::max(1, std::min(grid, w->s1_tiles));
-    cudaError_t e = launch_stream(kModeStage1, tc, gemv_nb(nb), tm, a, grid,
-                                  cfg.pdl != 0, ctx->stream);
+    cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
+                                  grid, cfg.pdl != 0, ctx->stream);
     if (e != cudaSuccess)
       return fail(DFK_ERR_CUDA, std::string("stage-1 launch: ") +
                                     cudaGetErrorString(e));
@@ -228,51 +276,69 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
 int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
                int64_t a2_ld, int64_t B, void* y, int64_t y_ld, bool y_bf16,
                const dfk_config& cfg) {
-  const bool tc = cfg.down_family != DFK_FAMILY_GEMV;
+  const Launch L = launch_shape(cfg.down_family);
   const void* ap;
   int64_t a_ld;
   DFK_TRY(tma_operand(ctx, a2, B, w->d_ff, a2_ld, ctx->a2pad, &ap, &a_ld));
-  const int64_t chunk = tc ? 256 : 8;
-  const int yacc_ld = w->dn_tiles * kDownCols;
-  DFK_TRY(ensure_buf(ctx->yacc,
-                     static_cast<size_t>(std::min<int64_t>(chunk, B)) *
-                         yacc_ld * sizeof(float),
-                     true, ctx->stream));
-  DFK_TRY(ensure_buf(ctx->counters, static_cast<size_t>(w->dn_tiles) * 4, true,
-                     ctx->stream));
-  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
-    const int64_t nb = std::min(chunk, B - b0);
-    const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
+  DFK_TRY(ensure_down_workspace(ctx, w, std::min(L.chunk, B)));
+  for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
+    const int64_t nb = std::min(L.chunk, B - b0);
+    StreamArgs a = {};
+    fill_common(ctx, w, nb, L.tc, cfg.down_stages, cfg.kbs, &a);
     CUtensorMap tm;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
-                     w->d_ff, nb, a_ld, n_pad, &tm));
-    StreamArgs a = {};
-    a.wpack = w->dn_pack;
-    a.tiles = w->dn_tiles;
-    a.kblocks = w->dn_kblocks;
-    a.B = static_cast<int>(nb);
-    a.n_pad = n_pad;
-    a.stages = cfg.down_stages > 0
-                   ? std::min(cfg.down_stages, max_stages(ctx, n_pad))
-                   : max_stages(ctx, n_pad);
-    a.split_k = 1;
-    a.yacc = static_cast<float*>(ctx->yacc.p);
-    a.yacc_ld = yacc_ld;
-    a.counters = static_cast<int*>(ctx->counters.p);
-    a.y = y_bf16 ? static_cast<void*>(static_cast<__nv_bfloat16*>(y) + b0 * y_ld)
-                 : static_cast<void*>(static_cast<float*>(y) + b0 * y_ld);
-    a.y_ld = y_ld;
-    a.y_bf16 = y_bf16 ? 1 : 0;
-    a.out_cols = static_cast<int>(w->d_model);
+                     w->d_ff, nb, a_ld, a.n_pad, &tm));
+    fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
     int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count;
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, U));
-    cudaError_t e = launch_stream(kModeDown, tc, gemv_nb(nb), tm, a,
+    cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
                                   static_cast<int>(grid), cfg.pdl != 0,
                                   ctx->stream);
     if (e != cudaSuccess)
       return fail(DFK_ERR_CUDA,
                   std::string("down launch: ") + cudaGetErrorString(e));
+    ctx->launches++;
+  }
+  return DFK_OK;
+}
+
+// The whole block in one persistent launch per batch chunk (kModeBlock).
+// Every CTA must be co-resident (down pieces spin on stage-1 tile flags), so
+// the grid never exceeds the SM count.
+int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
+                __nv_bfloat16* a2, int64_t a2_ld, void* y, int64_t y_ld,
+                bool y_bf16, const dfk_config& cfg) {
+  const Launch L = launch_shape(cfg.s1_family);
+  const void* xp;
+  int64_t x_ld;
+  DFK_TRY(tma_operand(ctx, x, B, w->d_model, w->d_model, ctx->xpad, &xp, &x_ld));
+  DFK_TRY(ensure_down_workspace(ctx, w, std::min(L.chunk, B)));
+  DFK_TRY(ensure_buf(ctx->flags, static_cast<size_t>(w->s1_tiles) * 4, true,
+                     ctx->stream));
+  for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
+    const int64_t nb = std::min(L.chunk, B - b0);
+    StreamArgs a = {};
+    fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg.kbs, &a);
+    CUtensorMap xm, am;
+    DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
+                     w->d_model, nb, x_ld, a.n_pad, &xm));
+    DFK_TRY(get_tmap(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.n_pad, &am));
+    a.a2 = a2 + b0 * a2_ld;
+    a.a2_ld = a2_ld;
+    a.cols_valid = static_cast<int>(w->d_ff);
+    fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
+    a.flags = static_cast<unsigned*>(ctx->flags.p);
+    if (++ctx->epoch == 0) ++ctx->epoch;
+    a.epoch = ctx->epoch;
+    a.mutant = cfg.mutant;
+    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : ctx->sm_count;
+    grid = std::max(1, std::min(grid, ctx->sm_count));
+    cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,
+                                  grid, cfg.pdl != 0, ctx->stream);
+    if (e != cudaSuccess)
+      return fail(DFK_ERR_CUDA,
+                  std::string("block launch: ") + cudaGetErrorString(e));
     ctx->launches++;
   }
   return DFK_OK;
@@ -481,6 +547,10 @@ int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   DFK_TRY(ensure_buf(ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
                      ctx->stream));
   auto* a2 = static_cast<__nv_bfloat16*>(ctx->a2.p);
+  if (cfg.variant == DFK_VARIANT_FUSED && cfg.block_kernel) {
+    return block_fused(ctx, w, x, B, a2, a2_ld, y, w->d_model,
+                       y_dtype == DFK_BF16, cfg);
+  }
   if (cfg.variant == DFK_VARIANT_FUSED) {
     DFK_TRY(stage1_fused(ctx, w, x, B, a2, a2_ld, cfg));
     return down_fused(ctx, w, a2, a2_ld, B, y, w->d_model, y_dtype == DFK_BF16,
@@ -555,7 +625,7 @@ int dfk_context_destroy(dfk_context ctx) {
   if (!ctx) return DFK_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc,
+  for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc, &ctx->flags,
                        &ctx->counters, &ctx->concat, &ctx->tmp1, &ctx->tmp2,
                        &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev}) {
     if (b->p) cudaFree(b->p);

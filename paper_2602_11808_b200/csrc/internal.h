@@ -67,6 +67,8 @@ struct dfk_context_s {
   dfk::DeviceBuf a2pad;    // padded A2 for dfk_down with unaligned d_ff
   dfk::DeviceBuf yacc;     // fp32 down accumulator (kept all-zero)
   dfk::DeviceBuf counters; // per-tile down arrival counters (kept zero)
+  dfk::DeviceBuf flags;    // per-stage-1-tile completion flags (block kernel)
+  unsigned epoch = 0;      // block-kernel launch epoch (flag value)
   dfk::DeviceBuf concat;   // unfused comparator intermediates
   dfk::DeviceBuf tmp1, tmp2;
   dfk::DeviceBuf lt_ws;    // cuBLASLt workspace

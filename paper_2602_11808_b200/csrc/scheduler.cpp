@@ -74,21 +74,24 @@ std::string now_iso8601() {
   return buf;
 }
 
-dfk_config make_cfg(int variant, int s1f, int s1st, int dnf, int dnst,
+dfk_config make_cfg(int variant, int s1f, int dnf, int kbs, int block,
                     int pdl) {
   dfk_config c;
   std::memset(&c, 0, sizeof(c));
   c.variant = variant;
   c.s1_family = s1f;
-  c.s1_stages = s1st;
   c.s1_split_k = 1;
   c.down_family = dnf;
-  c.down_stages = dnst;
+  c.kbs = kbs;
+  c.block_kernel = block;
   c.pdl = pdl;
   std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
   return c;
 }
 
+// The GPU candidate grid: the two unfused cuBLASLt layouts, the two-kernel
+// fused path (stage-1 family x down family x stage size) and the single
+// persistent block kernel (family x stage size), plus one no-PDL control.
 std::vector<dfk_config> candidates(int64_t B) {
   std::vector<dfk_config> out;
   out.push_back(make_cfg(DFK_VARIANT_FOUR_KERNEL, 0, 0, 0, 0, 0));
@@ -96,19 +99,21 @@ std::vector<dfk_config> candidates(int64_t B) {
   std::vector<int> fams = {DFK_FAMILY_TC};
   if (B <= 8) fams.push_back(DFK_FAMILY_GEMV);
   std::set<std::string> seen;
-  for (int s1f : fams)
-    for (int dnf : fams)
-      for (int st : {0, 4})
-        for (int pdl : {1, 0}) {
-          if (pdl == 0 && st != 0) continue;  // keep the grid small
-          dfk_config c = make_cfg(DFK_VARIANT_FUSED, s1f, st, dnf, st, pdl);
-          if (seen.insert(c.label).second) out.push_back(c);
-        }
+  auto add = [&](const dfk_config& c) {
+    if (seen.insert(c.label).second) out.push_back(c);
+  };
+  for (int kbs : {0, 1}) {
+    for (int f : fams) add(make_cfg(DFK_VARIANT_FUSED, f, f, kbs, 1, 1));
+    for (int s1f : fams)
+      for (int dnf : fams) add(make_cfg(DFK_VARIANT_FUSED, s1f, dnf, kbs, 0, 1));
+  }
+  add(make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 0, 0));
   return out;
 }
 
 json cfg_to_json(const dfk_config& c) {
   return json{{"variant", c.variant},         {"s1_family", c.s1_family},
+              {"block_kernel", c.block_kernel}, {"kbs", c.kbs},
               {"s1_stages", c.s1_stages},     {"s1_ctas", c.s1_ctas},
               {"s1_split_k", c.s1_split_k},   {"down_family", c.down_family},
               {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
@@ -139,6 +144,8 @@ dfk_config cfg_from_json(const json& j) {
   c.down_stages = get_field<int>(j, "down_stages");
   c.down_ctas = get_field<int>(j, "down_ctas");
   c.pdl = get_field<int>(j, "pdl");
+  c.block_kernel = get_field<int>(j, "block_kernel");
+  c.kbs = get_field<int>(j, "kbs");
   std::snprintf(c.label, sizeof(c.label), "%s",
                 get_field<std::string>(j, "label").c_str());
   return c;

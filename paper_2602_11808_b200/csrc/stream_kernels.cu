@@ -1,41 +1,46 @@
 // stream_kernels.cu — the hot path: weight-streaming kernels for the fused
 // SwiGLU MLP on sm_100a.
 //
-// One kernel template covers both stages of the block and both consumer
+// One kernel template covers every stage of the block and both consumer
 // families:
 //
-//   mode  kModeStage1  A2 = (X W_up) * silu(X W_gate)     (fused.cpp:74-168,
-//                      DeepFusionKernel: gate and up accumulate side by side,
-//                      the SiLU*up epilogue runs once per element after the
-//                      FULL K reduction, A2 is the only global write)
-//   mode  kModeDown    Y = A2 W_down                      (swiglu.cpp:214-226)
+//   kModeStage1  A2 = (X W_up) * silu(X W_gate)  (fused.cpp:74-168,
+//                DeepFusionKernel: gate and up accumulate side by side, the
+//                SiLU*up epilogue runs once per element after the FULL K
+//                reduction, A2 is the only global write)
+//   kModeDown    Y = A2 W_down                   (swiglu.cpp:214-226)
+//   kModeBlock   both in ONE persistent launch (run_fused, fused.cpp:209-216)
 //
-//   family tcgen05     weights are the MMA M=128 operand, the batch is MMA N
-//                      (swap-AB), fp32 accumulators in TMEM, epilogue via
-//                      tcgen05.ld ("F2")
-//   family GEMV        8 CUDA-core warps dot the same smem stages with fp32
-//                      FMAs, warp-shuffle reductions (batch 1-8, "F1")
+//   tcgen05 family  weights are the MMA M=128 operand, the batch is MMA N
+//                   (swap-AB), fp32 accumulators in TMEM, epilogue through
+//                   tcgen05.ld
+//   GEMV family     8 CUDA-core warps dot the same smem stages with fp32
+//                   FMAs and warp-shuffle reductions (batch <= 8)
 //
-// Common skeleton (warp-specialised, persistent, one CTA per SM):
-//   warp 0      producer: 16 KiB weight blocks HBM->smem with 1-D bulk copies
-//               (cp.async.bulk, L2 evict_first) + the activation rows of the
-//               same K block with a 2-D TMA (128B swizzle) into a ring of
-//               `stages` slots, completion counted in bytes on mbarriers.
-//               The first ring's weight copies are issued BEFORE
-//               griddepcontrol.wait, so under PDL they overlap the previous
-//               kernel's tail; activations are only read after the wait.
-//   warp 1      tcgen05: one lane issues 4 x (M128 x N x K16) MMAs per block
+// Skeleton (warp-specialised, persistent, one CTA per SM):
+//   warp 0      producer: weight K blocks (16 KiB, pre-swizzled in HBM) with
+//               1-D bulk copies (cp.async.bulk, L2 evict_first) + the
+//               activation rows of the same K blocks with 2-D TMA (128B
+//               swizzle); `kbs` blocks per ring stage (32 KiB copies stream
+//               at ~7 TB/s, tools/stream_probe.cu).  The first ring's weight
+//               copies are issued BEFORE griddepcontrol.wait, so under PDL
+//               they overlap the previous kernel's tail.
+//   warp 1      tcgen05: one lane issues 4 MMAs (M128 x N x K16) per K block
 //               and tcgen05.commit's the slot back to the producer.
 //   warps 2-5   tcgen05 epilogue (TMEM lane quarter = warp % 4).
-//   warps 1-8   GEMV family: math warps (no TMEM).
+//   warps 1-8   GEMV family math warps (no TMEM).
 //
-// Work split: stage 1 hands whole tiles (64 A2 columns x full d_model) to
-// CTAs round-robin, so partial gate/up sums never leave the SM.  Down is
-// stream-K: the flattened (tile, K-block) space is cut into gridDim equal
-// ranges; each CTA reduces its pieces into an fp32 workspace with
-// red.global.add, and the CTA that completes a tile's last piece (per-tile
-// arrival counter) converts it to the output dtype and re-zeroes the
-// workspace, so no memset is ever needed.
+// Work is a sequence of "pieces" (one tile, a contiguous K-block range):
+//   stage-1 pieces are whole tiles (64 A2 columns x all of d_model) handed
+//   out round-robin, so partial gate/up sums never leave the SM;
+//   down pieces come from a stream-K split of the flattened (tile, K block)
+//   space: partial sums go to an fp32 workspace with red.global.add and the
+//   CTA completing a tile's last piece converts it to the output dtype and
+//   re-zeroes the workspace (no memset, ever).
+//   kModeBlock orders the down space wave-major (all K blocks whose stage-1
+//   tile is computed in round-robin wave 0 first, ...) and gives each CTA a
+//   byte-balanced share: CTAs with fewer stage-1 tiles take more down work,
+//   starting on K blocks whose A2 is already published.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -53,71 +58,200 @@ namespace {
 constexpr int kTcThreads = 192;    // producer, MMA, 4 epilogue warps
 constexpr int kGemvThreads = 288;  // producer + 8 math warps
 constexpr int kGemvWarps = 8;
+constexpr int kMaxKbs = 4;
 
-struct Seg {
-  int tile, kb0, kb1;
+// ---------------------------------------------------------------------------
+// Work plan.
+// ---------------------------------------------------------------------------
+struct Piece {
+  int down;  // 0 = stage-1 tile, 1 = down piece
+  int tile;
+  int kb0, kb1;
 };
 
-// The i-th (tile, K range) piece of this CTA's work.
-__device__ __forceinline__ bool seg_get(const StreamArgs& a, int mode, int i,
-                                        Seg& s) {
-  const int G = gridDim.x, c = blockIdx.x;
+struct Plan {
+  int mode;
+  int G, c;
+  int n1;            // stage-1 tiles of this CTA
+  int rank;          // this CTA's rank in the down ordering
+  int64_t u0, u1;    // this CTA's down ordering range
+  int64_t U2;        // total down units
+  // Byte-balanced ranges (kModeBlock): start(k) closed form parameters.
+  int L;             // CTAs with the smaller stage-1 share (ranked first)
+  int64_t base, rem; // per-rank budget = base + (k < rem) + (k < L) * kb1
+  int split_case;    // 0: U2 > L*kb1 (formula above); 1: light ranks only
+};
+
+__device__ __forceinline__ int64_t plan_start(const StreamArgs& a, const Plan& p,
+                                              int64_t k) {
+  if (p.mode == kModeDown) return p.U2 * k / p.G;
+  if (p.split_case == 0) {
+    return k * p.base + (k < p.rem ? k : p.rem) +
+           (k < p.L ? k : static_cast<int64_t>(p.L)) * a.kb1;
+  }
+  const int64_t kk = k < p.L ? k : p.L;
+  return kk * p.base + (kk < p.rem ? kk : p.rem);
+}
+
+__device__ __forceinline__ Plan make_plan(const StreamArgs& a, int mode) {
+  Plan p;
+  p.mode = mode;
+  p.G = gridDim.x;
+  p.c = blockIdx.x;
+  p.U2 = static_cast<int64_t>(a.t2) * a.kb2;
+  p.n1 = 0;
+  p.L = p.G;
+  p.base = p.rem = 0;
+  p.split_case = 0;
+  if (mode != kModeDown) {
+    p.n1 = p.c < a.t1 ? (a.t1 - 1 - p.c) / p.G + 1 : 0;
+  }
   if (mode == kModeStage1) {
-    const int t = c + i * G;
-    if (t >= a.tiles) return false;
-    s.tile = t;
-    s.kb0 = 0;
-    s.kb1 = a.kblocks;
+    p.rank = p.c;
+    p.u0 = p.u1 = 0;
+    return p;
+  }
+  if (mode == kModeDown) {
+    p.rank = p.c;
+  } else {
+    // Heavy CTAs (c < r) own one stage-1 tile more than light ones; light
+    // CTAs are ranked first in the down ordering and get kb1 more units.
+    const int r = a.t1 % p.G;
+    p.L = p.G - r;
+    p.rank = p.c >= r ? p.c - r : p.L + p.c;
+    const int64_t extra = p.U2 - static_cast<int64_t>(p.L) * a.kb1;
+    if (extra > 0) {
+      p.split_case = 0;
+      p.base = extra / p.G;
+      p.rem = extra - p.base * p.G;
+    } else {
+      p.split_case = 1;
+      p.base = p.U2 / p.L;
+      p.rem = p.U2 - p.base * p.L;
+    }
+  }
+  p.u0 = plan_start(a, p, p.rank);
+  p.u1 = plan_start(a, p, p.rank + 1);
+  return p;
+}
+
+// Ordering index u -> (tile, kb) and the end of its contiguous segment.
+__device__ __forceinline__ void down_unit(const StreamArgs& a, const Plan& p,
+                                          int64_t u, int* t, int* kb,
+                                          int64_t* seg_end) {
+  if (p.mode == kModeDown) {
+    *t = static_cast<int>(u / a.kb2);
+    *kb = static_cast<int>(u % a.kb2);
+    *seg_end = static_cast<int64_t>(*t + 1) * a.kb2;
+    return;
+  }
+  // Wave-major: wave w = stage-1 tiles [w*G, (w+1)*G) (round-robin wave).
+  const int64_t wave_units = static_cast<int64_t>(a.t2) * p.G;
+  const int w = static_cast<int>(u / wave_units);
+  const int64_t uw = u - w * wave_units;
+  const int nw = min(p.G, a.kb2 - w * p.G);
+  *t = static_cast<int>(uw / nw);
+  *kb = w * p.G + static_cast<int>(uw % nw);
+  *seg_end = w * wave_units + static_cast<int64_t>(*t + 1) * nw;
+}
+
+struct PieceIter {
+  int i = 0;
+  int64_t u = -1;
+  __device__ __forceinline__ bool next(const StreamArgs& a, const Plan& p,
+                                       Piece& out) {
+    if (i < p.n1) {
+      out.down = 0;
+      out.tile = p.c + i * p.G;
+      out.kb0 = 0;
+      out.kb1 = a.kb1;
+      ++i;
+      return true;
+    }
+    if (p.mode == kModeStage1) return false;
+    if (u < 0) u = p.u0;
+    if (u >= p.u1) return false;
+    int t, kb;
+    int64_t seg_end;
+    down_unit(a, p, u, &t, &kb, &seg_end);
+    const int64_t end = seg_end < p.u1 ? seg_end : p.u1;
+    out.down = 1;
+    out.tile = t;
+    out.kb0 = kb;
+    out.kb1 = kb + static_cast<int>(end - u);
+    u = end;
+    ++i;
     return true;
   }
-  const int64_t U = static_cast<int64_t>(a.tiles) * a.kblocks;
-  const int64_t u0 = U * c / G, u1 = U * (c + 1) / G;
-  const int t = static_cast<int>(u0 / a.kblocks) + i;
-  const int64_t ts = static_cast<int64_t>(t) * a.kblocks;
-  if (ts >= u1) return false;
-  s.tile = t;
-  s.kb0 = static_cast<int>(u0 > ts ? u0 - ts : 0);
-  s.kb1 = static_cast<int>(u1 - ts < a.kblocks ? u1 - ts : a.kblocks);
-  return s.kb0 < s.kb1;
-}
+};
 
-__device__ __forceinline__ int64_t cta_work_blocks(const StreamArgs& a,
-                                                   int mode) {
-  const int G = gridDim.x, c = blockIdx.x;
-  if (mode == kModeStage1) {
-    const int mine = c < a.tiles ? (a.tiles - 1 - c) / G + 1 : 0;
-    return static_cast<int64_t>(mine) * a.kblocks;
+// Largest rank k with start(k) <= u.
+__device__ __forceinline__ int rank_of(const StreamArgs& a, const Plan& p,
+                                       int64_t u) {
+  int lo = 0, hi = p.G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (plan_start(a, p, mid) <= u) lo = mid; else hi = mid - 1;
   }
-  const int64_t U = static_cast<int64_t>(a.tiles) * a.kblocks;
-  return U * (c + 1) / G - U * c / G;
+  return lo;
 }
 
-// Number of CTAs whose stream-K range touches down tile t (all ranges are
-// non-empty because the launcher keeps gridDim <= tiles * kblocks).
-__device__ __forceinline__ int down_contributors(const StreamArgs& a, int t) {
-  const int64_t U = static_cast<int64_t>(a.tiles) * a.kblocks;
-  const int64_t G = gridDim.x;
-  const int64_t lo = static_cast<int64_t>(t) * a.kblocks;
-  const int64_t hi = lo + a.kblocks;
-  const int64_t c_first = ((lo + 1) * G + U - 1) / U - 1;
-  const int64_t c_last = (hi * G + U - 1) / U - 1;
-  return static_cast<int>(c_last - c_first + 1);
+// Number of non-empty ranges intersecting [lo, hi).
+__device__ __forceinline__ int pieces_in(const StreamArgs& a, const Plan& p,
+                                         int64_t lo, int64_t hi) {
+  if (hi <= lo) return 0;
+  const int k0 = rank_of(a, p, lo), k1 = rank_of(a, p, hi - 1);
+  int n = 0;
+  for (int k = k0; k <= k1; ++k)
+    if (plan_start(a, p, k + 1) > plan_start(a, p, k)) ++n;
+  return n;
+}
+
+// How many pieces (flushes) down tile t receives in total.
+__device__ __forceinline__ int down_tile_pieces(const StreamArgs& a,
+                                                const Plan& p, int t) {
+  if (p.mode == kModeDown) {
+    const int64_t lo = static_cast<int64_t>(t) * a.kb2;
+    return pieces_in(a, p, lo, lo + a.kb2);
+  }
+  int n = 0;
+  const int64_t wave_units = static_cast<int64_t>(a.t2) * p.G;
+  for (int w = 0; w * p.G < a.kb2; ++w) {
+    const int nw = min(p.G, a.kb2 - w * p.G);
+    const int64_t lo = w * wave_units + static_cast<int64_t>(t) * nw;
+    n += pieces_in(a, p, lo, lo + nw);
+  }
+  return n;
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Down epilogue tail: publish this CTA's contribution to tile t; the last
-// contributor converts the tile to the output dtype and re-zeroes it.
-__device__ __forceinline__ void down_finish_tile(const StreamArgs& a, int t,
-                                                 int tid, int nthr,
-                                                 int* smem_flag) {
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Down epilogue tail: publish this CTA's piece of tile t; the CTA adding the
+// last piece converts the tile to the output dtype and re-zeroes it.
+__device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
+                                                 const Plan& p, int t, int tid,
+                                                 int nthr, int* smem_flag) {
   __threadfence();
   named_bar(1, nthr);
   if (tid == 0) {
     const int old = atomicAdd(&a.counters[t], 1);
-    *smem_flag = (old == down_contributors(a, t) - 1) ? 1 : 0;
+    *smem_flag = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
   }
   named_bar(1, nthr);
   if (*smem_flag) {
@@ -126,15 +260,15 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a, int t,
     for (int idx = tid; idx < a.B * kDownCols; idx += nthr) {
       const int n = idx / kDownCols, j = col0 + idx % kDownCols;
       if (j < a.out_cols) {
-        float* p = a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j;
-        const float v = __ldcg(p);
+        float* q = a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j;
+        const float v = __ldcg(q);
         if (a.y_bf16) {
           reinterpret_cast<__nv_bfloat16*>(a.y)[n * a.y_ld + j] =
               __float2bfloat16_rn(v);
         } else {
           reinterpret_cast<float*>(a.y)[n * a.y_ld + j] = v;
         }
-        __stcg(p, 0.0f);
+        __stcg(q, 0.0f);
       }
     }
     if (tid == 0) a.counters[t] = 0;
@@ -142,64 +276,125 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a, int t,
   named_bar(1, nthr);
 }
 
+// Stage-1 epilogue tail in kModeBlock: make this tile's A2 stores visible to
+// other SMs' TMA reads, then publish the tile's completion flag.
+__device__ __forceinline__ void s1_publish(const StreamArgs& a, int tile,
+                                           int tid, int nthr) {
+  fence_proxy_async_global();
+  __threadfence();
+  named_bar(1, nthr);
+  if (tid == 0) st_release(a.flags + tile, a.epoch);
+}
+
 // ---------------------------------------------------------------------------
-// Producer (one lane): ring of `stages` slots; the first ring's weight
-// copies go out before griddepcontrol.wait (PDL overlap), activations after.
+// Producer (one lane).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void produce(const StreamArgs& a, int mode,
-                                        const CUtensorMap* xmap, uint8_t* smem,
+__device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
+                                        const CUtensorMap* xmap,
+                                        const CUtensorMap* amap, uint8_t* smem,
                                         int stage_bytes, uint64_t* full,
                                         uint64_t* empty) {
   const uint64_t policy = policy_evict_first();
-  const int64_t total = cta_work_blocks(a, mode);
-  const int pre = static_cast<int>(total < a.stages ? total : a.stages);
-  const uint32_t x_bytes = static_cast<uint32_t>(a.n_pad) * 128u;
-  const uint32_t bytes = static_cast<uint32_t>(kBlockBytes) + x_bytes;
-  int pend_kb[32];
+  const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
+  const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
+  struct Pend {
+    int kb, nb, down;
+  };
+  Pend pend[32];
   int64_t it = 0;
-  Seg s;
-  for (int i = 0; seg_get(a, mode, i, s); ++i) {
-    for (int kb = s.kb0; kb < s.kb1; ++kb, ++it) {
+  bool waited = false;
+  PieceIter pi;
+  Piece pc;
+  while (pi.next(a, p, pc)) {
+    const uint8_t* wbase = pc.down ? a.w2 : a.w1;
+    const int kbt = pc.down ? a.kb2 : a.kb1;
+    for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
+      const int nb = min(a.kbs, pc.kb1 - kb);
       const int slot = static_cast<int>(it % a.stages);
       const uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
       if (it >= a.stages) mbar_wait(&empty[slot], phase ^ 1u);
       uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
-      mbar_arrive_expect_tx(&full[slot], bytes);
-      const uint8_t* src =
-          a.wpack + (static_cast<int64_t>(s.tile) * a.kblocks + kb) *
-                        static_cast<int64_t>(kBlockBytes);
-      bulk_g2s(st, src, kBlockBytes, &full[slot], policy);
-      if (it < pre) {
-        pend_kb[it] = kb;
-        if (it == pre - 1) {
-          pdl_wait();
-          for (int j = 0; j < pre; ++j) {
-            tma_load_2d(smem + static_cast<int64_t>(j) * stage_bytes +
-                            kBlockBytes,
-                        xmap, pend_kb[j] * kBlockK, 0, &full[j]);
+      mbar_arrive_expect_tx(&full[slot],
+                            static_cast<uint32_t>(nb) * (kBlockBytes + xblk));
+      // nb consecutive K blocks of one tile are contiguous in the pack.
+      bulk_g2s(st,
+               wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
+                           static_cast<int64_t>(kBlockBytes),
+               static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
+      if (!waited) {
+        pend[it] = {kb, nb, pc.down};
+        if (it + 1 < a.stages) continue;  // keep prefetching weights
+        pdl_wait();
+        waited = true;
+        for (int j = 0; j <= it; ++j) {
+          uint8_t* sj = smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all;
+          for (int b = 0; b < pend[j].nb; ++b) {
+            const int kbb = pend[j].kb + b;
+            if (pend[j].down) {
+              if (a.flags) {
+                while (ld_acquire(a.flags + kbb) != a.epoch) {
+                }
+                fence_proxy_async_global();
+              }
+              tma_load_2d(sj + b * xblk, amap, kbb * kBlockK, 0, &full[j]);
+            } else {
+              tma_load_2d(sj + b * xblk, xmap, kbb * kBlockK, 0, &full[j]);
+            }
           }
         }
-      } else {
-        tma_load_2d(st + kBlockBytes, xmap, kb * kBlockK, 0, &full[slot]);
+        continue;
+      }
+      uint8_t* xs = st + wbytes_all;
+      for (int b = 0; b < nb; ++b) {
+        const int kbb = kb + b;
+        if (pc.down) {
+          if (a.flags) {
+            while (ld_acquire(a.flags + kbb) != a.epoch) {
+            }
+            fence_proxy_async_global();
+          }
+          tma_load_2d(xs + b * xblk, amap, kbb * kBlockK, 0, &full[slot]);
+        } else {
+          tma_load_2d(xs + b * xblk, xmap, kbb * kBlockK, 0, &full[slot]);
+        }
       }
     }
   }
-  if (pre == 0) pdl_wait();
+  if (!waited) {
+    // Fewer stages of work than ring slots: flush the deferred loads.
+    pdl_wait();
+    for (int j = 0; j < it; ++j) {
+      uint8_t* sj = smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all;
+      for (int b = 0; b < pend[j].nb; ++b) {
+        const int kbb = pend[j].kb + b;
+        if (pend[j].down) {
+          if (a.flags) {
+            while (ld_acquire(a.flags + kbb) != a.epoch) {
+            }
+            fence_proxy_async_global();
+          }
+          tma_load_2d(sj + b * xblk, amap, kbb * kBlockK, 0, &full[j]);
+        } else {
+          tma_load_2d(sj + b * xblk, xmap, kbb * kBlockK, 0, &full[j]);
+        }
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
-// GEMV math warps (batch <= NB). Lane = (q, c): c = 16-byte chunk of the
-// 64-wide K block, q = one of 4 rows this warp handles per pass; 4 passes
-// cover the 32-row group of each pass p.
+// GEMV math warps (batch <= NB).  Lane = (q, c): c = 16-byte chunk of the
+// 64-wide K block, q = one of the 4 rows this warp handles per pass; pass p
+// covers the 32-row group p of the 128-row block.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int gemv_row(int p, int mw, int q) {
-  // q 0,1 -> gate rows 2mw+q, q 2,3 -> matching up rows (16 apart), so the
-  // gate/up pair of one A2 column is lane ^ 16 within the warp.
+  // q 0,1 -> gate rows 2mw+q; q 2,3 -> the matching up rows (16 apart), so
+  // the gate/up pair of one A2 column is lane ^ 16.
   return p * 32 + (q < 2 ? 2 * mw + q : 16 + 2 * mw + (q - 2));
 }
 
-template <int kMode, int NB>
-__device__ __forceinline__ void gemv_consume(const StreamArgs& a,
+template <int NB>
+__device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
                                              uint8_t* smem, int stage_bytes,
                                              uint64_t* full, uint64_t* empty,
                                              int* smem_flag) {
@@ -207,88 +402,97 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a,
   const int lane = static_cast<int>(lane_id());
   const int q = lane >> 3, c = lane & 7;
   const int tid = mw * 32 + lane;
+  const int nthr = kGemvWarps * 32;
+  const int wbytes_all = a.kbs * kBlockBytes;
+  const int xblk = a.n_pad * 128;
   int64_t it = 0;
-  Seg s;
-  for (int i = 0; seg_get(a, kMode, i, s); ++i) {
+  PieceIter pi;
+  Piece pc;
+  while (pi.next(a, p, pc)) {
     float acc[4][NB];
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int n = 0; n < NB; ++n) acc[p][n] = 0.f;
+      for (int n = 0; n < NB; ++n) acc[r][n] = 0.f;
 
-    for (int kb = s.kb0; kb < s.kb1; ++kb, ++it) {
+    for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
+      const int nb = min(a.kbs, pc.kb1 - kb);
       const int slot = static_cast<int>(it % a.stages);
       const uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
       mbar_wait(&full[slot], phase);
       const uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
-      const uint8_t* xs = st + kBlockBytes;
-      float xf[NB][8];
+      for (int b = 0; b < nb; ++b) {
+        const uint8_t* ws = st + b * kBlockBytes;
+        const uint8_t* xs = st + wbytes_all + b * xblk;
+        float xf[NB][8];
 #pragma unroll
-      for (int n = 0; n < NB; ++n) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(
-            xs + n * 128 + ((c ^ (n & 7)) << 4));
-        xf[n][0] = bf16lo(xv.x); xf[n][1] = bf16hi(xv.x);
-        xf[n][2] = bf16lo(xv.y); xf[n][3] = bf16hi(xv.y);
-        xf[n][4] = bf16lo(xv.z); xf[n][5] = bf16hi(xv.z);
-        xf[n][6] = bf16lo(xv.w); xf[n][7] = bf16hi(xv.w);
-      }
+        for (int n = 0; n < NB; ++n) {
+          const uint4 xv = *reinterpret_cast<const uint4*>(
+              xs + n * 128 + ((c ^ (n & 7)) << 4));
+          xf[n][0] = bf16lo(xv.x); xf[n][1] = bf16hi(xv.x);
+          xf[n][2] = bf16lo(xv.y); xf[n][3] = bf16hi(xv.y);
+          xf[n][4] = bf16lo(xv.z); xf[n][5] = bf16hi(xv.z);
+          xf[n][6] = bf16lo(xv.w); xf[n][7] = bf16hi(xv.w);
+        }
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int r = gemv_row(p, mw, q);
-        const uint4 wv = *reinterpret_cast<const uint4*>(
-            st + r * 128 + ((c ^ (r & 7)) << 4));
-        float wf[8];
-        wf[0] = bf16lo(wv.x); wf[1] = bf16hi(wv.x);
-        wf[2] = bf16lo(wv.y); wf[3] = bf16hi(wv.y);
-        wf[4] = bf16lo(wv.z); wf[5] = bf16hi(wv.z);
-        wf[6] = bf16lo(wv.w); wf[7] = bf16hi(wv.w);
+        for (int r = 0; r < 4; ++r) {
+          const int row = gemv_row(r, mw, q);
+          const uint4 wv = *reinterpret_cast<const uint4*>(
+              ws + row * 128 + ((c ^ (row & 7)) << 4));
+          float wf[8];
+          wf[0] = bf16lo(wv.x); wf[1] = bf16hi(wv.x);
+          wf[2] = bf16lo(wv.y); wf[3] = bf16hi(wv.y);
+          wf[4] = bf16lo(wv.z); wf[5] = bf16hi(wv.z);
+          wf[6] = bf16lo(wv.w); wf[7] = bf16hi(wv.w);
 #pragma unroll
-        for (int n = 0; n < NB; ++n)
+          for (int n = 0; n < NB; ++n)
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[p][n] = fmaf(wf[e], xf[n][e], acc[p][n]);
+            for (int e = 0; e < 8; ++e)
+              acc[r][n] = fmaf(wf[e], xf[n][e], acc[r][n]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
 
-    // Reduce the 8 K-chunks of every row.
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int n = 0; n < NB; ++n) {
-        float v = acc[p][n];
+        float v = acc[r][n];
         v += __shfl_xor_sync(0xffffffffu, v, 1);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         v += __shfl_xor_sync(0xffffffffu, v, 4);
-        acc[p][n] = v;
+        acc[r][n] = v;
       }
 
-    if constexpr (kMode == kModeStage1) {
+    if (!pc.down) {
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int col = s.tile * kS1Cols + p * 16 + 2 * mw + q;
+      for (int r = 0; r < 4; ++r) {
+        const int col = pc.tile * kS1Cols + r * 16 + 2 * mw + q;
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
-          const float up = __shfl_xor_sync(0xffffffffu, acc[p][n], 16);
+          const float up = __shfl_xor_sync(0xffffffffu, acc[r][n], 16);
           if (c == 0 && q < 2 && n < a.B && col < a.cols_valid) {
             a.a2[n * a.a2_ld + col] =
-                __float2bfloat16_rn(silu_f(acc[p][n]) * up);
+                __float2bfloat16_rn(silu_f(acc[r][n]) * up);
           }
         }
       }
+      if (a.flags) s1_publish(a, pc.tile, tid, nthr);
     } else {
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int j = s.tile * kDownCols + gemv_row(p, mw, q);
+      for (int r = 0; r < 4; ++r) {
+        const int j = pc.tile * kDownCols + gemv_row(r, mw, q);
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
           if (c == 0 && n < a.B && j < a.out_cols) {
             atomicAdd(a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j,
-                      acc[p][n]);
+                      acc[r][n]);
           }
         }
       }
-      down_finish_tile(a, s.tile, tid, kGemvWarps * 32, smem_flag);
+      down_finish_tile(a, p, pc.tile, tid, nthr, smem_flag);
     }
   }
 }
@@ -296,46 +500,53 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a,
 // ---------------------------------------------------------------------------
 // tcgen05 MMA issuer (one lane of warp 1).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mma_issue(const StreamArgs& a, int mode,
+__device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
                                           uint8_t* smem, int stage_bytes,
                                           uint64_t* full, uint64_t* empty,
                                           uint64_t* tfull, uint64_t* tempty,
                                           uint32_t tmem_base) {
   const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>(a.n_pad));
+  const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
+  const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
   int64_t it = 0;
   int acc_it = 0;
-  Seg s;
-  for (int i = 0; seg_get(a, mode, i, s); ++i, ++acc_it) {
+  PieceIter pi;
+  Piece pc;
+  while (pi.next(a, p, pc)) {
     const int ab = acc_it & 1;
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tempty[ab], aph ^ 1u);
     tc_fence_after();
     const uint32_t d = tmem_base + static_cast<uint32_t>(ab * a.n_pad);
-    for (int kb = s.kb0; kb < s.kb1; ++kb, ++it) {
+    for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
+      const int nb = min(a.kbs, pc.kb1 - kb);
       const int slot = static_cast<int>(it % a.stages);
       const uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
       mbar_wait(&full[slot], phase);
       tc_fence_after();
-      const uint32_t wbase =
+      const uint32_t sbase =
           smem_u32(smem + static_cast<int64_t>(slot) * stage_bytes);
-      const uint32_t xbase = wbase + kBlockBytes;
+      for (int b = 0; b < nb; ++b) {
+        const uint32_t wb = sbase + b * kBlockBytes;
+        const uint32_t xb = sbase + wbytes_all + b * xblk;
 #pragma unroll
-      for (int k = 0; k < kBlockK / 16; ++k) {
-        tc_mma_bf16(d, umma_desc_sw128(wbase + k * 32),
-                    umma_desc_sw128(xbase + k * 32), idesc,
-                    (kb > s.kb0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < kBlockK / 16; ++k) {
+          tc_mma_bf16(d, umma_desc_sw128(wb + k * 32),
+                      umma_desc_sw128(xb + k * 32), idesc,
+                      (kb > pc.kb0 || b > 0 || k > 0) ? 1u : 0u);
+        }
       }
       tc_commit(&empty[slot]);
     }
     tc_commit(&tfull[ab]);
+    ++acc_it;
   }
 }
 
 // ---------------------------------------------------------------------------
 // tcgen05 epilogue (warps 2-5; TMEM lanes 32*(warp%4) .. +31).
 // ---------------------------------------------------------------------------
-template <int kMode>
-__device__ __forceinline__ void tc_epilogue(const StreamArgs& a,
+__device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
                                             uint64_t* tfull, uint64_t* tempty,
                                             uint32_t tmem_base,
                                             int* smem_flag) {
@@ -345,18 +556,20 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a,
   const int row = quarter * 32 + lane;
   const int tid = (w - 2) * 32 + lane;
   int acc_it = 0;
-  Seg s;
-  for (int i = 0; seg_get(a, kMode, i, s); ++i, ++acc_it) {
+  PieceIter pi;
+  Piece pc;
+  while (pi.next(a, p, pc)) {
     const int ab = acc_it & 1;
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tfull[ab], aph);
     tc_fence_after();
-    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+    const uint32_t taddr = tmem_base +
+                           (static_cast<uint32_t>(quarter * 32) << 16) +
                            static_cast<uint32_t>(ab * a.n_pad);
-    if constexpr (kMode == kModeStage1) {
+    if (!pc.down) {
       int is_up, cofs;
       s1_row_map(row, &is_up, &cofs);
-      const int col = s.tile * kS1Cols + cofs;
+      const int col = pc.tile * kS1Cols + cofs;
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + c0, v);
@@ -372,8 +585,9 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (a.flags) s1_publish(a, pc.tile, tid, 128);
     } else {
-      const int j = s.tile * kDownCols + row;
+      const int j = pc.tile * kDownCols + row;
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + c0, v);
@@ -388,14 +602,15 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      down_finish_tile(a, s.tile, tid, 128, smem_flag);
+      down_finish_tile(a, p, pc.tile, tid, 128, smem_flag);
     }
+    ++acc_it;
   }
 }
 
-__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+__device__ __forceinline__ uint8_t* align1024(uint8_t* ptr) {
   return reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(p) + 1023) & ~static_cast<uintptr_t>(1023));
+      (reinterpret_cast<uintptr_t>(ptr) + 1023) & ~static_cast<uintptr_t>(1023));
 }
 
 // ---------------------------------------------------------------------------
@@ -404,10 +619,11 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 template <int kMode, bool kTC, int NB>
 __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     stream_kernel(const __grid_constant__ CUtensorMap xmap,
+                  const __grid_constant__ CUtensorMap amap,
                   const StreamArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int stage_bytes = stream_stage_bytes(a.n_pad);
+  const int stage_bytes = stream_stage_bytes(a.n_pad, a.kbs);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
@@ -417,7 +633,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
 
   const uint32_t w = warp_id();
   if (w == 0 && lane_id() == 0) {
-    prefetch_tmap(&xmap);
+    if (kMode != kModeDown) prefetch_tmap(&xmap);
+    if (kMode != kModeStage1) prefetch_tmap(&amap);
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kTC ? 1 : kGemvWarps);
@@ -437,23 +654,25 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = kTC ? *tmem_slot : 0u;
+  const Plan plan = make_plan(a, kMode);
 
   // Let the next kernel in the stream get scheduled as SMs drain; it only
   // touches our outputs after its own griddepcontrol.wait.
   pdl_launch_dependents();
 
   if (w == 0) {
-    if (lane_id() == 0) produce(a, kMode, &xmap, smem, stage_bytes, full, empty);
+    if (lane_id() == 0)
+      produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty);
   } else if constexpr (kTC) {
     if (w == 1) {
       if (lane_id() == 0)
-        mma_issue(a, kMode, smem, stage_bytes, full, empty, tfull, tempty,
+        mma_issue(a, plan, smem, stage_bytes, full, empty, tfull, tempty,
                   tmem_base);
     } else {
-      tc_epilogue<kMode>(a, tfull, tempty, tmem_base, smem_flag);
+      tc_epilogue(a, plan, tfull, tempty, tmem_base, smem_flag);
     }
   } else {
-    gemv_consume<kMode, NB>(a, smem, stage_bytes, full, empty, smem_flag);
+    gemv_consume<NB>(a, plan, smem, stage_bytes, full, empty, smem_flag);
   }
 
   __syncthreads();
@@ -467,8 +686,9 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
 }
 
 template <int kMode, bool kTC, int NB>
-cudaError_t launch_one(const CUtensorMap& xmap, const StreamArgs& a, int grid,
-                       int smem, bool pdl, cudaStream_t stream) {
+cudaError_t launch_one(const CUtensorMap& xmap, const CUtensorMap& amap,
+                       const StreamArgs& a, int grid, int smem, bool pdl,
+                       cudaStream_t stream) {
   auto kern = stream_kernel<kMode, kTC, NB>;
   static int configured_smem = -1;  // per instantiation; one device per process
   if (smem > configured_smem) {
@@ -491,42 +711,46 @@ cudaError_t launch_one(const CUtensorMap& xmap, const StreamArgs& a, int grid,
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, kern, xmap, a);
+  return cudaLaunchKernelEx(&cfg, kern, xmap, amap, a);
+}
+
+template <int kMode>
+cudaError_t launch_mode(bool tc, int nb, const CUtensorMap& xmap,
+                        const CUtensorMap& amap, const StreamArgs& a, int grid,
+                        int smem, bool pdl, cudaStream_t s) {
+  if (tc) return launch_one<kMode, true, 0>(xmap, amap, a, grid, smem, pdl, s);
+  switch (nb) {
+    case 1: return launch_one<kMode, false, 1>(xmap, amap, a, grid, smem, pdl, s);
+    case 2: return launch_one<kMode, false, 2>(xmap, amap, a, grid, smem, pdl, s);
+    case 4: return launch_one<kMode, false, 4>(xmap, amap, a, grid, smem, pdl, s);
+    case 8: return launch_one<kMode, false, 8>(xmap, amap, a, grid, smem, pdl, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace
 
-int stream_smem_bytes(bool tc, int n_pad, int stages, int split_k) {
-  (void)tc;
-  (void)split_k;
-  return 1024 + stages * stream_stage_bytes(n_pad) + (2 * stages + 4) * 8 + 16;
+int stream_smem_bytes(int n_pad, int stages, int kbs) {
+  return 1024 + stages * stream_stage_bytes(n_pad, kbs) + (2 * stages + 4) * 8 + 16;
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
-                          const CUtensorMap& xmap, const StreamArgs& a,
-                          int grid, bool pdl, cudaStream_t stream) {
-  const int smem = stream_smem_bytes(tc, a.n_pad, a.stages, a.split_k);
-  if (tc) {
-    return mode == kModeStage1
-               ? launch_one<kModeStage1, true, 0>(xmap, a, grid, smem, pdl, stream)
-               : launch_one<kModeDown, true, 0>(xmap, a, grid, smem, pdl, stream);
-  }
-#define DFK_GEMV_CASE(NBV)                                                    \
-  case NBV:                                                                   \
-    return mode == kModeStage1                                                \
-               ? launch_one<kModeStage1, false, NBV>(xmap, a, grid, smem, pdl, \
-                                                     stream)                  \
-               : launch_one<kModeDown, false, NBV>(xmap, a, grid, smem, pdl,   \
-                                                   stream);
-  switch (nb_gemv) {
-    DFK_GEMV_CASE(1)
-    DFK_GEMV_CASE(2)
-    DFK_GEMV_CASE(4)
-    DFK_GEMV_CASE(8)
+                          const CUtensorMap& xmap, const CUtensorMap& amap,
+                          const StreamArgs& a, int grid, bool pdl,
+                          cudaStream_t stream) {
+  if (a.kbs < 1 || a.kbs > kMaxKbs || a.stages < 2 || a.stages > 32)
+    return cudaErrorInvalidValue;
+  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs);
+  switch (mode) {
+    case kModeStage1:
+      return launch_mode<kModeStage1>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);
+    case kModeDown:
+      return launch_mode<kModeDown>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);
+    case kModeBlock:
+      return launch_mode<kModeBlock>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);
     default:
       return cudaErrorInvalidValue;
   }
-#undef DFK_GEMV_CASE
 }
 
 }  // namespace dfk

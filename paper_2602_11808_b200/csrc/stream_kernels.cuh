@@ -9,23 +9,33 @@
 
 namespace dfk {
 
-enum StreamMode : int { kModeStage1 = 0, kModeDown = 1 };
+// kModeStage1: fused gate/up GEMM + SiLU*up epilogue -> A2 (one kernel).
+// kModeDown:   A2 W_down, stream-K over (tile, K block) -> Y.
+// kModeBlock:  the whole block in ONE persistent kernel: every CTA first
+//              streams its stage-1 tiles, then down pieces; a down piece's
+//              A2 block is loaded only after the stage-1 tile that produced
+//              it published its completion flag (epoch-tagged).
+enum StreamMode : int { kModeStage1 = 0, kModeDown = 1, kModeBlock = 2 };
 
 struct StreamArgs {
-  const uint8_t* wpack;  // packed weight blocks (layout.cuh)
-  int tiles;             // weight tiles (128 rows each)
-  int kblocks;           // 64-wide K blocks per tile
-  int B;                 // batch rows actually present
-  int n_pad;             // MMA N (tcgen05) / X box rows (GEMV)
-  int stages;            // pipeline depth
-  int split_k;           // stage 1: CTAs of a cluster sharing one tile
-  // Stage 1 output: A2 [B x a2_ld] bf16, columns < cols_valid written.
+  // Stage-1 pack ([W_gate|W_up] interleaved): t1 tiles x kb1 K blocks.
+  const uint8_t* w1;
+  int t1, kb1;
+  // Down pack (W_down): t2 tiles x kb2 K blocks (kb2 == t1: one K block of
+  // the down projection per stage-1 tile).
+  const uint8_t* w2;
+  int t2, kb2;
+  int B;       // batch rows present
+  int n_pad;   // MMA N (tcgen05) / activation box rows (GEMV)
+  int stages;  // ring depth
+  int kbs;     // K blocks (16 KiB each) per ring stage
+  // Stage-1 output: A2 [B x a2_ld] bf16, columns < cols_valid written.
   __nv_bfloat16* a2;
   int64_t a2_ld;
   int cols_valid;
-  // Down output: fp32 accumulation workspace (self-cleaning: zero on entry,
-  // re-zeroed by the CTA that finalises each tile), per-tile completion
-  // counters (zero on entry, reset on finalise), final Y [B x y_ld].
+  // Down output: fp32 accumulation workspace (zero on entry; re-zeroed by
+  // the CTA that finalises each tile), per-tile arrival counters (zero on
+  // entry, reset on finalise), final Y [B x y_ld] fp32 or bf16.
   float* yacc;
   int yacc_ld;
   int* counters;
@@ -33,22 +43,21 @@ struct StreamArgs {
   int64_t y_ld;
   int y_bf16;
   int out_cols;
-  // Debug / negative control: 1 = apply SiLU per K-chunk of a split-K tile
-  // (the reference's SiluPerKChunk mutant, verification.cpp:84-124).
+  // kModeBlock: per-stage-1-tile completion flags and this launch's epoch.
+  unsigned* flags;
+  unsigned epoch;
   int mutant;
 };
 
 // Smem bytes of one pipeline stage (weights + activation rows).
-__host__ __device__ inline int stream_stage_bytes(int n_pad) { return 16384 + n_pad * 128; }
+__host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs) {
+  return kbs * (16384 + n_pad * 128);
+}
 
-// Launchers (stream_kernels.cu). `tc` selects the tcgen05 family, else the
-// CUDA-core GEMV family.  grid = CTAs (multiple of split_k).  Returns the
-// cudaError of the launch.
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xmap,
-                          const StreamArgs& a, int grid, bool pdl,
-                          cudaStream_t stream);
+                          const CUtensorMap& amap, const StreamArgs& a, int grid,
+                          bool pdl, cudaStream_t stream);
 
-// Max dynamic smem the launcher will request for (tc, n_pad, stages).
-int stream_smem_bytes(bool tc, int n_pad, int stages, int split_k);
+int stream_smem_bytes(int n_pad, int stages, int kbs);
 
 }  // namespace dfk

@@ -78,17 +78,19 @@ class Config(C.Structure):
                 ("s1_split_k", C.c_int32), ("down_family", C.c_int32),
                 ("down_stages", C.c_int32), ("down_ctas", C.c_int32),
                 ("pdl", C.c_int32), ("mutant", C.c_int32),
-                ("reserved", C.c_int32 * 6), ("label", C.c_char * 64)]
+                ("block_kernel", C.c_int32), ("kbs", C.c_int32),
+                ("reserved", C.c_int32 * 4), ("label", C.c_char * 64)]
 
     @classmethod
     def make(cls, variant=VARIANT_FUSED, s1_family=FAMILY_TC, down_family=FAMILY_TC,
              s1_stages=0, down_stages=0, s1_ctas=0, down_ctas=0, pdl=1, mutant=0,
-             s1_split_k=1, label=""):
+             s1_split_k=1, block_kernel=0, kbs=0, label=""):
         c = cls()
         c.variant, c.s1_family, c.down_family = variant, s1_family, down_family
         c.s1_stages, c.down_stages, c.s1_ctas, c.down_ctas = (s1_stages, down_stages,
                                                               s1_ctas, down_ctas)
         c.pdl, c.mutant, c.s1_split_k = pdl, mutant, s1_split_k
+        c.block_kernel, c.kbs = block_kernel, kbs
         c.label = label.encode()[:63]
         return c
 

@@ -41,6 +41,9 @@ def configs(rt, B):
     out = {
         "fused_tc": rt.Config.make(s1_family=rt.FAMILY_TC, down_family=rt.FAMILY_TC),
         "fused_tc_nopdl": rt.Config.make(pdl=0),
+        "fused_tc_kbs1": rt.Config.make(kbs=1, s1_stages=3, down_stages=5),
+        "block_tc": rt.Config.make(block_kernel=1),
+        "block_tc_kbs1_c37": rt.Config.make(block_kernel=1, kbs=1, s1_ctas=37),
         "two_kernel": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
         "four_kernel": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
     }
@@ -49,6 +52,8 @@ def configs(rt, B):
                                            down_family=rt.FAMILY_GEMV)
         out["fused_gemv_tc"] = rt.Config.make(s1_family=rt.FAMILY_GEMV,
                                               down_family=rt.FAMILY_TC)
+        out["block_gemv"] = rt.Config.make(block_kernel=1, s1_family=rt.FAMILY_GEMV,
+                                           down_family=rt.FAMILY_GEMV)
     return out
 
 
@@ -158,11 +163,11 @@ def test_stage1_bitwise_invariant_across_launch_configs(rt, ctx, oracle_lib):
     outs = []
     for fam in (rt.FAMILY_TC, rt.FAMILY_GEMV):
         base = None
-        for stages in (2, 3, 5, 0):
+        for stages, kbs in ((2, 1), (3, 2), (5, 1), (0, 0), (2, 4)):
             for ctas in (1, 7, 148, 0):
                 a2 = ctx.array((B, df))
                 ctx.stage1(w, xd, a2, cfg=rt.Config.make(s1_family=fam, s1_stages=stages,
-                                                         s1_ctas=ctas))
+                                                         s1_ctas=ctas, kbs=kbs))
                 bits = a2.download_bits()
                 if base is None:
                     base = bits
