@@ -236,6 +236,12 @@ DFK_API int dfk_event_record(dfk_context ctx, void* ev);
 DFK_API int dfk_event_elapsed_ms(void* start, void* stop, float* ms);
 /* Writes `bytes` of junk to a scratch buffer larger than L2 (flush). */
 DFK_API int dfk_flush_l2(dfk_context ctx);
+/* Kernel timeline tracing (diagnostics): while `buf` is non-NULL every
+ * streaming-kernel launch of this context writes per-CTA globaltimer stamps
+ * (64 x uint64 per CTA: start, producer done, consumer done, then per piece
+ * issue / retire) into the device buffer `buf` of `slots` uint64.  NULL
+ * turns tracing off (the default; zero cost). */
+DFK_API int dfk_set_trace(dfk_context ctx, void* buf, int64_t slots);
 /* Number of hot-path kernel launches issued by this context so far. */
 DFK_API int dfk_launch_count(dfk_context ctx, int64_t* n);
 

@@ -218,6 +218,7 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   a->B = static_cast<int>(nb);
   a->n_pad = n_pad;
   a->kbs = pick_kbs(ctx, n_pad, kbs_req);
+  a->trace = ctx->trace;
   const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
@@ -990,6 +991,15 @@ int dfk_flush_l2(dfk_context ctx) {
   const size_t bytes = static_cast<size_t>(std::max(ctx->l2_bytes, 1 << 20)) * 2;
   DFK_TRY(ensure_buf(ctx->flush, bytes, false, ctx->stream));
   DFK_CUDA(launch_flush(ctx->flush.p, bytes, ctx->stream));
+  return DFK_OK;
+}
+
+int dfk_set_trace(dfk_context ctx, void* buf, int64_t slots) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  if (buf && slots < static_cast<int64_t>(ctx->sm_count) * 2 * kTraceSlots)
+    return fail(DFK_ERR_INVALID, "trace buffer needs >= 2 * SMs * 64 slots");
+  ctx->trace = static_cast<unsigned long long*>(buf);
+  ctx->trace_slots = slots;
   return DFK_OK;
 }
 

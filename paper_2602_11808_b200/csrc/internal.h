@@ -69,6 +69,8 @@ struct dfk_context_s {
   dfk::DeviceBuf counters; // per-tile down arrival counters (kept zero)
   dfk::DeviceBuf flags;    // per-stage-1-tile completion flags (block kernel)
   unsigned epoch = 0;      // block-kernel launch epoch (flag value)
+  unsigned long long* trace = nullptr;  // dfk_set_trace buffer
+  int64_t trace_slots = 0;
   dfk::DeviceBuf concat;   // unfused comparator intermediates
   dfk::DeviceBuf tmp1, tmp2;
   dfk::DeviceBuf lt_ws;    // cuBLASLt workspace

@@ -224,6 +224,17 @@ __device__ __forceinline__ int down_tile_pieces(const StreamArgs& a,
   return n;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void trace_stamp(const StreamArgs& a, int slot) {
+  if (a.trace && slot < kTraceSlots)
+    a.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + slot] = gtimer();
+}
+
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -306,6 +317,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
   PieceIter pi;
   Piece pc;
   while (pi.next(a, p, pc)) {
+    trace_stamp(a, 1 + 2 * pi.i);
     const uint8_t* wbase = pc.down ? a.w2 : a.w1;
     const int kbt = pc.down ? a.kb2 : a.kb1;
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
@@ -360,6 +372,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       }
     }
   }
+  trace_stamp(a, 1);
   if (!waited) {
     // Fewer stages of work than ring slots: flush the deferred loads.
     pdl_wait();
@@ -494,7 +507,9 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
       }
       down_finish_tile(a, p, pc.tile, tid, nthr, smem_flag);
     }
+    if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
   }
+  if (tid == 0) trace_stamp(a, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -604,8 +619,10 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       if (lane == 0) mbar_arrive(&tempty[ab]);
       down_finish_tile(a, p, pc.tile, tid, 128, smem_flag);
     }
+    if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
     ++acc_it;
   }
+  if (tid == 0) trace_stamp(a, 2);
 }
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* ptr) {
@@ -655,6 +672,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = kTC ? *tmem_slot : 0u;
   const Plan plan = make_plan(a, kMode);
+  if (threadIdx.x == 0) trace_stamp(a, 0);
 
   // Let the next kernel in the stream get scheduled as SMs drain; it only
   // touches our outputs after its own griddepcontrol.wait.

@@ -47,7 +47,13 @@ struct StreamArgs {
   unsigned* flags;
   unsigned epoch;
   int mutant;
+  // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
+  // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
+  // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.
+  unsigned long long* trace;
 };
+
+constexpr int kTraceSlots = 64;
 
 // Smem bytes of one pipeline stage (weights + activation rows).
 __host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs) {

@@ -152,6 +152,7 @@ _sigs = {
     "dfk_event_elapsed_ms": ([_vp, _vp, C.POINTER(C.c_float)], C.c_int),
     "dfk_flush_l2": ([_vp], C.c_int),
     "dfk_launch_count": ([_vp, C.POINTER(_i64)], C.c_int),
+    "dfk_set_trace": ([_vp, _vp, _i64], C.c_int),
 }
 EXPORTED_SYMBOLS = tuple(_sigs)
 for _name, (_args, _res) in _sigs.items():
@@ -373,6 +374,13 @@ class Context:
 
     def weights(self, w_gate, w_up, w_down, ff_range=None) -> Weights:
         return Weights(self, w_gate, w_up, w_down, ff_range)
+
+    def set_trace(self, buf: Optional["DeviceArray"]):
+        """Enable (device buffer of uint64 stamps) or disable (None) tracing."""
+        if buf is None:
+            _check(lib.dfk_set_trace(self.h, None, 0))
+        else:
+            _check(lib.dfk_set_trace(self.h, buf.ptr, buf.nbytes // 8))
 
     def flush_l2(self):
         _check(lib.dfk_flush_l2(self.h))
