@@ -304,6 +304,43 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
   return DFK_OK;
 }
 
+// Work plan of the block kernel (see StreamArgs): stage-1 tiles round-robin,
+// then down units in two groups so that no CTA waits long on a stage-1 tile
+// that is still being computed.  Group A (K blocks whose stage-1 tile lies in
+// an early round-robin wave) goes to the CTAs with one tile fewer, group B
+// (last wave) is shared by everyone with byte-balanced budgets.
+void block_plan(int G, const dfk_weights_s* w, StreamArgs* a) {
+  const int T1 = w->s1_tiles, kb1 = w->s1_kblocks;
+  const int t2 = w->dn_tiles, kb2 = w->dn_kblocks;
+  const int q = T1 / G, r = T1 % G;
+  a->bp_r = r;
+  a->bp_L = G - r;
+  if (r > 0) {
+    a->bp_nA = q * G;
+    a->bp_nB = r;
+    a->bp_kB0 = q * G;
+  } else {  // every CTA owns q tiles: no early group
+    a->bp_nA = 0;
+    a->bp_nB = kb2;
+    a->bp_kB0 = 0;
+  }
+  const int64_t L = a->bp_L;
+  const int64_t A = static_cast<int64_t>(t2) * a->bp_nA;
+  const int64_t Bn = static_cast<int64_t>(t2) * a->bp_nB;
+  // Group B: uniform.
+  a->bp_bl = Bn / G;
+  a->bp_rB = Bn - a->bp_bl * G;
+  // Group A: total per CTA balanced, i.e. light ranks take kb1 more.
+  const int64_t WT = static_cast<int64_t>(T1) * kb1 + static_cast<int64_t>(t2) * kb2;
+  int64_t ah = (WT - static_cast<int64_t>(G) * (q + 1) * kb1 - Bn) / G;
+  if (ah < 0 || r == 0) ah = 0;
+  if (ah * r > A) ah = r > 0 ? A / r : 0;
+  const int64_t al = (A - ah * r) / L;
+  a->bp_ah = ah;
+  a->bp_al = al;
+  a->bp_rA = A - al * L - ah * r;
+}
+
 // The whole block in one persistent launch per batch chunk (kModeBlock).
 // Every CTA must be co-resident (down pieces spin on stage-1 tile flags), so
 // the grid never exceeds the SM count.
@@ -335,6 +372,9 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     a.mutant = cfg.mutant;
     int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : ctx->sm_count;
     grid = std::max(1, std::min(grid, ctx->sm_count));
+    block_plan(grid, w, &a);
+    if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
+      return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,
                                   grid, cfg.pdl != 0, ctx->stream);
     if (e != cudaSuccess)

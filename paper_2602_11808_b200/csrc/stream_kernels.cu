@@ -72,25 +72,24 @@ struct Piece {
 struct Plan {
   int mode;
   int G, c;
-  int n1;            // stage-1 tiles of this CTA
-  int rank;          // this CTA's rank in the down ordering
-  int64_t u0, u1;    // this CTA's down ordering range
-  int64_t U2;        // total down units
-  // Byte-balanced ranges (kModeBlock): start(k) closed form parameters.
-  int L;             // CTAs with the smaller stage-1 share (ranked first)
-  int64_t base, rem; // per-rank budget = base + (k < rem) + (k < L) * kb1
-  int split_case;    // 0: U2 > L*kb1 (formula above); 1: light ranks only
+  int n1;           // stage-1 tiles of this CTA
+  int rank;         // this CTA's rank (kModeDown: c; kModeBlock: light first)
+  int64_t a0, a1;   // kModeBlock group-A range of this CTA
+  int64_t u0, u1;   // down range (kModeDown: whole space; kModeBlock: group B)
+  int64_t U2;       // total down units
 };
 
-__device__ __forceinline__ int64_t plan_start(const StreamArgs& a, const Plan& p,
-                                              int64_t k) {
+// Group-B (or plain stream-K) range start of rank k.
+__device__ __forceinline__ int64_t start_b(const StreamArgs& a, const Plan& p,
+                                           int64_t k) {
   if (p.mode == kModeDown) return p.U2 * k / p.G;
-  if (p.split_case == 0) {
-    return k * p.base + (k < p.rem ? k : p.rem) +
-           (k < p.L ? k : static_cast<int64_t>(p.L)) * a.kb1;
-  }
-  const int64_t kk = k < p.L ? k : p.L;
-  return kk * p.base + (kk < p.rem ? kk : p.rem);
+  return k * a.bp_bl + (k < a.bp_rB ? k : a.bp_rB);
+}
+
+// Group-A range start of rank k (k in [0, G]).
+__device__ __forceinline__ int64_t start_a(const StreamArgs& a, int64_t k) {
+  const int64_t kl = k < a.bp_L ? k : a.bp_L;
+  return kl * a.bp_al + (k - kl) * a.bp_ah + (k < a.bp_rA ? k : a.bp_rA);
 }
 
 __device__ __forceinline__ Plan make_plan(const StreamArgs& a, int mode) {
@@ -99,81 +98,65 @@ __device__ __forceinline__ Plan make_plan(const StreamArgs& a, int mode) {
   p.G = gridDim.x;
   p.c = blockIdx.x;
   p.U2 = static_cast<int64_t>(a.t2) * a.kb2;
-  p.n1 = 0;
-  p.L = p.G;
-  p.base = p.rem = 0;
-  p.split_case = 0;
-  if (mode != kModeDown) {
-    p.n1 = p.c < a.t1 ? (a.t1 - 1 - p.c) / p.G + 1 : 0;
+  p.n1 = mode != kModeDown && p.c < a.t1 ? (a.t1 - 1 - p.c) / p.G + 1 : 0;
+  p.a0 = p.a1 = 0;
+  p.u0 = p.u1 = 0;
+  p.rank = p.c;
+  if (mode == kModeStage1) return p;
+  if (mode == kModeBlock) {
+    p.rank = p.c >= a.bp_r ? p.c - a.bp_r : a.bp_L + p.c;
+    p.a0 = start_a(a, p.rank);
+    p.a1 = start_a(a, p.rank + 1);
   }
-  if (mode == kModeStage1) {
-    p.rank = p.c;
-    p.u0 = p.u1 = 0;
-    return p;
-  }
-  if (mode == kModeDown) {
-    p.rank = p.c;
-  } else {
-    // Heavy CTAs (c < r) own one stage-1 tile more than light ones; light
-    // CTAs are ranked first in the down ordering and get kb1 more units.
-    const int r = a.t1 % p.G;
-    p.L = p.G - r;
-    p.rank = p.c >= r ? p.c - r : p.L + p.c;
-    const int64_t extra = p.U2 - static_cast<int64_t>(p.L) * a.kb1;
-    if (extra > 0) {
-      p.split_case = 0;
-      p.base = extra / p.G;
-      p.rem = extra - p.base * p.G;
-    } else {
-      p.split_case = 1;
-      p.base = p.U2 / p.L;
-      p.rem = p.U2 - p.base * p.L;
-    }
-  }
-  p.u0 = plan_start(a, p, p.rank);
-  p.u1 = plan_start(a, p, p.rank + 1);
+  p.u0 = start_b(a, p, p.rank);
+  p.u1 = start_b(a, p, p.rank + 1);
   return p;
-}
-
-// Ordering index u -> (tile, kb) and the end of its contiguous segment.
-__device__ __forceinline__ void down_unit(const StreamArgs& a, const Plan& p,
-                                          int64_t u, int* t, int* kb,
-                                          int64_t* seg_end) {
-  if (p.mode == kModeDown) {
-    *t = static_cast<int>(u / a.kb2);
-    *kb = static_cast<int>(u % a.kb2);
-    *seg_end = static_cast<int64_t>(*t + 1) * a.kb2;
-    return;
-  }
-  // Wave-major: wave w = stage-1 tiles [w*G, (w+1)*G) (round-robin wave).
-  const int64_t wave_units = static_cast<int64_t>(a.t2) * p.G;
-  const int w = static_cast<int>(u / wave_units);
-  const int64_t uw = u - w * wave_units;
-  const int nw = min(p.G, a.kb2 - w * p.G);
-  *t = static_cast<int>(uw / nw);
-  *kb = w * p.G + static_cast<int>(uw % nw);
-  *seg_end = w * wave_units + static_cast<int64_t>(*t + 1) * nw;
 }
 
 struct PieceIter {
   int i = 0;
+  int grp = 0;        // 0 = stage 1, 1 = group A, 2 = group B / stream-K
   int64_t u = -1;
   __device__ __forceinline__ bool next(const StreamArgs& a, const Plan& p,
                                        Piece& out) {
-    if (i < p.n1) {
-      out.down = 0;
-      out.tile = p.c + i * p.G;
-      out.kb0 = 0;
-      out.kb1 = a.kb1;
-      ++i;
-      return true;
+    if (grp == 0) {
+      if (i < p.n1) {
+        out.down = 0;
+        out.tile = p.c + i * p.G;
+        out.kb0 = 0;
+        out.kb1 = a.kb1;
+        ++i;
+        return true;
+      }
+      if (p.mode == kModeStage1) return false;
+      grp = p.mode == kModeBlock ? 1 : 2;
+      u = -1;
     }
-    if (p.mode == kModeStage1) return false;
+    if (grp == 1) {
+      if (u < 0) u = p.a0;
+      if (u < p.a1) {
+        const int t = static_cast<int>(u / a.bp_nA);
+        const int kb = static_cast<int>(u % a.bp_nA);
+        const int64_t seg_end = static_cast<int64_t>(t + 1) * a.bp_nA;
+        const int64_t end = seg_end < p.a1 ? seg_end : p.a1;
+        out.down = 1;
+        out.tile = t;
+        out.kb0 = kb;
+        out.kb1 = kb + static_cast<int>(end - u);
+        u = end;
+        ++i;
+        return true;
+      }
+      grp = 2;
+      u = -1;
+    }
     if (u < 0) u = p.u0;
     if (u >= p.u1) return false;
-    int t, kb;
-    int64_t seg_end;
-    down_unit(a, p, u, &t, &kb, &seg_end);
+    const int nseg = p.mode == kModeDown ? a.kb2 : a.bp_nB;
+    const int kofs = p.mode == kModeDown ? 0 : a.bp_kB0;
+    const int t = static_cast<int>(u / nseg);
+    const int kb = kofs + static_cast<int>(u % nseg);
+    const int64_t seg_end = static_cast<int64_t>(t + 1) * nseg;
     const int64_t end = seg_end < p.u1 ? seg_end : p.u1;
     out.down = 1;
     out.tile = t;
@@ -185,42 +168,44 @@ struct PieceIter {
   }
 };
 
-// Largest rank k with start(k) <= u.
-__device__ __forceinline__ int rank_of(const StreamArgs& a, const Plan& p,
-                                       int64_t u) {
-  int lo = 0, hi = p.G - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (plan_start(a, p, mid) <= u) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// Number of non-empty ranges intersecting [lo, hi).
-__device__ __forceinline__ int pieces_in(const StreamArgs& a, const Plan& p,
-                                         int64_t lo, int64_t hi) {
-  if (hi <= lo) return 0;
-  const int k0 = rank_of(a, p, lo), k1 = rank_of(a, p, hi - 1);
-  int n = 0;
+// Number of non-empty ranges [start(k), start(k+1)), k in [0, n), that
+// intersect [lo, hi); start is monotone.
+template <typename StartFn>
+__device__ __forceinline__ int pieces_in(StartFn start, int n, int64_t lo,
+                                         int64_t hi) {
+  if (hi <= lo || n <= 0) return 0;
+  // k0 = largest k with start(k) <= lo, k1 = largest k with start(k) <= hi-1.
+  auto rank_of = [&](int64_t u) {
+    int l = 0, h = n - 1;
+    while (l < h) {
+      const int mid = (l + h + 1) >> 1;
+      if (start(mid) <= u) l = mid; else h = mid - 1;
+    }
+    return l;
+  };
+  const int k0 = rank_of(lo), k1 = rank_of(hi - 1);
+  int cnt = 0;
   for (int k = k0; k <= k1; ++k)
-    if (plan_start(a, p, k + 1) > plan_start(a, p, k)) ++n;
-  return n;
+    if (start(k + 1) > start(k)) ++cnt;
+  return cnt;
 }
 
 // How many pieces (flushes) down tile t receives in total.
 __device__ __forceinline__ int down_tile_pieces(const StreamArgs& a,
                                                 const Plan& p, int t) {
+  auto sb = [&](int64_t k) { return start_b(a, p, k); };
   if (p.mode == kModeDown) {
     const int64_t lo = static_cast<int64_t>(t) * a.kb2;
-    return pieces_in(a, p, lo, lo + a.kb2);
+    return pieces_in(sb, p.G, lo, lo + a.kb2);
   }
   int n = 0;
-  const int64_t wave_units = static_cast<int64_t>(a.t2) * p.G;
-  for (int w = 0; w * p.G < a.kb2; ++w) {
-    const int nw = min(p.G, a.kb2 - w * p.G);
-    const int64_t lo = w * wave_units + static_cast<int64_t>(t) * nw;
-    n += pieces_in(a, p, lo, lo + nw);
+  if (a.bp_nA > 0) {
+    auto sa = [&](int64_t k) { return start_a(a, k); };
+    const int64_t lo = static_cast<int64_t>(t) * a.bp_nA;
+    n += pieces_in(sa, p.G, lo, lo + a.bp_nA);
   }
+  const int64_t lo = static_cast<int64_t>(t) * a.bp_nB;
+  n += pieces_in(sb, p.G, lo, lo + a.bp_nB);
   return n;
 }
 
@@ -267,19 +252,42 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
   named_bar(1, nthr);
   if (*smem_flag) {
     __threadfence();
+    // 128 columns x B rows, 4 consecutive floats per thread and iteration;
+    // loads are issued 4 deep before any store (the reads are L2 round trips).
     const int col0 = t * kDownCols;
-    for (int idx = tid; idx < a.B * kDownCols; idx += nthr) {
-      const int n = idx / kDownCols, j = col0 + idx % kDownCols;
-      if (j < a.out_cols) {
-        float* q = a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j;
-        const float v = __ldcg(q);
-        if (a.y_bf16) {
-          reinterpret_cast<__nv_bfloat16*>(a.y)[n * a.y_ld + j] =
-              __float2bfloat16_rn(v);
-        } else {
-          reinterpret_cast<float*>(a.y)[n * a.y_ld + j] = v;
+    const int nvec = a.B * (kDownCols / 4);
+    for (int base = tid; base < nvec; base += 4 * nthr) {
+      float4 v[4];
+      float4* q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * nthr;
+        q[u] = nullptr;
+        if (idx < nvec) {
+          const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
+          q[u] = reinterpret_cast<float4*>(a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j);
+          v[u] = __ldcg(q[u]);
         }
-        __stcg(q, 0.0f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * nthr;
+        if (idx < nvec) {
+          const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
+          const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (j + e < a.out_cols) {
+              if (a.y_bf16) {
+                reinterpret_cast<__nv_bfloat16*>(a.y)[n * a.y_ld + j + e] =
+                    __float2bfloat16_rn(vv[e]);
+              } else {
+                reinterpret_cast<float*>(a.y)[n * a.y_ld + j + e] = vv[e];
+              }
+            }
+          }
+          __stcg(q[u], make_float4(0.f, 0.f, 0.f, 0.f));
+        }
       }
     }
     if (tid == 0) a.counters[t] = 0;

@@ -47,6 +47,18 @@ struct StreamArgs {
   unsigned* flags;
   unsigned epoch;
   int mutant;
+  // kModeBlock plan (host-computed, block_plan in api.cu).  Stage-1 tiles go
+  // round-robin: CTAs c < r own q+1 tiles ("heavy"), the rest own q
+  // ("light").  Down units form two groups, each split over all G ranks
+  // (light CTA c has rank c - r, heavy CTA c has rank L + c):
+  //   A = K blocks [0, kB0) whose stage-1 tile is in an early wave: t-major
+  //       segments of nA units; light ranks get al, heavy ah (al - ah = one
+  //       stage-1 tile of K blocks), +1 for the first rA ranks;
+  //   B = K blocks [kB0, kb2) of the last wave: t-major segments of nB
+  //       units, bl per rank, +1 for the first rB ranks.
+  // A CTA runs its stage-1 tiles, then its A range, then its B range.
+  int bp_r, bp_L, bp_nA, bp_nB, bp_kB0;
+  int64_t bp_al, bp_ah, bp_rA, bp_bl, bp_rB;
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.

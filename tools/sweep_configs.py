@@ -39,7 +39,7 @@ for B in [int(b) for b in a.batches.split(",")]:
     fams = [rt.FAMILY_TC] + ([rt.FAMILY_GEMV] if B <= 8 else [])
     res = []
     if "s1" in what:
-        for fam, kbs, st, ctas in itertools.product(fams, (1, 2, 3), (0, 3, 4), (0, 112, 296)):
+        for fam, kbs, st, ctas in itertools.product(fams, (2, 3, 4), (0,), (0, 112)):
             cfg = rt.Config.make(s1_family=fam, kbs=kbs, s1_stages=st, s1_ctas=ctas)
             try:
                 us = timeit(lambda i: ctx.stage1(sets[i % len(sets)], x, a2, cfg=cfg))
@@ -48,17 +48,17 @@ for B in [int(b) for b in a.batches.split(",")]:
             res.append(("s1", fam, kbs, st, ctas, us, s1b(B) / us / 1e3))
     if "down" in what:
         ctx.stage1(sets[0], x, a2)
-        for fam, kbs, st, ctas in itertools.product(fams, (1, 2, 3), (0, 4), (0, 296)):
+        for fam, kbs, st, ctas in itertools.product(fams, (2, 3, 4), (0,), (74, 96, 112, 0)):
             cfg = rt.Config.make(down_family=fam, kbs=kbs, down_stages=st, down_ctas=ctas)
             us = timeit(lambda i: ctx.down(sets[i % len(sets)], a2, y, cfg=cfg))
             res.append(("down", fam, kbs, st, ctas, us, dnb(B) / us / 1e3))
     if "block" in what:
-        for fam, kbs, st in itertools.product(fams, (1, 2, 3), (0, 3, 4)):
+        for fam, kbs, st in itertools.product(fams, (2, 3, 4), (0,)):
             cfg = rt.Config.make(block_kernel=1, s1_family=fam, down_family=fam, kbs=kbs, s1_stages=st)
             us = timeit(lambda i: ctx.forward(sets[i % len(sets)], x, y, cfg=cfg))
             res.append(("block", fam, kbs, st, 0, us, (s1b(B) + dnb(B)) / us / 1e3))
     if "fwd" in what:
-        for fam, kbs, pdl in itertools.product(fams, (1, 2), (0, 1)):
+        for fam, kbs, pdl in itertools.product(fams, (2, 3), (1,)):
             cfg = rt.Config.make(s1_family=fam, down_family=rt.FAMILY_TC, kbs=kbs, pdl=pdl)
             us = timeit(lambda i: ctx.forward(sets[i % len(sets)], x, y, cfg=cfg))
             res.append(("fwd", fam, kbs, pdl, 0, us, (s1b(B) + dnb(B)) / us / 1e3))
