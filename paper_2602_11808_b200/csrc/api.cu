@@ -151,11 +151,23 @@ int max_stages(dfk_context_s* ctx, int n_pad, int kbs) {
   return std::min(s, 32);
 }
 
-// 32 KiB ring stages stream fastest (tools/stream_probe.cu); fall back to
-// 16 KiB when a 32 KiB stage would leave fewer than 4 slots.
+// Bigger ring stages stream faster (tools/stream_probe.cu, profiles/): take
+// the largest stage (up to 4 x 16 KiB weight blocks) that still leaves 3
+// slots in shared memory.
 int pick_kbs(dfk_context_s* ctx, int n_pad, int requested) {
   if (requested > 0) return std::min(requested, 4);
-  return max_stages(ctx, n_pad, 2) >= 4 ? 2 : 1;
+  for (int kbs = 4; kbs > 1; --kbs)
+    if (max_stages(ctx, n_pad, kbs) >= 3) return kbs;
+  return 1;
+}
+
+// Persistent stage-1 grid: as many CTAs as keep every CTA at the same tile
+// count (224 tiles on 148 SMs -> 112 CTAs x 2 tiles): per-SM bandwidth
+// scales with bytes in flight, so fewer, evenly loaded CTAs beat a ragged
+// last wave.
+int balanced_grid(int tiles, int sms) {
+  const int waves = (tiles + sms - 1) / sms;
+  return (tiles + waves - 1) / waves;
 }
 
 int gemv_nb(int64_t b) {
@@ -262,7 +274,7 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     a.mutant = cfg.mutant;
-    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : ctx->sm_count;
+    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : balanced_grid(w->s1_tiles, ctx->sm_count);
     grid = std::max(1, std::min(grid, w->s1_tiles));
     cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
                                   grid, cfg.pdl != 0, ctx->stream);

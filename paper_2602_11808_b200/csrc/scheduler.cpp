@@ -89,10 +89,12 @@ dfk_config make_cfg(int variant, int s1f, int dnf, int kbs, int block,
   return c;
 }
 
-// The GPU candidate grid: the two unfused cuBLASLt layouts, the two-kernel
-// fused path (stage-1 family x down family x stage size) and the single
-// persistent block kernel (family x stage size), plus one no-PDL control.
-std::vector<dfk_config> candidates(int64_t B) {
+// The GPU candidate grid: the two unfused cuBLASLt layouts, the single
+// persistent block kernel (per family), the two-kernel fused path (stage-1
+// family x down family x down grid), plus one no-PDL control.  Stage sizes
+// and the stage-1 grid use the library's defaults (pick_kbs, balanced_grid),
+// which were themselves chosen from measured sweeps (profiles/).
+std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
   std::vector<dfk_config> out;
   out.push_back(make_cfg(DFK_VARIANT_FOUR_KERNEL, 0, 0, 0, 0, 0));
   out.push_back(make_cfg(DFK_VARIANT_TWO_KERNEL, 0, 0, 0, 0, 0));
@@ -102,11 +104,17 @@ std::vector<dfk_config> candidates(int64_t B) {
   auto add = [&](const dfk_config& c) {
     if (seen.insert(c.label).second) out.push_back(c);
   };
-  for (int kbs : {0, 1}) {
-    for (int f : fams) add(make_cfg(DFK_VARIANT_FUSED, f, f, kbs, 1, 1));
-    for (int s1f : fams)
-      for (int dnf : fams) add(make_cfg(DFK_VARIANT_FUSED, s1f, dnf, kbs, 0, 1));
-  }
+  for (int f : fams) add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
+  const int dn_ctas[2] = {0, ctx->sm_count * 3 / 4};
+  for (int s1f : fams)
+    for (int dnf : fams)
+      for (int dc : dn_ctas) {
+        dfk_config c = make_cfg(DFK_VARIANT_FUSED, s1f, dnf, 0, 0, 1);
+        c.down_ctas = dc;
+        std::snprintf(c.label, sizeof(c.label), "%s", "");
+        std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+        add(c);
+      }
   add(make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 0, 0));
   return out;
 }
@@ -299,7 +307,7 @@ int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
                    dfk_config* out, int32_t cap, int32_t* n) {
   if (!ctx || !w || !n) return fail(DFK_ERR_INVALID, "null argument");
   if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
-  const auto c = candidates(batch);
+  const auto c = candidates(ctx, batch);
   *n = static_cast<int32_t>(c.size());
   for (int32_t i = 0; i < std::min<int32_t>(cap, *n); ++i) out[i] = c[i];
   return DFK_OK;
@@ -378,7 +386,7 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   std::vector<Result> results;
-  for (const dfk_config& c : candidates(batch)) {
+  for (const dfk_config& c : candidates(ctx, batch)) {
     Result r;
     r.cfg = c;
     r.label = c.label;

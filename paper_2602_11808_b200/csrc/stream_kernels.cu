@@ -306,99 +306,98 @@ __device__ __forceinline__ void s1_publish(const StreamArgs& a, int tile,
 }
 
 // ---------------------------------------------------------------------------
-// Producer (one lane).
+// Producer (all of warp 0; lane 0 issues the copies).  In kModeBlock the
+// warp checks the stage-1 completion flags a down piece depends on
+// cooperatively (32 acquire loads in flight), once per piece.
 // ---------------------------------------------------------------------------
+struct ReadyCache {
+  int lo = 0, hi = 0;  // flags of stage-1 tiles [lo, hi) known published
+};
+
+__device__ __forceinline__ void ensure_ready(const StreamArgs& a,
+                                            ReadyCache& rc, int lo, int hi) {
+  if (!a.flags || (lo >= rc.lo && hi <= rc.hi)) return;
+  const int lane = static_cast<int>(lane_id());
+  for (int j = lo + lane; j < hi; j += 32) {
+    while (ld_acquire(a.flags + j) != a.epoch) {
+    }
+  }
+  __syncwarp();
+  fence_proxy_async_global();
+  rc.lo = lo;
+  rc.hi = hi;
+}
+
 __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                                         const CUtensorMap* xmap,
                                         const CUtensorMap* amap, uint8_t* smem,
                                         int stage_bytes, uint64_t* full,
                                         uint64_t* empty) {
+  const bool leader = lane_id() == 0;
   const uint64_t policy = policy_evict_first();
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
   const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
   struct Pend {
-    int kb, nb, down;
+    int kb, nb, down, pk0, pk1;
   };
   Pend pend[32];
+  ReadyCache rc;
   int64_t it = 0;
   bool waited = false;
   PieceIter pi;
   Piece pc;
+  auto act_loads = [&](uint8_t* xs, int kb, int nb, int down, uint64_t* bar) {
+    if (!leader) return;
+    for (int b = 0; b < nb; ++b) {
+      tma_load_2d(xs + b * xblk, down ? amap : xmap, (kb + b) * kBlockK, 0, bar);
+    }
+  };
   while (pi.next(a, p, pc)) {
-    trace_stamp(a, 1 + 2 * pi.i);
+    if (leader) trace_stamp(a, 1 + 2 * pi.i);
     const uint8_t* wbase = pc.down ? a.w2 : a.w1;
     const int kbt = pc.down ? a.kb2 : a.kb1;
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
       const int slot = static_cast<int>(it % a.stages);
       const uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
-      if (it >= a.stages) mbar_wait(&empty[slot], phase ^ 1u);
+      if (it >= a.stages) {
+        if (leader) mbar_wait(&empty[slot], phase ^ 1u);
+        __syncwarp();
+      }
       uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
-      mbar_arrive_expect_tx(&full[slot],
-                            static_cast<uint32_t>(nb) * (kBlockBytes + xblk));
-      // nb consecutive K blocks of one tile are contiguous in the pack.
-      bulk_g2s(st,
-               wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
-                           static_cast<int64_t>(kBlockBytes),
-               static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
+      if (leader) {
+        mbar_arrive_expect_tx(&full[slot],
+                              static_cast<uint32_t>(nb) * (kBlockBytes + xblk));
+        // nb consecutive K blocks of one tile are contiguous in the pack.
+        bulk_g2s(st,
+                 wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
+                             static_cast<int64_t>(kBlockBytes),
+                 static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
+      }
       if (!waited) {
-        pend[it] = {kb, nb, pc.down};
+        pend[it] = {kb, nb, pc.down, pc.kb0, pc.kb1};
         if (it + 1 < a.stages) continue;  // keep prefetching weights
         pdl_wait();
         waited = true;
         for (int j = 0; j <= it; ++j) {
-          uint8_t* sj = smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all;
-          for (int b = 0; b < pend[j].nb; ++b) {
-            const int kbb = pend[j].kb + b;
-            if (pend[j].down) {
-              if (a.flags) {
-                while (ld_acquire(a.flags + kbb) != a.epoch) {
-                }
-                fence_proxy_async_global();
-              }
-              tma_load_2d(sj + b * xblk, amap, kbb * kBlockK, 0, &full[j]);
-            } else {
-              tma_load_2d(sj + b * xblk, xmap, kbb * kBlockK, 0, &full[j]);
-            }
-          }
+          if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
+          act_loads(smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all,
+                    pend[j].kb, pend[j].nb, pend[j].down, &full[j]);
         }
         continue;
       }
-      uint8_t* xs = st + wbytes_all;
-      for (int b = 0; b < nb; ++b) {
-        const int kbb = kb + b;
-        if (pc.down) {
-          if (a.flags) {
-            while (ld_acquire(a.flags + kbb) != a.epoch) {
-            }
-            fence_proxy_async_global();
-          }
-          tma_load_2d(xs + b * xblk, amap, kbb * kBlockK, 0, &full[slot]);
-        } else {
-          tma_load_2d(xs + b * xblk, xmap, kbb * kBlockK, 0, &full[slot]);
-        }
-      }
+      if (pc.down) ensure_ready(a, rc, pc.kb0, pc.kb1);
+      act_loads(st + wbytes_all, kb, nb, pc.down, &full[slot]);
     }
   }
-  trace_stamp(a, 1);
+  if (leader) trace_stamp(a, 1);
   if (!waited) {
     // Fewer stages of work than ring slots: flush the deferred loads.
     pdl_wait();
     for (int j = 0; j < it; ++j) {
-      uint8_t* sj = smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all;
-      for (int b = 0; b < pend[j].nb; ++b) {
-        const int kbb = pend[j].kb + b;
-        if (pend[j].down) {
-          if (a.flags) {
-            while (ld_acquire(a.flags + kbb) != a.epoch) {
-            }
-            fence_proxy_async_global();
-          }
-          tma_load_2d(sj + b * xblk, amap, kbb * kBlockK, 0, &full[j]);
-        } else {
-          tma_load_2d(sj + b * xblk, xmap, kbb * kBlockK, 0, &full[j]);
-        }
-      }
+      if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
+      act_loads(smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all,
+                pend[j].kb, pend[j].nb, pend[j].down, &full[j]);
     }
   }
 }
@@ -687,8 +686,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   pdl_launch_dependents();
 
   if (w == 0) {
-    if (lane_id() == 0)
-      produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty);
+    produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty);
   } else if constexpr (kTC) {
     if (w == 1) {
       if (lane_id() == 0)
