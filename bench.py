@@ -289,7 +289,7 @@ def main():
 
     # ---- per-batch µs/call (fused, scheduler pick) and the unfused comparator ----
     def time_calls(B, cfg, n, fn=None):
-        for i in range(2):
+        for i in range(len(sets)):  # touch every weight set (lazy comparator prep)
             (fn or call)(B, i, cfg)
         barrier()
         ctx.sync()

@@ -12,6 +12,7 @@ ap.add_argument("--batches", default="1,16,64")
 ap.add_argument("--sets", type=int, default=3)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--what", default="s1,down,block,fwd")
+ap.add_argument("--specs", default="", help="';'-separated kind:k=v,... (kind s1|down|block|fwd|two)")
 a = ap.parse_args()
 DM, DF = a.dm, a.df
 ctx = rt.Context(0)
@@ -66,7 +67,27 @@ for B in [int(b) for b in a.batches.split(",")]:
             cfg = rt.Config.make(variant=v)
             us = timeit(lambda i: ctx.forward(sets[i % len(sets)], x, y, cfg=cfg))
             res.append(("cublas", 0, 0, 0, 0, us, (s1b(B) + dnb(B)) / us / 1e3))
+    for spec in [t for t in a.specs.split(";") if t]:
+        kind, _, kv = spec.partition(":")
+        kw = {k: int(v) for k, v in (p.split("=") for p in kv.split(",") if p)}
+        if kind == "block":
+            kw["block_kernel"] = 1
+        if kind == "two":
+            kw["variant"] = rt.VARIANT_TWO_KERNEL
+        cfg = rt.Config.make(**kw)
+        if kind == "s1":
+            fn, nb = (lambda i: ctx.stage1(sets[i % len(sets)], x, a2, cfg=cfg)), s1b(B)
+        elif kind == "down":
+            ctx.stage1(sets[0], x, a2)
+            fn, nb = (lambda i: ctx.down(sets[i % len(sets)], a2, y, cfg=cfg)), dnb(B)
+        else:
+            fn, nb = (lambda i: ctx.forward(sets[i % len(sets)], x, y, cfg=cfg)), s1b(B) + dnb(B)
+        us = timeit(fn)
+        res.append((kind, kv, "", "", 0, us, nb / us / 1e3))
     print(f"=== B={B}")
     for r in res:
-        print(f"  {r[0]:6s} fam={r[1]} kbs={r[2]} st={r[3]} ctas={r[4]:3d}  {r[5]:8.2f} us  {r[6]:7.1f} GB/s")
+        if isinstance(r[1], str):
+            print(f"  {r[0]:6s} {r[1]:40s}  {r[5]:8.2f} us  {r[6]:7.1f} GB/s")
+        else:
+            print(f"  {r[0]:6s} fam={r[1]} kbs={r[2]} st={r[3]} ctas={r[4]:3d}  {r[5]:8.2f} us  {r[6]:7.1f} GB/s")
     sys.stdout.flush()
