@@ -303,7 +303,9 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
                      w->d_ff, nb, a_ld, a.n_pad, &tm));
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
-    int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count;
+    // Default: 3/4 of the SMs with deep rings streams faster than every SM
+    // with the same ring (measured, profiles/sweeps_r1.md).
+    int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count * 3 / 4;
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, U));
     cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
                                   static_cast<int>(grid), cfg.pdl != 0,
@@ -382,7 +384,8 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     if (++ctx->epoch == 0) ++ctx->epoch;
     a.epoch = ctx->epoch;
     a.mutant = cfg.mutant;
-    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : ctx->sm_count;
+    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas
+                               : balanced_grid(w->s1_tiles, ctx->sm_count);
     grid = std::max(1, std::min(grid, ctx->sm_count));
     block_plan(grid, w, &a);
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)

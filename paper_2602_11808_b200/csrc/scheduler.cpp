@@ -105,7 +105,7 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
     if (seen.insert(c.label).second) out.push_back(c);
   };
   for (int f : fams) add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
-  const int dn_ctas[2] = {0, ctx->sm_count * 3 / 4};
+  const int dn_ctas[2] = {0, ctx->sm_count};  // 0 = library default (3/4 SMs)
   for (int s1f : fams)
     for (int dnf : fams)
       for (int dc : dn_ctas) {
