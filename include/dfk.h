@@ -109,7 +109,11 @@ typedef struct dfk_config {
                            flags (the paper's single deeply fused kernel);
                            0 = two kernels (stage 1, then down)          */
   int32_t kbs;          /* 16 KiB weight blocks per pipeline stage (0 = auto) */
-  int32_t reserved[4];
+  int32_t dynamic_sched;/* 1 = CTAs pull work pieces from an atomic counter
+                           (tiles, then fixed-size down chunks) instead of
+                           the static byte-balanced plan                    */
+  int32_t chunk_kb;     /* K blocks per dynamic down chunk (0 = auto)      */
+  int32_t reserved[2];
   char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
 } dfk_config;
 

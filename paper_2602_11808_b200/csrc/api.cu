@@ -76,11 +76,13 @@ std::string config_label(const dfk_config& c) {
   if (c.variant == DFK_VARIANT_TWO_KERNEL) return "two_kernel_cublaslt";
   if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
   if (c.block_kernel) {
+    if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
       << (c.pdl ? "_pdl" : "");
     return o.str();
   }
+  if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
   o << "fused_s1" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
     << c.s1_stages << "_c" << c.s1_ctas << "_dn"
     << (c.down_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
@@ -218,6 +220,17 @@ Launch launch_shape(int family) {
   return {tc, tc ? 256 : 8};
 }
 
+int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
+                 StreamArgs* a) {
+  if (!cfg.dynamic_sched) return DFK_OK;
+  DFK_TRY(ensure_buf(ctx->sched, 64, true, ctx->stream));
+  a->dynamic = 1;
+  a->sched = static_cast<int*>(ctx->sched.p);
+  a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb
+                                 : std::max(1, std::min(w->dn_kblocks, 32));
+  return DFK_OK;
+}
+
 void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
                  int stages_req, int kbs_req, StreamArgs* a) {
   const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
@@ -274,6 +287,7 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     a.mutant = cfg.mutant;
+    DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
     int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : balanced_grid(w->s1_tiles, ctx->sm_count);
     grid = std::max(1, std::min(grid, w->s1_tiles));
     cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
@@ -302,6 +316,7 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
                      w->d_ff, nb, a_ld, a.n_pad, &tm));
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
+    DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
     // Default: 3/4 of the SMs with deep rings streams faster than every SM
     // with the same ring (measured, profiles/sweeps_r1.md).
@@ -388,6 +403,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
                                : balanced_grid(w->s1_tiles, ctx->sm_count);
     grid = std::max(1, std::min(grid, ctx->sm_count));
     block_plan(grid, w, &a);
+    DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,
@@ -681,7 +697,7 @@ int dfk_context_destroy(dfk_context ctx) {
   if (!ctx) return DFK_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc, &ctx->flags,
+  for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc, &ctx->flags, &ctx->sched,
                        &ctx->counters, &ctx->concat, &ctx->tmp1, &ctx->tmp2,
                        &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev}) {
     if (b->p) cudaFree(b->p);

@@ -68,6 +68,7 @@ struct dfk_context_s {
   dfk::DeviceBuf yacc;     // fp32 down accumulator (kept all-zero)
   dfk::DeviceBuf counters; // per-tile down arrival counters (kept zero)
   dfk::DeviceBuf flags;    // per-stage-1-tile completion flags (block kernel)
+  dfk::DeviceBuf sched;    // dynamic-scheduler counters (kept zero between launches)
   unsigned epoch = 0;      // block-kernel launch epoch (flag value)
   unsigned long long* trace = nullptr;  // dfk_set_trace buffer
   int64_t trace_slots = 0;

@@ -104,7 +104,14 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
   auto add = [&](const dfk_config& c) {
     if (seen.insert(c.label).second) out.push_back(c);
   };
-  for (int f : fams) add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
+  for (int f : fams) {
+    add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
+    dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
+    d.dynamic_sched = 1;
+    std::snprintf(d.label, sizeof(d.label), "%s", "");
+    std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
+    add(d);
+  }
   const int dn_ctas[2] = {0, ctx->sm_count};  // 0 = library default (3/4 SMs)
   for (int s1f : fams)
     for (int dnf : fams)
@@ -125,7 +132,8 @@ json cfg_to_json(const dfk_config& c) {
               {"s1_stages", c.s1_stages},     {"s1_ctas", c.s1_ctas},
               {"s1_split_k", c.s1_split_k},   {"down_family", c.down_family},
               {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
-              {"pdl", c.pdl},                 {"label", std::string(c.label)}};
+              {"pdl", c.pdl},                 {"dynamic_sched", c.dynamic_sched},
+              {"chunk_kb", c.chunk_kb},       {"label", std::string(c.label)}};
 }
 
 template <typename T>
@@ -154,6 +162,8 @@ dfk_config cfg_from_json(const json& j) {
   c.pdl = get_field<int>(j, "pdl");
   c.block_kernel = get_field<int>(j, "block_kernel");
   c.kbs = get_field<int>(j, "kbs");
+  c.dynamic_sched = get_field<int>(j, "dynamic_sched");
+  c.chunk_kb = get_field<int>(j, "chunk_kb");
   std::snprintf(c.label, sizeof(c.label), "%s",
                 get_field<std::string>(j, "label").c_str());
   return c;

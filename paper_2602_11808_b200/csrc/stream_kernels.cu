@@ -168,6 +168,79 @@ struct PieceIter {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Dynamic scheduling: piece index -> piece, and the smem piece queue that
+// carries the producer's choices to the MMA / epilogue / math warps.
+// ---------------------------------------------------------------------------
+struct PieceQueue {
+  int4 q[kPieceQueue];
+  uint64_t full[kPieceQueue];
+  uint64_t empty[kPieceQueue];
+};
+
+__device__ __forceinline__ int dyn_chunks(const StreamArgs& a) {
+  return (a.kb2 + a.chunk_kb - 1) / a.chunk_kb;
+}
+
+__device__ __forceinline__ bool decode_dyn(const StreamArgs& a, int mode,
+                                           int64_t idx, Piece& out) {
+  const int64_t n1 = mode != kModeDown ? a.t1 : 0;
+  const int64_t n2 =
+      mode != kModeStage1 ? static_cast<int64_t>(a.t2) * dyn_chunks(a) : 0;
+  if (idx < n1) {
+    out.down = 0;
+    out.tile = static_cast<int>(idx);
+    out.kb0 = 0;
+    out.kb1 = a.kb1;
+    return true;
+  }
+  idx -= n1;
+  if (idx >= n2) return false;
+  const int kc = static_cast<int>(idx / a.t2);
+  out.down = 1;
+  out.tile = static_cast<int>(idx % a.t2);
+  out.kb0 = kc * a.chunk_kb;
+  out.kb1 = min(a.kb2, out.kb0 + a.chunk_kb);
+  return true;
+}
+
+// The consumers' view of the piece sequence (static plan or queue).
+struct PieceReader {
+  int i = 0;
+  PieceIter it;
+  // single: the calling thread alone consumes the slot; otherwise the whole
+  // warp calls and lane 0 releases it.
+  __device__ __forceinline__ bool next(const StreamArgs& a, const Plan& p,
+                                       PieceQueue* pq, bool single,
+                                       Piece& out) {
+    if (!a.dynamic) {
+      const bool ok = it.next(a, p, out);
+      if (ok) ++i;
+      return ok;
+    }
+    const int slot = i % kPieceQueue;
+    mbar_wait(&pq->full[slot], static_cast<uint32_t>((i / kPieceQueue) & 1));
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(&pq->q[slot]))
+                 : "memory");
+    if (single) {
+      mbar_arrive(&pq->empty[slot]);
+    } else {
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&pq->empty[slot]);
+    }
+    ++i;
+    if (v.w < 0) return false;
+    out.tile = v.x;
+    out.kb0 = v.y;
+    out.kb1 = v.z;
+    out.down = v.w;
+    return true;
+  }
+};
+
 // Number of non-empty ranges [start(k), start(k+1)), k in [0, n), that
 // intersect [lo, hi); start is monotone.
 template <typename StartFn>
@@ -193,6 +266,7 @@ __device__ __forceinline__ int pieces_in(StartFn start, int n, int64_t lo,
 // How many pieces (flushes) down tile t receives in total.
 __device__ __forceinline__ int down_tile_pieces(const StreamArgs& a,
                                                 const Plan& p, int t) {
+  if (a.dynamic) return dyn_chunks(a);
   auto sb = [&](int64_t k) { return start_b(a, p, k); };
   if (p.mode == kModeDown) {
     const int64_t lo = static_cast<int64_t>(t) * a.kb2;
@@ -332,7 +406,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                                         const CUtensorMap* xmap,
                                         const CUtensorMap* amap, uint8_t* smem,
                                         int stage_bytes, uint64_t* full,
-                                        uint64_t* empty) {
+                                        uint64_t* empty, PieceQueue* pq) {
   const bool leader = lane_id() == 0;
   const uint64_t policy = policy_evict_first();
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
@@ -341,19 +415,56 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     int kb, nb, down, pk0, pk1;
   };
   Pend pend[32];
+  int npend = 0;
   ReadyCache rc;
   int64_t it = 0;
   bool waited = false;
   PieceIter pi;
-  Piece pc;
   auto act_loads = [&](uint8_t* xs, int kb, int nb, int down, uint64_t* bar) {
     if (!leader) return;
     for (int b = 0; b < nb; ++b) {
       tma_load_2d(xs + b * xblk, down ? amap : xmap, (kb + b) * kBlockK, 0, bar);
     }
   };
-  while (pi.next(a, p, pc)) {
-    if (leader) trace_stamp(a, 1 + 2 * pi.i);
+  // griddepcontrol.wait, then the activation loads deferred so far.
+  auto release_deferred = [&]() {
+    if (waited) return;
+    pdl_wait();
+    waited = true;
+    for (int j = 0; j < npend; ++j) {
+      if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
+      act_loads(smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all,
+                pend[j].kb, pend[j].nb, pend[j].down, &full[j]);
+    }
+  };
+  for (int qi = 0;; ++qi) {
+    Piece pc;
+    bool valid;
+    if (!a.dynamic) {
+      valid = pi.next(a, p, pc);
+    } else {
+      int64_t idx = blockIdx.x;
+      if (qi > 0) {
+        release_deferred();  // no global atomics before the previous grid ends
+        int got = 0;
+        if (leader) got = atomicAdd(a.sched, 1);
+        idx = static_cast<int64_t>(gridDim.x) + __shfl_sync(0xffffffffu, got, 0);
+      }
+      valid = decode_dyn(a, p.mode, idx, pc);
+      const int slot = qi % kPieceQueue;
+      if (qi >= kPieceQueue) {
+        if (leader)
+          mbar_wait(&pq->empty[slot],
+                    static_cast<uint32_t>(((qi / kPieceQueue) & 1) ^ 1));
+        __syncwarp();
+      }
+      if (leader) {
+        pq->q[slot] = make_int4(pc.tile, pc.kb0, pc.kb1, valid ? pc.down : -1);
+        mbar_arrive(&pq->full[slot]);
+      }
+    }
+    if (!valid) break;
+    if (leader) trace_stamp(a, 3 + 2 * qi);
     const uint8_t* wbase = pc.down ? a.w2 : a.w1;
     const int kbt = pc.down ? a.kb2 : a.kb1;
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
@@ -375,15 +486,8 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                  static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
       }
       if (!waited) {
-        pend[it] = {kb, nb, pc.down, pc.kb0, pc.kb1};
-        if (it + 1 < a.stages) continue;  // keep prefetching weights
-        pdl_wait();
-        waited = true;
-        for (int j = 0; j <= it; ++j) {
-          if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
-          act_loads(smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all,
-                    pend[j].kb, pend[j].nb, pend[j].down, &full[j]);
-        }
+        pend[npend++] = {kb, nb, pc.down, pc.kb0, pc.kb1};
+        if (it + 1 >= a.stages) release_deferred();  // ring full of weights
         continue;
       }
       if (pc.down) ensure_ready(a, rc, pc.kb0, pc.kb1);
@@ -391,15 +495,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     }
   }
   if (leader) trace_stamp(a, 1);
-  if (!waited) {
-    // Fewer stages of work than ring slots: flush the deferred loads.
-    pdl_wait();
-    for (int j = 0; j < it; ++j) {
-      if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
-      act_loads(smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all,
-                pend[j].kb, pend[j].nb, pend[j].down, &full[j]);
-    }
-  }
+  release_deferred();  // fewer stages of work than ring slots
 }
 
 // ---------------------------------------------------------------------------
@@ -417,7 +513,7 @@ template <int NB>
 __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
                                              uint8_t* smem, int stage_bytes,
                                              uint64_t* full, uint64_t* empty,
-                                             int* smem_flag) {
+                                             int* smem_flag, PieceQueue* pq) {
   const int mw = static_cast<int>(warp_id()) - 1;
   const int lane = static_cast<int>(lane_id());
   const int q = lane >> 3, c = lane & 7;
@@ -426,9 +522,9 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
   const int wbytes_all = a.kbs * kBlockBytes;
   const int xblk = a.n_pad * 128;
   int64_t it = 0;
-  PieceIter pi;
+  PieceReader pi;
   Piece pc;
-  while (pi.next(a, p, pc)) {
+  while (pi.next(a, p, pq, false, pc)) {
     float acc[4][NB];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -526,15 +622,15 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
                                           uint8_t* smem, int stage_bytes,
                                           uint64_t* full, uint64_t* empty,
                                           uint64_t* tfull, uint64_t* tempty,
-                                          uint32_t tmem_base) {
+                                          uint32_t tmem_base, PieceQueue* pq) {
   const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>(a.n_pad));
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
   const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
   int64_t it = 0;
   int acc_it = 0;
-  PieceIter pi;
+  PieceReader pi;
   Piece pc;
-  while (pi.next(a, p, pc)) {
+  while (pi.next(a, p, pq, true, pc)) {
     const int ab = acc_it & 1;
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tempty[ab], aph ^ 1u);
@@ -571,16 +667,16 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
 __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
                                             uint64_t* tfull, uint64_t* tempty,
                                             uint32_t tmem_base,
-                                            int* smem_flag) {
+                                            int* smem_flag, PieceQueue* pq) {
   const int w = static_cast<int>(warp_id());
   const int quarter = w & 3;
   const int lane = static_cast<int>(lane_id());
   const int row = quarter * 32 + lane;
   const int tid = (w - 2) * 32 + lane;
   int acc_it = 0;
-  PieceIter pi;
+  PieceReader pi;
   Piece pc;
-  while (pi.next(a, p, pc)) {
+  while (pi.next(a, p, pq, false, pc)) {
     const int ab = acc_it & 1;
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tfull[ab], aph);
@@ -652,7 +748,9 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  PieceQueue* pq = reinterpret_cast<PieceQueue*>(
+      (reinterpret_cast<uintptr_t>(tempty + 2) + 15) & ~static_cast<uintptr_t>(15));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pq + 1);
   int* smem_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const uint32_t w = warp_id();
@@ -666,6 +764,10 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
+    }
+    for (int i = 0; i < kPieceQueue; ++i) {
+      mbar_init(&pq->full[i], 1);
+      mbar_init(&pq->empty[i], kTC ? 5 : kGemvWarps);
     }
     fence_barrier_init();
   }
@@ -686,20 +788,29 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   pdl_launch_dependents();
 
   if (w == 0) {
-    produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty);
+    produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty, pq);
   } else if constexpr (kTC) {
     if (w == 1) {
       if (lane_id() == 0)
         mma_issue(a, plan, smem, stage_bytes, full, empty, tfull, tempty,
-                  tmem_base);
+                  tmem_base, pq);
     } else {
-      tc_epilogue(a, plan, tfull, tempty, tmem_base, smem_flag);
+      tc_epilogue(a, plan, tfull, tempty, tmem_base, smem_flag, pq);
     }
   } else {
-    gemv_consume<NB>(a, plan, smem, stage_bytes, full, empty, smem_flag);
+    gemv_consume<NB>(a, plan, smem, stage_bytes, full, empty, smem_flag, pq);
   }
 
   __syncthreads();
+  if (a.dynamic && threadIdx.x == 0) {
+    // The last CTA out re-arms the work counter for the next launch.
+    __threadfence();
+    if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      a.sched[0] = 0;
+      a.sched[1] = 0;
+      __threadfence();
+    }
+  }
   if constexpr (kTC) {
     if (w == 1) {
       __syncwarp();
@@ -755,7 +866,8 @@ cudaError_t launch_mode(bool tc, int nb, const CUtensorMap& xmap,
 }  // namespace
 
 int stream_smem_bytes(int n_pad, int stages, int kbs) {
-  return 1024 + stages * stream_stage_bytes(n_pad, kbs) + (2 * stages + 4) * 8 + 16;
+  return 1024 + stages * stream_stage_bytes(n_pad, kbs) + (2 * stages + 4) * 8 +
+         static_cast<int>(sizeof(PieceQueue)) + 32;
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv,

@@ -59,6 +59,15 @@ struct StreamArgs {
   // A CTA runs its stage-1 tiles, then its A range, then its B range.
   int bp_r, bp_L, bp_nA, bp_nB, bp_kB0;
   int64_t bp_al, bp_ah, bp_rA, bp_bl, bp_rB;
+  // Dynamic scheduling (dynamic != 0): pieces are handed out by an atomic
+  // work counter instead of the static plan.  Piece index i: i < t1 (modes
+  // Stage1/Block) = stage-1 tile i; then down chunks of chunk_kb K blocks,
+  // chunk-major (all t2 tiles of K chunk 0, then chunk 1, ...).  CTA c takes
+  // piece c first (prefetched before griddepcontrol.wait), then
+  // G + atomicAdd(sched[0], 1); the last CTA to exit resets sched[0..1].
+  int dynamic;
+  int chunk_kb;
+  int* sched;
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.
@@ -66,6 +75,7 @@ struct StreamArgs {
 };
 
 constexpr int kTraceSlots = 64;
+constexpr int kPieceQueue = 8;  // producer -> consumers piece queue depth
 
 // Smem bytes of one pipeline stage (weights + activation rows).
 __host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs) {

@@ -44,6 +44,10 @@ def configs(rt, B):
         "fused_tc_kbs1": rt.Config.make(kbs=1, s1_stages=3, down_stages=5),
         "block_tc": rt.Config.make(block_kernel=1),
         "block_tc_kbs1_c37": rt.Config.make(block_kernel=1, kbs=1, s1_ctas=37),
+        "dyn_block_tc": rt.Config.make(block_kernel=1, dynamic_sched=1),
+        "dyn_block_tc_c5_ch3": rt.Config.make(block_kernel=1, dynamic_sched=1,
+                                              s1_ctas=5, chunk_kb=3, kbs=2),
+        "dyn_fused_tc": rt.Config.make(dynamic_sched=1, down_ctas=148, s1_ctas=148),
         "two_kernel": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
         "four_kernel": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
     }
@@ -54,6 +58,9 @@ def configs(rt, B):
                                               down_family=rt.FAMILY_TC)
         out["block_gemv"] = rt.Config.make(block_kernel=1, s1_family=rt.FAMILY_GEMV,
                                            down_family=rt.FAMILY_GEMV)
+        out["dyn_block_gemv"] = rt.Config.make(block_kernel=1, dynamic_sched=1,
+                                               s1_family=rt.FAMILY_GEMV,
+                                               down_family=rt.FAMILY_GEMV)
     return out
 
 
