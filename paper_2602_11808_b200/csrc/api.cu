@@ -399,8 +399,12 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     if (++ctx->epoch == 0) ++ctx->epoch;
     a.epoch = ctx->epoch;
     a.mutant = cfg.mutant;
-    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas
-                               : balanced_grid(w->s1_tiles, ctx->sm_count);
+    // Static plan: the balanced stage-1 grid; dynamic: 7/8 of the SMs (the
+    // measured optimum, profiles/) -- never more CTAs than SMs, since down
+    // pieces spin on other CTAs' stage-1 flags.
+    int grid = cfg.s1_ctas > 0       ? cfg.s1_ctas
+               : cfg.dynamic_sched ? ctx->sm_count * 7 / 8
+                                   : balanced_grid(w->s1_tiles, ctx->sm_count);
     grid = std::max(1, std::min(grid, ctx->sm_count));
     block_plan(grid, w, &a);
     DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
@@ -567,13 +571,17 @@ void default_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
                     dfk_config* out) {
   (void)ctx;
   (void)w;
+  (void)B;
+  // The single persistent block kernel with dynamic scheduling: the fastest
+  // configuration in the measured sweeps at every batch (profiles/).
   std::memset(out, 0, sizeof(*out));
   out->variant = DFK_VARIANT_FUSED;
   out->s1_family = DFK_FAMILY_TC;
   out->down_family = DFK_FAMILY_TC;
   out->s1_split_k = 1;
+  out->block_kernel = 1;
+  out->dynamic_sched = 1;
   out->pdl = 1;
-  (void)B;
   std::snprintf(out->label, sizeof(out->label), "%s",
                 config_label(*out).c_str());
 }
