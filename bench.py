@@ -343,7 +343,7 @@ def main():
         hx[B].arr[...] = xs[B].download_bits()
 
     def host_call(B, i, cfg):
-        ctx.forward_host_into(sets[i % len(sets)], hx[B].arr, hy[B].arr, cfg=cfg)
+        ctx.forward_host_async(sets[i % len(sets)], hx[B].arr, hy[B].arr, cfg=cfg)
 
     for k in range(2):
         for B in sweep:
@@ -354,8 +354,12 @@ def main():
     t0 = time.perf_counter()
     ev0.record(ctx)
     for k in range(e2e_steps):
+        # one step = every batch of the sweep: H2D of its X from pinned host
+        # memory, the block, D2H of its Y; the host waits for the step's
+        # results before starting the next step.
         for j, B in enumerate(sweep):
             host_call(B, k * len(sweep) + j, cfgs[B])
+        ctx.sync()
     ev1.record(ctx)
     ctx.sync()
     wall = time.perf_counter() - t0

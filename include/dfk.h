@@ -173,6 +173,14 @@ DFK_API int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
                              int32_t x_dtype, int64_t batch, void* y,
                              int32_t y_dtype, const dfk_config* cfg);
 
+/* Asynchronous host-buffer call for pipelined callers: X is bf16 in PINNED
+ * host memory, Y is fp32 in PINNED host memory; enqueues H2D(X), the block
+ * (or TP block) and D2H(Y) on the context stream and returns.  Buffers must
+ * stay valid until dfk_context_sync. */
+DFK_API int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
+                                   const void* x_pinned_bf16, int64_t batch,
+                                   float* y_pinned, const dfk_config* cfg);
+
 /* --- scheduler (tuner.cpp semantics) ----------------------------------- */
 /* Candidate grid for (weights, B): fills up to `cap` configs, returns the
  * count in *n (default_candidates, tuner.cpp:59-88). */

@@ -964,6 +964,32 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
   return DFK_OK;
 }
 
+int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
+                           const void* x_pinned_bf16, int64_t batch,
+                           float* y_pinned, const dfk_config* cfg) {
+  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_batch(batch));
+  if (!x_pinned_bf16 || !y_pinned) return fail(DFK_ERR_INVALID, "null host pointer");
+  const size_t xb = static_cast<size_t>(batch * w->d_model) * 2;
+  const size_t yb = static_cast<size_t>(batch * w->d_model) * 4;
+  // Stream order makes one staging pair safe: the next call's H2D runs after
+  // this call's kernels, its kernels after this call's D2H.
+  DFK_TRY(ensure_buf(ctx->hx_dev, xb, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx->hy_dev, yb, false, ctx->stream));
+  DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, x_pinned_bf16, xb,
+                           cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->comm) {
+    DFK_TRY(dfk_tp_forward(ctx, w, ctx->hx_dev.p, batch,
+                           static_cast<float*>(ctx->hy_dev.p), cfg));
+  } else {
+    DFK_TRY(forward_impl(ctx, w, ctx->hx_dev.p, batch, ctx->hy_dev.p, DFK_F32,
+                         cfg));
+  }
+  DFK_CUDA(cudaMemcpyAsync(y_pinned, ctx->hy_dev.p, yb, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  return DFK_OK;
+}
+
 int dfk_balanced_range(int64_t extent, int64_t parts, int64_t index,
                        int64_t* begin, int64_t* end) {
   if (parts < 1) return fail(DFK_ERR_SHAPE, "balanced_ranges: parts must be >= 1");

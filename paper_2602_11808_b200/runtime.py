@@ -127,6 +127,7 @@ _sigs = {
     "dfk_forward": ([_vp, _vp, _vp, _i64, _vp, _i32, C.POINTER(Config)], C.c_int),
     "dfk_forward_host": ([_vp, _vp, _vp, _i32, _i64, _vp, _i32, C.POINTER(Config)],
                          C.c_int),
+    "dfk_forward_host_async": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
     "dfk_candidates": ([_vp, _vp, _i64, C.POINTER(Config), _i32, C.POINTER(_i32)],
                        C.c_int),
     "dfk_tune": ([_vp, _vp, _i64, C.c_char_p, _i32, _i32, C.POINTER(Config),
@@ -427,6 +428,12 @@ class Context:
         """forward_host into caller-owned host buffers (x bf16 bits, y fp32)."""
         _check(lib.dfk_forward_host(self.h, w.h, x.ctypes.data, BF16, x.shape[0],
                                     y.ctypes.data, F32, self._cfg(cfg)))
+
+    def forward_host_async(self, w: Weights, x_pinned: np.ndarray, y_pinned: np.ndarray,
+                           cfg: Optional[Config] = None):
+        """Enqueue H2D(x) + block + D2H(y) on pinned host buffers; no sync."""
+        _check(lib.dfk_forward_host_async(self.h, w.h, x_pinned.ctypes.data, x_pinned.shape[0],
+                                          y_pinned.ctypes.data, self._cfg(cfg)))
 
     # --- scheduler -------------------------------------------------------
     def candidates(self, w: Weights, batch: int):
