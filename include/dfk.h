@@ -212,6 +212,10 @@ DFK_API int dfk_tp_init(dfk_context ctx, const void* id128, int rank,
 /* Single process driving `n` contexts on n devices (ncclCommInitAll). */
 DFK_API int dfk_tp_init_all(dfk_context* ctxs, int n);
 DFK_API int dfk_tp_rank(dfk_context ctx, int* rank, int* nranks);
+/* Bracket per-device calls when ONE thread drives several ranks
+ * (ncclGroupStart / ncclGroupEnd). */
+DFK_API int dfk_tp_group_start(void);
+DFK_API int dfk_tp_group_end(void);
 /* Fused stage 1 + down on this rank's shard into fp32 partial Y, then one
  * in-place ncclAllReduce(sum) of B x d_model on the context stream (the one
  * collective of the compound scheme, tp.cpp:140-167). */

@@ -43,7 +43,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    for d in (CSRC, os.path.join(ROOT, "include")):
+    for d in (CSRC, os.path.join(ROOT, "include"), os.path.join(PKG, "cpp")):
         for f in os.listdir(d):
             if os.path.getmtime(os.path.join(d, f)) > t:
                 return True
@@ -81,7 +81,26 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 5) -> str:
     _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcublasLt", "-lnccl",
           "-Xlinker", "-rpath,/usr/local/cuda/lib64"], verbose)
     os.replace(tmp, LIB)
+    build_cpp(verbose)
     return LIB
+
+
+SHIM_LIB = os.path.join(LIBDIR, "libdeepfusion_b200.so")
+CPP_TEST = os.path.join(ROOT, "tests", "cpp", "test_deepfusion_gpu")
+
+
+def build_cpp(verbose: bool = False) -> None:
+    """The C++ drop-in shim (reference operator API over the C ABI) and its
+    test binary; both link libdfk.so through an $ORIGIN-relative rpath."""
+    cpp = os.path.join(PKG, "cpp")
+    _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall",
+          f"-I{os.path.join(ROOT, 'include')}", f"-I{cpp}",
+          os.path.join(cpp, "deepfusion_gpu.cpp"), "-o", SHIM_LIB,
+          f"-L{LIBDIR}", "-ldfk", "-Wl,-rpath,$ORIGIN"], verbose)
+    _run(["g++", "-O2", "-std=c++20", "-Wall", f"-I{cpp}",
+          os.path.join(ROOT, "tests", "cpp", "test_deepfusion_gpu.cpp"), "-o", CPP_TEST,
+          f"-L{LIBDIR}", "-ldeepfusion_b200", "-ldfk",
+          f"-Wl,-rpath,$ORIGIN/../../paper_2602_11808_b200/lib"], verbose)
 
 
 if __name__ == "__main__":

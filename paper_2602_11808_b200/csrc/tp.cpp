@@ -81,6 +81,18 @@ int dfk_tp_rank(dfk_context ctx, int* rank, int* nranks) {
   return DFK_OK;
 }
 
+int dfk_tp_group_start(void) {
+  ncclResult_t r = ncclGroupStart();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+  return DFK_OK;
+}
+
+int dfk_tp_group_end(void) {
+  ncclResult_t r = ncclGroupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+  return DFK_OK;
+}
+
 int dfk_tp_forward(dfk_context ctx, dfk_weights w, const void* x,
                    int64_t batch, float* y, const dfk_config* cfg) {
   if (!ctx || !w) return fail(DFK_ERR_INVALID, "null handle");

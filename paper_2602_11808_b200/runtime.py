@@ -137,6 +137,8 @@ _sigs = {
     "dfk_tp_init": ([_vp, _vp, C.c_int, C.c_int], C.c_int),
     "dfk_tp_init_all": ([C.POINTER(_vp), C.c_int], C.c_int),
     "dfk_tp_rank": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "dfk_tp_group_start": ([], C.c_int),
+    "dfk_tp_group_end": ([], C.c_int),
     "dfk_tp_forward": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
     "dfk_balanced_range": ([_i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)],
                            C.c_int),

@@ -337,3 +337,24 @@ def test_llama8b_full_shape_parity(rt, ctx, oracle_lib, B):
         assert rel_err(a2, a2_ref) <= TOL, (label, rel_err(a2, a2_ref))
         assert rel_err(y1, y_ref) <= TOL, (label, rel_err(y1, y_ref))
         assert rel_err(y2, y_ref) <= TOL, (label, rel_err(y2, y_ref))
+
+
+def test_forward_host_async_pipelined(rt, ctx, oracle_lib):
+    """Async host-buffer calls (pinned X bf16 -> Y fp32) queued back to back
+    and synchronised once match the oracle for every call."""
+    from paper_2602_11808_b200.runtime import PinnedHost, to_bf16_bits
+    dm, df = 256, 512
+    ws, refs, hx, hy = [], [], [], []
+    for i, B in enumerate((1, 4, 16)):
+        x, wu, wg, wd = instance(oracle_lib, 60 + i, B, dm, df)
+        ws.append(ctx.weights(wg, wu, wd))
+        refs.append(oracle_lib.forward(x, wu, wg, wd)[1])
+        px = PinnedHost((B, dm), np.uint16)
+        px.arr[...] = to_bf16_bits(x)
+        hx.append(px)
+        hy.append(PinnedHost((B, dm), np.float32))
+    for i in range(3):
+        ctx.forward_host_async(ws[i], hx[i].arr, hy[i].arr)
+    ctx.sync()
+    for i in range(3):
+        assert rel_err(hy[i].arr, refs[i]) <= TOL, i
