@@ -16,6 +16,8 @@ ap.add_argument("--family", default="tc", choices=["tc", "gemv"])
 ap.add_argument("--variant", default="fused", choices=["fused", "two", "four"])
 ap.add_argument("--s1-stages", type=int, default=0)
 ap.add_argument("--pdl", type=int, default=1)
+ap.add_argument("--path", default="default", choices=["default", "two", "block", "block-static"],
+                help="default = the library's default config (NULL cfg)")
 a = ap.parse_args()
 ctx = rt.Context(0)
 s = 1 / np.sqrt(a.dm)
@@ -28,7 +30,12 @@ x = ctx.array((a.B, a.dm)).fill_uniform(4)
 y = ctx.array((a.B, a.dm), rt.F32)
 fam = rt.FAMILY_TC if a.family == "tc" else rt.FAMILY_GEMV
 var = {"fused": rt.VARIANT_FUSED, "two": rt.VARIANT_TWO_KERNEL, "four": rt.VARIANT_FOUR_KERNEL}[a.variant]
-cfg = rt.Config.make(variant=var, s1_family=fam, down_family=fam, s1_stages=a.s1_stages, pdl=a.pdl)
+if a.path == "default" and a.variant == "fused":
+    cfg = None
+else:
+    cfg = rt.Config.make(variant=var, s1_family=fam, down_family=fam, s1_stages=a.s1_stages,
+                         pdl=a.pdl, block_kernel=int(a.path.startswith("block")),
+                         dynamic_sched=int(a.path == "block"))
 for i in range(a.calls):
     ctx.forward(w, x, y, cfg=cfg)
 ctx.sync()
