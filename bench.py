@@ -210,26 +210,20 @@ def main():
         return
 
     from paper_2602_11808_b200 import runtime as rt
+    from paper_2602_11808_b200 import tp_host
 
     P = world
     ctx = rt.Context(local_rank)
     if P > 1:
-        uid = [rt.Context.tp_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.tp_init(uid[0], rank, P)
-    f0, f1 = rt.balanced_range(DF, P, rank)
+        ctx.tp_init(tp_host.exchange_uid(dist, rank), rank, P)
+    f0, f1 = tp_host.shard_range(DF, P, rank)
 
     def barrier():
         if dist:
             dist.barrier()
 
     def max_over_ranks(v):
-        if not dist:
-            return v
-        import torch
-        t = torch.tensor([v], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return tp_host.max_over_ranks(dist, v)
 
     # Weight sets: synthetic bf16 U[-1/sqrt(dm), 1/sqrt(dm)) generated on the
     # device in the reference layout, then prepacked (sources freed).

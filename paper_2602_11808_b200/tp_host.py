@@ -1,0 +1,56 @@
+"""Host-side plumbing of the tensor-parallel path (one process per GPU).
+
+The GPU work and the all-reduce live in libdfk.so (dfk_tp_init /
+dfk_tp_forward, NCCL); this module holds the rank-level logic around it so
+it can be exercised on CPU with the gloo backend (tests/test_tp_gloo.py):
+
+* shard_range  — this rank's [ff_begin, ff_end) of d_ff (balanced_ranges,
+                 tp.cpp:8-29, through the C ABI);
+* exchange_uid — rank 0's 128-byte NCCL unique id broadcast to every rank;
+* max_over_ranks — the bench contract's max-over-ranks timing reduction;
+* sum_partials — the compound scheme's single all-reduce of partial Y for
+                 host-resident fp64 partials (the check the gloo test runs).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional, Tuple
+
+import numpy as np
+
+from . import runtime as rt
+
+
+def shard_range(d_ff: int, world: int, rank: int) -> Tuple[int, int]:
+    return rt.balanced_range(d_ff, world, rank)
+
+
+def exchange_uid(dist, rank: int, make_uid: Optional[Callable[[], bytes]] = None) -> bytes:
+    """Rank 0 creates the NCCL unique id (dfk_tp_unique_id); all ranks get it."""
+    box = [None]
+    if rank == 0:
+        box[0] = (make_uid or rt.Context.tp_unique_id)()
+    if dist is not None:
+        dist.broadcast_object_list(box, src=0)
+    uid = box[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise ValueError("NCCL unique id must be 128 bytes")
+    return bytes(uid)
+
+
+def max_over_ranks(dist, value: float) -> float:
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_partials(dist, partial: np.ndarray) -> np.ndarray:
+    """All-reduce(sum) of a host fp64 partial (one collective of B x d_model)."""
+    if dist is None:
+        return partial
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(partial, dtype=np.float64).copy())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.numpy()
