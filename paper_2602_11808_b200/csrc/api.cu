@@ -76,7 +76,7 @@ std::string config_label(const dfk_config& c) {
   if (c.variant == DFK_VARIANT_TWO_KERNEL) return "two_kernel_cublaslt";
   if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
   if (c.block_kernel) {
-    if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
+    if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_tpp" << c.tiles_per_piece << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
       << (c.pdl ? "_pdl" : "");
@@ -147,19 +147,19 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
   return DFK_OK;
 }
 
-int max_stages(dfk_context_s* ctx, int n_pad, int kbs) {
+int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int tpp = 1) {
   const int avail = ctx->max_smem_optin - 1024 - 1024;
-  int s = avail / stream_stage_bytes(n_pad, kbs);
+  int s = avail / stream_stage_bytes(n_pad, kbs, tpp);
   return std::min(s, 32);
 }
 
 // Bigger ring stages stream faster (tools/stream_probe.cu, profiles/): take
 // the largest stage (up to 4 x 16 KiB weight blocks) that still leaves 3
 // slots in shared memory.
-int pick_kbs(dfk_context_s* ctx, int n_pad, int requested) {
+int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int tpp = 1) {
   if (requested > 0) return std::min(requested, 4);
   for (int kbs = 4; kbs > 1; --kbs)
-    if (max_stages(ctx, n_pad, kbs) >= 3) return kbs;
+    if (max_stages(ctx, n_pad, kbs, tpp) >= 3) return kbs;
   return 1;
 }
 
@@ -231,8 +231,9 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   return DFK_OK;
 }
 
+// Ring geometry for one launch: stage size (kbs), depth and tiles per piece.
 void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
-                 int stages_req, int kbs_req, StreamArgs* a) {
+                 int stages_req, const dfk_config& cfg, StreamArgs* a) {
   const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
   a->w1 = w->s1_pack;
   a->t1 = w->s1_tiles;
@@ -242,9 +243,19 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   a->kb2 = w->dn_kblocks;
   a->B = static_cast<int>(nb);
   a->n_pad = n_pad;
-  a->kbs = pick_kbs(ctx, n_pad, kbs_req);
+  // Two weight tiles per activation stage once the activation block is a
+  // sizeable fraction of the weight block (B > 16): halves the X / A2
+  // re-reads (dynamic tcgen05 path only; TMEM holds 2 x tpp x N columns).
+  int tpp = 1;
+  if (tc && cfg.dynamic_sched) {
+    tpp = cfg.tiles_per_piece > 0 ? std::min(cfg.tiles_per_piece, 2)
+                                  : (n_pad >= 32 ? 2 : 1);
+    if (2 * tpp * n_pad > 512) tpp = 1;
+  }
+  a->tpp = tpp;
+  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, tpp);
   a->trace = ctx->trace;
-  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs));
+  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, tpp));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
 
@@ -279,7 +290,7 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
-    fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg.kbs, &a);
+    fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap tm;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
                      w->d_model, nb, x_ld, a.n_pad, &tm));
@@ -311,7 +322,7 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
-    fill_common(ctx, w, nb, L.tc, cfg.down_stages, cfg.kbs, &a);
+    fill_common(ctx, w, nb, L.tc, cfg.down_stages, cfg, &a);
     CUtensorMap tm;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
                      w->d_ff, nb, a_ld, a.n_pad, &tm));
@@ -386,7 +397,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
-    fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg.kbs, &a);
+    fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap xm, am;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
                      w->d_model, nb, x_ld, a.n_pad, &xm));

@@ -106,11 +106,15 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
   };
   for (int f : fams) {
     add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
-    dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
-    d.dynamic_sched = 1;
-    std::snprintf(d.label, sizeof(d.label), "%s", "");
-    std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
-    add(d);
+    for (int tpp : {0, 1}) {  // 0 = auto (2 tiles per piece at B > 16)
+      if (tpp == 1 && (f != DFK_FAMILY_TC || B <= 16)) continue;
+      dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
+      d.dynamic_sched = 1;
+      d.tiles_per_piece = tpp;
+      std::snprintf(d.label, sizeof(d.label), "%s", "");
+      std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
+      add(d);
+    }
   }
   const int dn_ctas[2] = {0, ctx->sm_count};  // 0 = library default (3/4 SMs)
   for (int s1f : fams)
@@ -133,7 +137,8 @@ json cfg_to_json(const dfk_config& c) {
               {"s1_split_k", c.s1_split_k},   {"down_family", c.down_family},
               {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
               {"pdl", c.pdl},                 {"dynamic_sched", c.dynamic_sched},
-              {"chunk_kb", c.chunk_kb},       {"label", std::string(c.label)}};
+              {"chunk_kb", c.chunk_kb},       {"tiles_per_piece", c.tiles_per_piece},
+              {"label", std::string(c.label)}};
 }
 
 template <typename T>
@@ -164,6 +169,7 @@ dfk_config cfg_from_json(const json& j) {
   c.kbs = get_field<int>(j, "kbs");
   c.dynamic_sched = get_field<int>(j, "dynamic_sched");
   c.chunk_kb = get_field<int>(j, "chunk_kb");
+  c.tiles_per_piece = get_field<int>(j, "tiles_per_piece");
   std::snprintf(c.label, sizeof(c.label), "%s",
                 get_field<std::string>(j, "label").c_str());
   return c;

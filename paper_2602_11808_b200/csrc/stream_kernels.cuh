@@ -68,6 +68,10 @@ struct StreamArgs {
   int dynamic;
   int chunk_kb;
   int* sched;
+  // Tiles per piece (dynamic tcgen05 path): a piece streams `tpp` adjacent
+  // weight tiles against ONE activation stage (tpp accumulators in TMEM), so
+  // the X / A2 block of each K block is loaded once per tpp weight tiles.
+  int tpp;
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.
@@ -78,14 +82,14 @@ constexpr int kTraceSlots = 64;
 constexpr int kPieceQueue = 8;  // producer -> consumers piece queue depth
 
 // Smem bytes of one pipeline stage (weights + activation rows).
-__host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs) {
-  return kbs * (16384 + n_pad * 128);
+__host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs, int tpp = 1) {
+  return kbs * (tpp * 16384 + n_pad * 128);
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xmap,
                           const CUtensorMap& amap, const StreamArgs& a, int grid,
                           bool pdl, cudaStream_t stream);
 
-int stream_smem_bytes(int n_pad, int stages, int kbs);
+int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp = 1);
 
 }  // namespace dfk

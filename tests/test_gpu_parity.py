@@ -48,6 +48,9 @@ def configs(rt, B):
         "dyn_block_tc_c5_ch3": rt.Config.make(block_kernel=1, dynamic_sched=1,
                                               s1_ctas=5, chunk_kb=3, kbs=2),
         "dyn_fused_tc": rt.Config.make(dynamic_sched=1, down_ctas=148, s1_ctas=148),
+        "dyn_block_tpp2": rt.Config.make(block_kernel=1, dynamic_sched=1, tiles_per_piece=2),
+        "dyn_fused_tpp2_ch5": rt.Config.make(dynamic_sched=1, tiles_per_piece=2, chunk_kb=5,
+                                             s1_ctas=9, down_ctas=13),
         "two_kernel": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
         "four_kernel": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
     }
