@@ -243,13 +243,13 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   a->kb2 = w->dn_kblocks;
   a->B = static_cast<int>(nb);
   a->n_pad = n_pad;
-  // Two weight tiles per activation stage once the activation block is a
-  // sizeable fraction of the weight block (B > 16): halves the X / A2
-  // re-reads (dynamic tcgen05 path only; TMEM holds 2 x tpp x N columns).
+  // Optional: two weight tiles per activation stage (halves the X / A2
+  // re-reads; dynamic tcgen05 path only; TMEM holds 2 x tpp x N columns).
+  // Measured slower at every batch on Llama-8B (the 2 x weight smem forces
+  // 16 KiB copies and a shallow ring, profiles/r1_sweeps.md), so opt-in.
   int tpp = 1;
-  if (tc && cfg.dynamic_sched) {
-    tpp = cfg.tiles_per_piece > 0 ? std::min(cfg.tiles_per_piece, 2)
-                                  : (n_pad >= 32 ? 2 : 1);
+  if (tc && cfg.dynamic_sched && cfg.tiles_per_piece > 1) {
+    tpp = std::min(cfg.tiles_per_piece, 2);
     if (2 * tpp * n_pad > 512) tpp = 1;
   }
   a->tpp = tpp;

@@ -106,8 +106,7 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
   };
   for (int f : fams) {
     add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
-    for (int tpp : {0, 1}) {  // 0 = auto (2 tiles per piece at B > 16)
-      if (tpp == 1 && (f != DFK_FAMILY_TC || B <= 16)) continue;
+    for (int tpp : {0}) {  // tpp=2 measured slower everywhere (profiles/)
       dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
       d.dynamic_sched = 1;
       d.tiles_per_piece = tpp;
