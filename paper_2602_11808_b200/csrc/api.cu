@@ -77,12 +77,14 @@ std::string config_label(const dfk_config& c) {
   if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
   if (c.block_kernel) {
     if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_tpp" << c.tiles_per_piece << "_";
+    if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
       << (c.pdl ? "_pdl" : "");
     return o.str();
   }
   if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
+  if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
   o << "fused_s1" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
     << c.s1_stages << "_c" << c.s1_ctas << "_dn"
     << (c.down_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
@@ -147,8 +149,10 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
   return DFK_OK;
 }
 
-int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int tpp = 1) {
-  const int avail = ctx->max_smem_optin - 1024 - 1024;
+int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int tpp = 1,
+               int split_k = 1) {
+  const int avail =
+      ctx->max_smem_optin - 1024 - 1024 - split_red_bytes(n_pad, split_k);
   int s = avail / stream_stage_bytes(n_pad, kbs, tpp);
   return std::min(s, 32);
 }
@@ -156,10 +160,11 @@ int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int tpp = 1) {
 // Bigger ring stages stream faster (tools/stream_probe.cu, profiles/): take
 // the largest stage (up to 4 x 16 KiB weight blocks) that still leaves 3
 // slots in shared memory.
-int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int tpp = 1) {
+int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int tpp = 1,
+             int split_k = 1) {
   if (requested > 0) return std::min(requested, 4);
   for (int kbs = 4; kbs > 1; --kbs)
-    if (max_stages(ctx, n_pad, kbs, tpp) >= 3) return kbs;
+    if (max_stages(ctx, n_pad, kbs, tpp, split_k) >= 3) return kbs;
   return 1;
 }
 
@@ -231,6 +236,16 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   return DFK_OK;
 }
 
+// Stage-1 split-K (cluster of `split` CTAs per tile, DSMEM reduction): only
+// for the tcgen05 family, the static plan, N <= 64 (reduction buffer) and a
+// K-block count divisible by the split.  Returns 1 when not applicable.
+int effective_split(const dfk_config& cfg, const dfk_weights_s* w, int64_t nb) {
+  const int sk = cfg.s1_split_k;
+  if (sk <= 1 || cfg.s1_family == DFK_FAMILY_GEMV || cfg.dynamic_sched) return 1;
+  if (sk > 8 || round_up(nb, 16) > 64 || w->s1_kblocks % sk != 0) return 1;
+  return sk;
+}
+
 // Ring geometry for one launch: stage size (kbs), depth and tiles per piece.
 void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
                  int stages_req, const dfk_config& cfg, StreamArgs* a) {
@@ -253,9 +268,10 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
     if (2 * tpp * n_pad > 512) tpp = 1;
   }
   a->tpp = tpp;
-  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, tpp);
+  const int sk = a->split_k > 1 ? a->split_k : 1;
+  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, tpp, sk);
   a->trace = ctx->trace;
-  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, tpp));
+  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, tpp, sk));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
 
@@ -290,6 +306,7 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
+    a.split_k = effective_split(cfg, w, nb);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap tm;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
@@ -298,9 +315,14 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     a.mutant = cfg.mutant;
-    DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
-    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas : balanced_grid(w->s1_tiles, ctx->sm_count);
-    grid = std::max(1, std::min(grid, w->s1_tiles));
+    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
+    const int sk = a.split_k;
+    // Clusters of sk CTAs; as many clusters as keep every cluster at the
+    // same tile count.
+    int clusters = cfg.s1_ctas > 0 ? cfg.s1_ctas / sk
+                                   : balanced_grid(w->s1_tiles, ctx->sm_count / sk);
+    clusters = std::max(1, std::min(clusters, w->s1_tiles));
+    const int grid = clusters * sk;
     cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
                                   grid, cfg.pdl != 0, ctx->stream);
     if (e != cudaSuccess)
@@ -350,16 +372,21 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
 // an early round-robin wave) goes to the CTAs with one tile fewer, group B
 // (last wave) is shared by everyone with byte-balanced budgets.
 void block_plan(int G, const dfk_weights_s* w, StreamArgs* a) {
-  const int T1 = w->s1_tiles, kb1 = w->s1_kblocks;
+  // With split-K, stage-1 tiles go round-robin over Q = G / split clusters
+  // and every CTA of a cluster owns kb1 / split K blocks of each tile.
+  const int split = a->split_k > 1 ? a->split_k : 1;
+  const int Q = G / split;
+  const int T1 = w->s1_tiles, kb1c = w->s1_kblocks / split;
   const int t2 = w->dn_tiles, kb2 = w->dn_kblocks;
-  const int q = T1 / G, r = T1 % G;
+  const int q = T1 / Q, rt = T1 % Q;
+  const int r = rt * split;  // heavy CTAs (in the first rt clusters)
   a->bp_r = r;
   a->bp_L = G - r;
-  if (r > 0) {
-    a->bp_nA = q * G;
-    a->bp_nB = r;
-    a->bp_kB0 = q * G;
-  } else {  // every CTA owns q tiles: no early group
+  if (rt > 0) {
+    a->bp_nA = q * Q;
+    a->bp_nB = rt;
+    a->bp_kB0 = q * Q;
+  } else {  // every cluster owns q tiles: no early group
     a->bp_nA = 0;
     a->bp_nB = kb2;
     a->bp_kB0 = 0;
@@ -370,9 +397,11 @@ void block_plan(int G, const dfk_weights_s* w, StreamArgs* a) {
   // Group B: uniform.
   a->bp_bl = Bn / G;
   a->bp_rB = Bn - a->bp_bl * G;
-  // Group A: total per CTA balanced, i.e. light ranks take kb1 more.
-  const int64_t WT = static_cast<int64_t>(T1) * kb1 + static_cast<int64_t>(t2) * kb2;
-  int64_t ah = (WT - static_cast<int64_t>(G) * (q + 1) * kb1 - Bn) / G;
+  // Group A: total per CTA balanced, i.e. light ranks take one stage-1 part
+  // (kb1c K blocks) more.
+  const int64_t WT = static_cast<int64_t>(T1) * kb1c * split +
+                     static_cast<int64_t>(t2) * kb2;
+  int64_t ah = (WT - static_cast<int64_t>(G) * (q + 1) * kb1c - Bn) / G;
   if (ah < 0 || r == 0) ah = 0;
   if (ah * r > A) ah = r > 0 ? A / r : 0;
   const int64_t al = (A - ah * r) / L;
@@ -397,6 +426,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
+    a.split_k = effective_split(cfg, w, nb);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap xm, am;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
@@ -417,8 +447,9 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
                : cfg.dynamic_sched ? ctx->sm_count * 7 / 8
                                    : balanced_grid(w->s1_tiles, ctx->sm_count);
     grid = std::max(1, std::min(grid, ctx->sm_count));
+    grid = std::max(a.split_k, grid / a.split_k * a.split_k);
     block_plan(grid, w, &a);
-    DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
+    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,

@@ -183,6 +183,17 @@ __device__ __forceinline__ void st_dsmem_f4(const void* p, uint32_t rank,
       : "memory");
 }
 
+// Atomic add into CTA `rank`'s shared memory (DSMEM) at the address `p`
+// has in this CTA.
+__device__ __forceinline__ void red_add_dsmem(const float* p, uint32_t rank,
+                                              float v) {
+  asm volatile(
+      "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
+      " red.shared::cluster.add.f32 [ra], %2;\n}" ::"r"(smem_u32(p)),
+      "r"(rank), "f"(v)
+      : "memory");
+}
+
 // ----------------------------------------------------------------------------
 // tcgen05 / TMEM.
 // ----------------------------------------------------------------------------

@@ -94,7 +94,8 @@ dfk_config make_cfg(int variant, int s1f, int dnf, int kbs, int block,
 // family x down family x down grid), plus one no-PDL control.  Stage sizes
 // and the stage-1 grid use the library's defaults (pick_kbs, balanced_grid),
 // which were themselves chosen from measured sweeps (profiles/).
-std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
+std::vector<dfk_config> candidates(const dfk_context_s* ctx,
+                                   const dfk_weights_s* w, int64_t B) {
   std::vector<dfk_config> out;
   out.push_back(make_cfg(DFK_VARIANT_FOUR_KERNEL, 0, 0, 0, 0, 0));
   out.push_back(make_cfg(DFK_VARIANT_TWO_KERNEL, 0, 0, 0, 0, 0));
@@ -125,6 +126,20 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, int64_t B) {
         std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
         add(c);
       }
+  // Fewer stage-1 tiles than SMs (tensor-parallel shards): split each tile's
+  // K over a cluster (DSMEM reduction), static plan.
+  if (w->s1_tiles < ctx->sm_count && B <= 64) {
+    for (int sk : {2, 4}) {
+      if (w->s1_kblocks % sk) continue;
+      for (int block : {1, 0}) {
+        dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, block, 1);
+        c.s1_split_k = sk;
+        std::snprintf(c.label, sizeof(c.label), "%s", "");
+        std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+        add(c);
+      }
+    }
+  }
   add(make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 0, 0));
   return out;
 }
@@ -322,7 +337,7 @@ int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
                    dfk_config* out, int32_t cap, int32_t* n) {
   if (!ctx || !w || !n) return fail(DFK_ERR_INVALID, "null argument");
   if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
-  const auto c = candidates(ctx, batch);
+  const auto c = candidates(ctx, w, batch);
   *n = static_cast<int32_t>(c.size());
   for (int32_t i = 0; i < std::min<int32_t>(cap, *n); ++i) out[i] = c[i];
   return DFK_OK;
@@ -401,7 +416,7 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   std::vector<Result> results;
-  for (const dfk_config& c : candidates(ctx, batch)) {
+  for (const dfk_config& c : candidates(ctx, w, batch)) {
     Result r;
     r.cfg = c;
     r.label = c.label;

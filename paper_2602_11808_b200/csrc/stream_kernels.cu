@@ -73,6 +73,9 @@ struct Piece {
 struct Plan {
   int mode;
   int G, c;
+  int split;        // CTAs per stage-1 tile (cluster size), 1 = none
+  int q, Q;         // cluster index of this CTA, number of clusters
+  int krank;        // rank in the cluster = K part of each stage-1 tile
   int n1;           // stage-1 tiles of this CTA
   int rank;         // this CTA's rank (kModeDown: c; kModeBlock: light first)
   int64_t a0, a1;   // kModeBlock group-A range of this CTA
@@ -99,7 +102,11 @@ __device__ __forceinline__ Plan make_plan(const StreamArgs& a, int mode) {
   p.G = gridDim.x;
   p.c = blockIdx.x;
   p.U2 = static_cast<int64_t>(a.t2) * a.kb2;
-  p.n1 = mode != kModeDown && p.c < a.t1 ? (a.t1 - 1 - p.c) / p.G + 1 : 0;
+  p.split = (mode != kModeDown && a.split_k > 1) ? a.split_k : 1;
+  p.Q = p.G / p.split;
+  p.q = p.c / p.split;
+  p.krank = p.c % p.split;
+  p.n1 = mode != kModeDown && p.q < a.t1 ? (a.t1 - 1 - p.q) / p.Q + 1 : 0;
   p.a0 = p.a1 = 0;
   p.u0 = p.u1 = 0;
   p.rank = p.c;
@@ -123,9 +130,9 @@ struct PieceIter {
     if (grp == 0) {
       if (i < p.n1) {
         out.down = 0;
-        out.tile = p.c + i * p.G;
-        out.kb0 = 0;
-        out.kb1 = a.kb1;
+        out.tile = p.q + i * p.Q;
+        out.kb0 = p.krank * a.kb1 / p.split;
+        out.kb1 = (p.krank + 1) * a.kb1 / p.split;
         out.nt = 1;
         ++i;
         return true;
@@ -686,16 +693,86 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
 // ---------------------------------------------------------------------------
 // tcgen05 epilogue (warps 2-5; TMEM lanes 32*(warp%4) .. +31).
 // ---------------------------------------------------------------------------
+// Stage-1 epilogue of a K-split tile (cluster of p.split CTAs).  Non-leaders
+// add their partial gate/up accumulators into the leader's smem buffer
+// red[n][row] over DSMEM and arrive on the leader's red_full barrier; the
+// leader adds them to its own partial, runs SiLU*up, writes A2, re-zeroes the
+// buffer and releases every non-leader's red_free barrier.  mutant == 1
+// applies SiLU per K part instead (the reference's SiluPerKChunk negative
+// control, verification.cpp:84-124) and must fail parity.
+__device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
+                                                  const Plan& p, int tile,
+                                                  uint32_t taddr, int row,
+                                                  int lane, float* red,
+                                                  uint64_t* red_full,
+                                                  uint64_t* red_free,
+                                                  int split_iter) {
+  int is_up, cofs;
+  s1_row_map(row, &is_up, &cofs);
+  const int col = tile * kS1Cols + cofs;
+  const uint32_t par = static_cast<uint32_t>(split_iter & 1);
+  const bool mutant = a.mutant == 1;
+  if (p.krank != 0) {
+    mbar_wait_cluster(red_free, par ^ 1u);
+    for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+      float v[16];
+      tmem_ld16(taddr + c0, v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float val = v[e];
+        if (mutant) {
+          const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
+          val = is_up ? 0.f : silu_f(v[e]) * up;
+        }
+        red_add_dsmem(red + (c0 + e) * 128 + row, 0, val);
+      }
+    }
+    mbar_arrive_cluster(red_full, 0);
+    return;
+  }
+  // Leader.
+  mbar_wait_cluster(red_full, par);
+  for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+    float v[16];
+    tmem_ld16(taddr + c0, v);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      float* slot = red + (c0 + e) * 128 + row;
+      const float other = *slot;
+      *slot = 0.f;
+      float out;
+      if (!mutant) {
+        const float g_or_u = v[e] + other;
+        const float up = __shfl_xor_sync(0xffffffffu, g_or_u, 16);
+        out = silu_f(g_or_u) * up;
+      } else {
+        const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
+        out = silu_f(v[e]) * up + other;
+      }
+      const int n = c0 + e;
+      if (!is_up && n < a.B && col < a.cols_valid) {
+        a.a2[n * a.a2_ld + col] = __float2bfloat16_rn(out);
+      }
+    }
+  }
+  // Every non-leader's buffer-free barrier counts 128 arrivals per phase.
+  for (int r = 1; r < p.split; ++r) mbar_arrive_cluster(red_free, r);
+  (void)lane;
+}
+
 __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
                                             uint64_t* tfull, uint64_t* tempty,
                                             uint32_t tmem_base,
-                                            int* smem_flag, PieceQueue* pq) {
+                                            int* smem_flag, PieceQueue* pq,
+                                            float* red, uint64_t* red_full,
+                                            uint64_t* red_free) {
   const int w = static_cast<int>(warp_id());
   const int quarter = w & 3;
   const int lane = static_cast<int>(lane_id());
   const int row = quarter * 32 + lane;
   const int tid = (w - 2) * 32 + lane;
   int acc_it = 0;
+  int split_iter = 0;
   PieceReader pi;
   Piece pc;
   while (pi.next(a, p, pq, false, pc)) {
@@ -704,6 +781,20 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
     mbar_wait(&tfull[ab], aph);
     tc_fence_after();
     const int tpp = a.tpp > 0 ? a.tpp : 1;
+    if (!pc.down && p.split > 1) {
+      const uint32_t taddr = tmem_base +
+                             (static_cast<uint32_t>(quarter * 32) << 16) +
+                             static_cast<uint32_t>(ab * tpp * a.n_pad);
+      s1_split_epilogue(a, p, pc.tile, taddr, row, lane, red, red_full, red_free,
+                        split_iter++);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (a.flags && p.krank == 0) s1_publish(a, pc.tile, tid, 128);
+      if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
+      ++acc_it;
+      continue;
+    }
     const uint32_t tbase = tmem_base +
                            (static_cast<uint32_t>(quarter * 32) << 16) +
                            static_cast<uint32_t>(ab * tpp * a.n_pad);
@@ -782,8 +873,14 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   uint64_t* tempty = tfull + 2;
   PieceQueue* pq = reinterpret_cast<PieceQueue*>(
       (reinterpret_cast<uintptr_t>(tempty + 2) + 15) & ~static_cast<uintptr_t>(15));
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pq + 1);
+  uint64_t* red_full = reinterpret_cast<uint64_t*>(pq + 1);
+  uint64_t* red_free = red_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_free + 1);
   int* smem_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  // Split-K reduction buffer: after the barriers, 16-byte aligned.
+  float* red = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(smem_flag + 4) + 15) & ~static_cast<uintptr_t>(15));
+  const bool split = kMode != kModeDown && a.split_k > 1;
 
   const uint32_t w = warp_id();
   if (w == 0 && lane_id() == 0) {
@@ -801,7 +898,14 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
       mbar_init(&pq->full[i], 1);
       mbar_init(&pq->empty[i], kTC ? 5 : kGemvWarps);
     }
+    if (split) {
+      mbar_init(red_full, (a.split_k - 1) * 128);  // every non-leader epilogue thread
+      mbar_init(red_free, 128);                     // every leader epilogue thread
+    }
     fence_barrier_init();
+  }
+  if (split) {
+    for (int i = threadIdx.x; i < a.n_pad * 128; i += blockDim.x) red[i] = 0.f;
   }
   uint32_t tmem_cols = 0;
   if constexpr (kTC) {
@@ -811,6 +915,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     if (w == 1) tmem_alloc(tmem_slot, tmem_cols);
   }
   __syncthreads();
+  if (split) cluster_sync();  // barriers initialised + buffer zeroed cluster-wide
   tc_fence_after();
   const uint32_t tmem_base = kTC ? *tmem_slot : 0u;
   const Plan plan = make_plan(a, kMode);
@@ -828,7 +933,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
         mma_issue(a, plan, smem, stage_bytes, full, empty, tfull, tempty,
                   tmem_base, pq);
     } else {
-      tc_epilogue(a, plan, tfull, tempty, tmem_base, smem_flag, pq);
+      tc_epilogue(a, plan, tfull, tempty, tmem_base, smem_flag, pq, red, red_full,
+                  red_free);
     }
   } else {
     gemv_consume<NB>(a, plan, smem, stage_bytes, full, empty, smem_flag, pq);
@@ -844,6 +950,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
       __threadfence();
     }
   }
+  if (split) cluster_sync();  // no CTA leaves while peers may touch its smem
   if constexpr (kTC) {
     if (w == 1) {
       __syncwarp();
@@ -870,8 +977,15 @@ cudaError_t launch_one(const CUtensorMap& xmap, const CUtensorMap& amap,
   cfg.blockDim = dim3(kTC ? kTcThreads : kGemvThreads);
   cfg.dynamicSmemBytes = static_cast<size_t>(smem);
   cfg.stream = stream;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   int na = 0;
+  if (a.split_k > 1 && kMode != kModeDown) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = static_cast<unsigned>(a.split_k);
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
   if (pdl) {
     attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attrs[na].val.programmaticStreamSerializationAllowed = 1;
@@ -898,9 +1012,9 @@ cudaError_t launch_mode(bool tc, int nb, const CUtensorMap& xmap,
 
 }  // namespace
 
-int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp) {
+int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp, int split_k) {
   return 1024 + stages * stream_stage_bytes(n_pad, kbs, tpp) + (2 * stages + 4) * 8 +
-         static_cast<int>(sizeof(PieceQueue)) + 32;
+         static_cast<int>(sizeof(PieceQueue)) + 128 + split_red_bytes(n_pad, split_k);
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
@@ -911,7 +1025,10 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
     return cudaErrorInvalidValue;
   if (a.tpp > 1 && (!tc || !a.dynamic || 2 * a.tpp * a.n_pad > 512))
     return cudaErrorInvalidValue;
-  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.tpp > 0 ? a.tpp : 1);
+  if (a.split_k > 1 && (!tc || a.dynamic || a.split_k > 8 || grid % a.split_k != 0))
+    return cudaErrorInvalidValue;
+  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.tpp > 0 ? a.tpp : 1,
+                                     mode == kModeDown ? 1 : a.split_k);
   switch (mode) {
     case kModeStage1:
       return launch_mode<kModeStage1>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);

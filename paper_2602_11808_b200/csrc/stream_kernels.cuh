@@ -28,6 +28,12 @@ struct StreamArgs {
   int B;       // batch rows present
   int n_pad;   // MMA N (tcgen05) / activation box rows (GEMV)
   int stages;  // ring depth
+  // split_k (field below) > 1: stage-1 tiles are split along K over the
+  // split_k CTAs of a thread-block cluster; partial gate/up accumulators are
+  // reduced into the leader CTA's shared memory through DSMEM
+  // (red.shared::cluster) before the SiLU*up epilogue, so partial sums never
+  // leave the SMs.  Static plan, tcgen05 family only.
+  int split_k;
   int kbs;     // K blocks (16 KiB each) per ring stage
   // Stage-1 output: A2 [B x a2_ld] bf16, columns < cols_valid written.
   __nv_bfloat16* a2;
@@ -86,10 +92,15 @@ __host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs, int tpp = 
   return kbs * (tpp * 16384 + n_pad * 128);
 }
 
+// Stage-1 split-K reduction buffer (leader CTA of a cluster): fp32 [N][128].
+__host__ __device__ inline int split_red_bytes(int n_pad, int split_k) {
+  return split_k > 1 ? n_pad * 128 * 4 : 0;
+}
+
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xmap,
                           const CUtensorMap& amap, const StreamArgs& a, int grid,
                           bool pdl, cudaStream_t stream);
 
-int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp = 1);
+int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp = 1, int split_k = 1);
 
 }  // namespace dfk

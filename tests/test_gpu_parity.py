@@ -51,6 +51,10 @@ def configs(rt, B):
         "dyn_block_tpp2": rt.Config.make(block_kernel=1, dynamic_sched=1, tiles_per_piece=2),
         "dyn_fused_tpp2_ch5": rt.Config.make(dynamic_sched=1, tiles_per_piece=2, chunk_kb=5,
                                              s1_ctas=9, down_ctas=13),
+        "fused_sk2": rt.Config.make(s1_split_k=2),
+        "fused_sk4_c8": rt.Config.make(s1_split_k=4, s1_ctas=8, kbs=1),
+        "block_sk2": rt.Config.make(block_kernel=1, s1_split_k=2),
+        "block_sk8": rt.Config.make(block_kernel=1, s1_split_k=8, kbs=2),
         "two_kernel": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
         "four_kernel": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
     }
@@ -361,3 +365,25 @@ def test_forward_host_async_pipelined(rt, ctx, oracle_lib):
     ctx.sync()
     for i in range(3):
         assert rel_err(hy[i].arr, refs[i]) <= TOL, i
+
+
+@pytest.mark.parametrize("split", [2, 4])
+def test_split_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, split):
+    """Negative control (the reference's SiluPerKChunk mutant,
+    verification.cpp:84-124): applying SiLU*up to each K part of a split
+    tile and summing must FAIL parity, while the correct split-K passes."""
+    B, dm, df = 4, 1024, 1024
+    x, wu, wg, wd = instance(oracle_lib, 80 + split, B, dm, df)
+    a2_ref, _ = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    xd = ctx.array((B, dm)).upload(x)
+    for block in (0, 1):
+        a2 = ctx.array((B, df))
+        if block:
+            y = ctx.array((B, dm), rt.F32)
+        ok = rt.Config.make(s1_split_k=split, block_kernel=block)
+        bad = rt.Config.make(s1_split_k=split, block_kernel=block, mutant=1)
+        ctx.stage1(w, xd, a2, cfg=ok)
+        assert rel_err(a2.download(), a2_ref) <= TOL
+        ctx.stage1(w, xd, a2, cfg=bad)
+        assert rel_err(a2.download(), a2_ref) > 5 * TOL
