@@ -226,13 +226,18 @@ Launch launch_shape(int family) {
 }
 
 int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
-                 StreamArgs* a) {
+                 int grid, StreamArgs* a) {
   if (!cfg.dynamic_sched) return DFK_OK;
   DFK_TRY(ensure_buf(ctx->sched, 64, true, ctx->stream));
   a->dynamic = 1;
   a->sched = static_cast<int*>(ctx->sched.p);
+  // Enough down chunks for ~2 per CTA (small TP shards), at most 32 K blocks
+  // (512 KiB) each and at least 4.
+  const int per_tile = std::max(1, (2 * grid + w->dn_tiles - 1) / w->dn_tiles);
+  const int auto_chunk = (w->dn_kblocks + per_tile - 1) / per_tile;
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb
-                                 : std::max(1, std::min(w->dn_kblocks, 32));
+                                 : std::max(1, std::min({w->dn_kblocks, 32,
+                                                         std::max(4, auto_chunk)}));
   return DFK_OK;
 }
 
@@ -242,8 +247,17 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
 int effective_split(const dfk_config& cfg, const dfk_weights_s* w, int64_t nb) {
   const int sk = cfg.s1_split_k;
   if (sk <= 1 || cfg.s1_family == DFK_FAMILY_GEMV || cfg.dynamic_sched) return 1;
-  if (sk > 8 || round_up(nb, 16) > 64 || w->s1_kblocks % sk != 0) return 1;
+  if (sk > 8 || w->s1_kblocks % sk != 0) return 1;
+  if (split_red_bytes(static_cast<int>(round_up(nb, 16)), sk) > 64 * 1024) return 1;
   return sk;
+}
+
+// Clusters of `split` CTAs that can be co-resident for this launch shape.
+int cluster_cap(int mode, const StreamArgs& a) {
+  if (a.split_k <= 1) return 1 << 30;
+  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.tpp > 0 ? a.tpp : 1,
+                                     a.split_k);
+  return stream_max_clusters(mode, a.split_k, smem);
 }
 
 // Ring geometry for one launch: stage size (kbs), depth and tiles per piece.
@@ -315,14 +329,14 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     a.mutant = cfg.mutant;
-    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
     const int sk = a.split_k;
     // Clusters of sk CTAs; as many clusters as keep every cluster at the
-    // same tile count.
+    // same tile count, never more than can be co-resident.
     int clusters = cfg.s1_ctas > 0 ? cfg.s1_ctas / sk
                                    : balanced_grid(w->s1_tiles, ctx->sm_count / sk);
-    clusters = std::max(1, std::min(clusters, w->s1_tiles));
+    clusters = std::max(1, std::min({clusters, w->s1_tiles, cluster_cap(kModeStage1, a)}));
     const int grid = clusters * sk;
+    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
     cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
                                   grid, cfg.pdl != 0, ctx->stream);
     if (e != cudaSuccess)
@@ -349,12 +363,12 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
                      w->d_ff, nb, a_ld, a.n_pad, &tm));
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
-    DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
     // Default: 3/4 of the SMs with deep rings streams faster than every SM
-    // with the same ring (measured, profiles/sweeps_r1.md).
+    // with the same ring (measured, profiles/r1_sweeps.md).
     int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count * 3 / 4;
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, U));
+    DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a));
     cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
                                   static_cast<int>(grid), cfg.pdl != 0,
                                   ctx->stream);
@@ -443,13 +457,20 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     // Static plan: the balanced stage-1 grid; dynamic: 7/8 of the SMs (the
     // measured optimum, profiles/) -- never more CTAs than SMs, since down
     // pieces spin on other CTAs' stage-1 flags.
-    int grid = cfg.s1_ctas > 0       ? cfg.s1_ctas
-               : cfg.dynamic_sched ? ctx->sm_count * 7 / 8
-                                   : balanced_grid(w->s1_tiles, ctx->sm_count);
+    // Dynamic: 7/8 of the SMs; static: the balanced stage-1 grid but at least
+    // 3/4 of the SMs (the down work needs the CTAs even when the shard has
+    // few stage-1 tiles) -- always co-resident (down pieces spin on other
+    // CTAs' stage-1 flags): never more CTAs than SMs or resident clusters.
+    int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas
+               : cfg.dynamic_sched
+                   ? ctx->sm_count * 7 / 8
+                   : std::max(balanced_grid(w->s1_tiles, ctx->sm_count),
+                              ctx->sm_count * 3 / 4);
     grid = std::max(1, std::min(grid, ctx->sm_count));
-    grid = std::max(a.split_k, grid / a.split_k * a.split_k);
+    grid = std::min(grid / a.split_k, cluster_cap(kModeBlock, a)) * a.split_k;
+    grid = std::max(grid, a.split_k);
     block_plan(grid, w, &a);
-    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, &a));
+    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,

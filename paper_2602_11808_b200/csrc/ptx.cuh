@@ -183,6 +183,16 @@ __device__ __forceinline__ void st_dsmem_f4(const void* p, uint32_t rank,
       : "memory");
 }
 
+// Store one float into CTA `rank`'s shared memory (DSMEM).
+__device__ __forceinline__ void st_dsmem_f32(const float* p, uint32_t rank,
+                                             float v) {
+  asm volatile(
+      "{\n .reg .b32 ra;\n mapa.shared::cluster.u32 ra, %0, %1;\n"
+      " st.shared::cluster.f32 [ra], %2;\n}" ::"r"(smem_u32(p)),
+      "r"(rank), "f"(v)
+      : "memory");
+}
+
 // Atomic add into CTA `rank`'s shared memory (DSMEM) at the address `p`
 // has in this CTA.
 __device__ __forceinline__ void red_add_dsmem(const float* p, uint32_t rank,

@@ -693,12 +693,14 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
 // ---------------------------------------------------------------------------
 // tcgen05 epilogue (warps 2-5; TMEM lanes 32*(warp%4) .. +31).
 // ---------------------------------------------------------------------------
-// Stage-1 epilogue of a K-split tile (cluster of p.split CTAs).  Non-leaders
-// add their partial gate/up accumulators into the leader's smem buffer
-// red[n][row] over DSMEM and arrive on the leader's red_full barrier; the
-// leader adds them to its own partial, runs SiLU*up, writes A2, re-zeroes the
-// buffer and releases every non-leader's red_free barrier.  mutant == 1
-// applies SiLU per K part instead (the reference's SiluPerKChunk negative
+// Stage-1 epilogue of a K-split tile (cluster of p.split CTAs).  Each
+// non-leader stores its partial gate/up accumulators into ITS OWN slot
+// red[rank-1][n][row] of the leader's shared memory with plain DSMEM stores
+// (a warp writes 128 contiguous bytes per n; no atomics, no contention) and
+// arrives on the leader's red_full barrier; the leader adds the slots to its
+// own partial, runs SiLU*up, writes A2 and releases every non-leader's
+// red_free barrier.  Partial sums never leave the SMs.  mutant == 1 applies
+// SiLU*up per K part instead (the reference's SiluPerKChunk negative
 // control, verification.cpp:84-124) and must fail parity.
 __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
                                                   const Plan& p, int tile,
@@ -712,7 +714,9 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
   const int col = tile * kS1Cols + cofs;
   const uint32_t par = static_cast<uint32_t>(split_iter & 1);
   const bool mutant = a.mutant == 1;
+  const int slot_floats = a.n_pad * 128;
   if (p.krank != 0) {
+    float* mine = red + (p.krank - 1) * slot_floats;
     mbar_wait_cluster(red_free, par ^ 1u);
     for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
       float v[16];
@@ -724,7 +728,7 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
           const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
           val = is_up ? 0.f : silu_f(v[e]) * up;
         }
-        red_add_dsmem(red + (c0 + e) * 128 + row, 0, val);
+        st_dsmem_f32(mine + (c0 + e) * 128 + row, 0, val);
       }
     }
     mbar_arrive_cluster(red_full, 0);
@@ -737,9 +741,8 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
     tmem_ld16(taddr + c0, v);
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      float* slot = red + (c0 + e) * 128 + row;
-      const float other = *slot;
-      *slot = 0.f;
+      float other = 0.f;
+      for (int r = 1; r < p.split; ++r) other += red[(r - 1) * slot_floats + (c0 + e) * 128 + row];
       float out;
       if (!mutant) {
         const float g_or_u = v[e] + other;
@@ -904,9 +907,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     }
     fence_barrier_init();
   }
-  if (split) {
-    for (int i = threadIdx.x; i < a.n_pad * 128; i += blockDim.x) red[i] = 0.f;
-  }
+
   uint32_t tmem_cols = 0;
   if constexpr (kTC) {
     tmem_cols = 32;
@@ -1011,6 +1012,35 @@ cudaError_t launch_mode(bool tc, int nb, const CUtensorMap& xmap,
 }
 
 }  // namespace
+
+// How many clusters of `split` CTAs (with this kernel's smem) can be
+// co-resident; clusters beyond it would run in a second wave (and, in the
+// block kernel, spin on flags of tiles whose CTAs are not resident yet).
+int stream_max_clusters(int mode, int split, int smem) {
+  if (split <= 1) return 1 << 30;
+  auto kern = mode == kModeBlock ? stream_kernel<kModeBlock, true, 0>
+                                 : stream_kernel<kModeStage1, true, 0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (split > 8)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(split * 64));
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = static_cast<unsigned>(split);
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n > 0 ? n : 1;
+}
 
 int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp, int split_k) {
   return 1024 + stages * stream_stage_bytes(n_pad, kbs, tpp) + (2 * stages + 4) * 8 +

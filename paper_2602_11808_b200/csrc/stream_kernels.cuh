@@ -92,9 +92,10 @@ __host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs, int tpp = 
   return kbs * (tpp * 16384 + n_pad * 128);
 }
 
-// Stage-1 split-K reduction buffer (leader CTA of a cluster): fp32 [N][128].
+// Stage-1 split-K reduction buffer (leader CTA of a cluster): one fp32
+// [N][128] slot per non-leader rank.
 __host__ __device__ inline int split_red_bytes(int n_pad, int split_k) {
-  return split_k > 1 ? n_pad * 128 * 4 : 0;
+  return split_k > 1 ? (split_k - 1) * n_pad * 128 * 4 : 0;
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xmap,
@@ -102,5 +103,6 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xma
                           bool pdl, cudaStream_t stream);
 
 int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp = 1, int split_k = 1);
+int stream_max_clusters(int mode, int split, int smem);
 
 }  // namespace dfk

@@ -63,7 +63,7 @@ for spec in a.cfgs.split(";"):
         print(f"  piece {i}: n={n:3d} issue {np.nanmin(iss):6.1f} {np.nanmedian(iss):6.1f} {np.nanmax(iss):6.1f}"
               f"  retire {np.nanmin(ret):6.1f} {np.nanmedian(ret):6.1f} {np.nanmax(ret):6.1f}")
     # coarse per-CTA listing of the slowest 5
-    order = np.argsort(-rel[:, 2])[:5]
+    order = np.argsort(-rel[:, 2])[:8]
     for c in order:
         vals = " ".join(f"{v:6.1f}" for v in rel[c, 3:15] if not np.isnan(v))
         print(f"  cta{np.flatnonzero(used)[c]:4d} done {rel[c,2]:6.1f}: {vals}")
