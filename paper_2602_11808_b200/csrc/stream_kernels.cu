@@ -731,7 +731,12 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
         st_dsmem_f32(mine + (c0 + e) * 128 + row, 0, val);
       }
     }
-    mbar_arrive_cluster(red_full, 0);
+    // One remote arrive per warp (hundreds of per-thread arrivals on one
+    // mbarrier serialise at the leader): every lane's DSMEM stores are
+    // fenced at cluster scope, the warp syncs, lane 0 releases.
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cluster(red_full, 0);
     return;
   }
   // Leader.
@@ -758,9 +763,12 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
       }
     }
   }
-  // Every non-leader's buffer-free barrier counts 128 arrivals per phase.
-  for (int r = 1; r < p.split; ++r) mbar_arrive_cluster(red_free, r);
-  (void)lane;
+  // Each non-leader's buffer-free barrier counts one arrival per leader
+  // epilogue warp.
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  __syncwarp();
+  if (lane == 0)
+    for (int r = 1; r < p.split; ++r) mbar_arrive_cluster(red_free, r);
 }
 
 __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
@@ -902,8 +910,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
       mbar_init(&pq->empty[i], kTC ? 5 : kGemvWarps);
     }
     if (split) {
-      mbar_init(red_full, (a.split_k - 1) * 128);  // every non-leader epilogue thread
-      mbar_init(red_free, 128);                     // every leader epilogue thread
+      mbar_init(red_full, (a.split_k - 1) * 4);  // one per non-leader epilogue warp
+      mbar_init(red_free, 4);                     // one per leader epilogue warp
     }
     fence_barrier_init();
   }
@@ -961,18 +969,32 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   }
 }
 
+// Opt every kernel instantiation in to the device's full dynamic shared
+// memory once (the per-launch amount is set in the launch config).
+cudaError_t allow_max_smem(const void* kern) {
+  static int max_optin = -1;
+  static const void* done[64];
+  static int ndone = 0;
+  for (int i = 0; i < ndone; ++i)
+    if (done[i] == kern) return cudaSuccess;
+  if (max_optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  const cudaError_t e = cudaFuncSetAttribute(
+      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+  if (e == cudaSuccess && ndone < 64) done[ndone++] = kern;
+  return e;
+}
+
 template <int kMode, bool kTC, int NB>
 cudaError_t launch_one(const CUtensorMap& xmap, const CUtensorMap& amap,
                        const StreamArgs& a, int grid, int smem, bool pdl,
                        cudaStream_t stream) {
   auto kern = stream_kernel<kMode, kTC, NB>;
-  static int configured_smem = -1;  // per instantiation; one device per process
-  if (smem > configured_smem) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured_smem = smem;
-  }
+  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kTC ? kTcThreads : kGemvThreads);
@@ -1020,7 +1042,7 @@ int stream_max_clusters(int mode, int split, int smem) {
   if (split <= 1) return 1 << 30;
   auto kern = mode == kModeBlock ? stream_kernel<kModeBlock, true, 0>
                                  : stream_kernel<kModeStage1, true, 0>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  allow_max_smem(reinterpret_cast<const void*>(kern));
   if (split > 8)
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
