@@ -717,7 +717,9 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
   const int slot_floats = a.n_pad * 128;
   if (p.krank != 0) {
     float* mine = red + (p.krank - 1) * slot_floats;
+    if (row == 0 && split_iter == 0) trace_stamp(a, 61);
     mbar_wait_cluster(red_free, par ^ 1u);
+    if (row == 0 && split_iter == 0) trace_stamp(a, 62);
     for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
       float v[16];
       tmem_ld16(taddr + c0, v);
@@ -737,10 +739,13 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
     asm volatile("fence.acq_rel.cluster;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive_cluster(red_full, 0);
+    if (row == 0 && split_iter == 0) trace_stamp(a, 63);
     return;
   }
   // Leader.
+  if (row == 0 && split_iter == 0) trace_stamp(a, 61);
   mbar_wait_cluster(red_full, par);
+  if (row == 0 && split_iter == 0) trace_stamp(a, 62);
   for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
     float v[16];
     tmem_ld16(taddr + c0, v);

@@ -62,6 +62,15 @@ for spec in a.cfgs.split(";"):
         n = np.sum(~np.isnan(ret))
         print(f"  piece {i}: n={n:3d} issue {np.nanmin(iss):6.1f} {np.nanmedian(iss):6.1f} {np.nanmax(iss):6.1f}"
               f"  retire {np.nanmin(ret):6.1f} {np.nanmedian(ret):6.1f} {np.nanmax(ret):6.1f}")
+    if np.any(~np.isnan(rel[:, 61])):
+        for sl, nm in ((61, "split: before wait"), (62, "split: after wait"), (63, "split: non-leader arrived")):
+            col = rel[:, sl]
+            lead = np.array([i % 4 == 0 for i in np.flatnonzero(used)])
+            for who, m in (("leaders", lead), ("others", ~lead)):
+                c = col[m]
+                c = c[~np.isnan(c)]
+                if len(c):
+                    print(f"  {nm:28s} {who:8s} {c.min():6.1f} {np.median(c):6.1f} {c.max():6.1f}")
     # coarse per-CTA listing of the slowest 5
     order = np.argsort(-rel[:, 2])[:8]
     for c in order:
