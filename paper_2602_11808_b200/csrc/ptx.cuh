@@ -193,6 +193,28 @@ __device__ __forceinline__ void st_dsmem_f32(const float* p, uint32_t rank,
       : "memory");
 }
 
+// Asynchronous 16-byte DSMEM store into CTA `rank` whose completion is
+// counted (in bytes) on that CTA's mbarrier `bar` (same smem offset).
+__device__ __forceinline__ void st_async_f4(const void* p, uint64_t* bar,
+                                            uint32_t rank, float x, float y,
+                                            float z, float w) {
+  asm volatile(
+      "{\n .reg .b32 ra, rb;\n mapa.shared::cluster.u32 ra, %0, %6;\n"
+      " mapa.shared::cluster.u32 rb, %1, %6;\n"
+      " st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [ra], "
+      "{%2, %3, %4, %5}, [rb];\n}" ::"r"(smem_u32(p)),
+      "r"(smem_u32(bar)), "f"(x), "f"(y), "f"(z), "f"(w), "r"(rank)
+      : "memory");
+}
+
+__device__ __forceinline__ float4 ld_shared_f4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
 // Atomic add into CTA `rank`'s shared memory (DSMEM) at the address `p`
 // has in this CTA.
 __device__ __forceinline__ void red_add_dsmem(const float* p, uint32_t rank,
@@ -307,7 +329,14 @@ __device__ __forceinline__ float bf16hi(uint32_t u) {
 // silu(g) = g * sigmoid(g), stable for |g| >> 1 (no NaN: __expf saturates to
 // inf/0 and the division stays finite), mirroring tensor.hpp:155-163.
 __device__ __forceinline__ float silu_f(float g) {
-  return g / (1.0f + __expf(-g));
+  // rcp(inf) = 0, so large negative g gives -0, never NaN.
+  return g * __frcp_rn(1.0f + __expf(-g));
+}
+
+__device__ __forceinline__ float ld_shared_f32(const float* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
+  return v;
 }
 
 }  // namespace dfk

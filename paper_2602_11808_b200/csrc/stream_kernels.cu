@@ -694,18 +694,18 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
 // tcgen05 epilogue (warps 2-5; TMEM lanes 32*(warp%4) .. +31).
 // ---------------------------------------------------------------------------
 // Stage-1 epilogue of a K-split tile (cluster of p.split CTAs).  Each
-// non-leader stores its partial gate/up accumulators into ITS OWN slot
-// red[rank-1][n][row] of the leader's shared memory with plain DSMEM stores
-// (a warp writes 128 contiguous bytes per n; no atomics, no contention) and
-// arrives on the leader's red_full barrier; the leader adds the slots to its
-// own partial, runs SiLU*up, writes A2 and releases every non-leader's
-// red_free barrier.  Partial sums never leave the SMs.  mutant == 1 applies
-// SiLU*up per K part instead (the reference's SiluPerKChunk negative
-// control, verification.cpp:84-124) and must fail parity.
+// non-leader writes its partial gate/up accumulators into ITS OWN slot
+// red[rank-1][row][n] of the leader's shared memory with st.async (16-byte
+// DSMEM stores whose completion is counted in bytes on the leader's
+// red_full mbarrier: no fences, no per-thread arrivals); the leader adds the
+// slots to its own partial, runs SiLU*up, writes A2 and releases every
+// non-leader's red_free barrier.  Partial sums never leave the SMs.
+// mutant == 1 applies SiLU*up per K part instead (the reference's
+// SiluPerKChunk negative control, verification.cpp:84-124): must fail parity.
 __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
                                                   const Plan& p, int tile,
                                                   uint32_t taddr, int row,
-                                                  int lane, float* red,
+                                                  int lane, int tid, float* red,
                                                   uint64_t* red_full,
                                                   uint64_t* red_free,
                                                   int split_iter) {
@@ -714,53 +714,64 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
   const int col = tile * kS1Cols + cofs;
   const uint32_t par = static_cast<uint32_t>(split_iter & 1);
   const bool mutant = a.mutant == 1;
-  const int slot_floats = a.n_pad * 128;
+  const int rs = split_row_floats(a.n_pad);
+  const int slot_floats = 128 * rs;
   if (p.krank != 0) {
-    float* mine = red + (p.krank - 1) * slot_floats;
+    float* mine = red + (p.krank - 1) * slot_floats + row * rs;
     if (row == 0 && split_iter == 0) trace_stamp(a, 61);
     mbar_wait_cluster(red_free, par ^ 1u);
     if (row == 0 && split_iter == 0) trace_stamp(a, 62);
     for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
       float v[16];
       tmem_ld16(taddr + c0, v);
+      if (mutant) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        float val = v[e];
-        if (mutant) {
+        for (int e = 0; e < 16; ++e) {
           const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
-          val = is_up ? 0.f : silu_f(v[e]) * up;
+          v[e] = is_up ? 0.f : silu_f(v[e]) * up;
         }
-        st_dsmem_f32(mine + (c0 + e) * 128 + row, 0, val);
       }
+#pragma unroll
+      for (int e = 0; e < 16; e += 4)
+        st_async_f4(mine + c0 + e, red_full, 0, v[e], v[e + 1], v[e + 2], v[e + 3]);
     }
-    // One remote arrive per warp (hundreds of per-thread arrivals on one
-    // mbarrier serialise at the leader): every lane's DSMEM stores are
-    // fenced at cluster scope, the warp syncs, lane 0 releases.
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cluster(red_full, 0);
     if (row == 0 && split_iter == 0) trace_stamp(a, 63);
     return;
   }
-  // Leader.
+  // Leader: arm the byte count of this phase, wait for every partner slot.
+  if (tid == 0)
+    mbar_arrive_expect_tx(red_full, static_cast<uint32_t>((p.split - 1) * 128 * a.n_pad * 4));
   if (row == 0 && split_iter == 0) trace_stamp(a, 61);
   mbar_wait_cluster(red_full, par);
   if (row == 0 && split_iter == 0) trace_stamp(a, 62);
+  if ((row & 31) == 0 && split_iter == 0) trace_stamp(a, 44 + (row >> 5));
   for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+    float other[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) other[e] = 0.f;
+    for (int r = 1; r < p.split; ++r) {
+      const float* src = red + (r - 1) * slot_floats + row * rs + c0;
+#pragma unroll
+      for (int e = 0; e < 16; e += 4) {
+        const float4 t = ld_shared_f4(src + e);
+        other[e] += t.x;
+        other[e + 1] += t.y;
+        other[e + 2] += t.z;
+        other[e + 3] += t.w;
+      }
+    }
     float v[16];
     tmem_ld16(taddr + c0, v);
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      float other = 0.f;
-      for (int r = 1; r < p.split; ++r) other += red[(r - 1) * slot_floats + (c0 + e) * 128 + row];
       float out;
       if (!mutant) {
-        const float g_or_u = v[e] + other;
+        const float g_or_u = v[e] + other[e];
         const float up = __shfl_xor_sync(0xffffffffu, g_or_u, 16);
         out = silu_f(g_or_u) * up;
       } else {
         const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
-        out = silu_f(v[e]) * up + other;
+        out = silu_f(v[e]) * up + other[e];
       }
       const int n = c0 + e;
       if (!is_up && n < a.B && col < a.cols_valid) {
@@ -768,12 +779,13 @@ __device__ __forceinline__ void s1_split_epilogue(const StreamArgs& a,
       }
     }
   }
-  // Each non-leader's buffer-free barrier counts one arrival per leader
-  // epilogue warp.
-  asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  // Release the slots: one arrival per leader epilogue warp on every
+  // partner's red_free (the release orders this warp's slot reads).
+  if ((row & 31) == 0 && split_iter == 0) trace_stamp(a, 48 + (row >> 5));
   __syncwarp();
   if (lane == 0)
     for (int r = 1; r < p.split; ++r) mbar_arrive_cluster(red_free, r);
+  if ((row & 31) == 0 && split_iter == 0) trace_stamp(a, 52 + (row >> 5));
 }
 
 __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
@@ -801,7 +813,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       const uint32_t taddr = tmem_base +
                              (static_cast<uint32_t>(quarter * 32) << 16) +
                              static_cast<uint32_t>(ab * tpp * a.n_pad);
-      s1_split_epilogue(a, p, pc.tile, taddr, row, lane, red, red_full, red_free,
+      s1_split_epilogue(a, p, pc.tile, taddr, row, lane, tid, red, red_full, red_free,
                         split_iter++);
       tc_fence_before();
       __syncwarp();
@@ -915,8 +927,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
       mbar_init(&pq->empty[i], kTC ? 5 : kGemvWarps);
     }
     if (split) {
-      mbar_init(red_full, (a.split_k - 1) * 4);  // one per non-leader epilogue warp
-      mbar_init(red_free, 4);                     // one per leader epilogue warp
+      mbar_init(red_full, 1);  // the leader's expect_tx; partners count bytes
+      mbar_init(red_free, 4);  // one per leader epilogue warp
     }
     fence_barrier_init();
   }

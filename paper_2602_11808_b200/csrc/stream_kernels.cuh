@@ -93,9 +93,11 @@ __host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs, int tpp = 
 }
 
 // Stage-1 split-K reduction buffer (leader CTA of a cluster): one fp32
-// [N][128] slot per non-leader rank.
+// [128][N + 4] slot per non-leader rank (row-major, padded against bank
+// conflicts of the 16-byte accesses).
+__host__ __device__ inline int split_row_floats(int n_pad) { return n_pad + 4; }
 __host__ __device__ inline int split_red_bytes(int n_pad, int split_k) {
-  return split_k > 1 ? (split_k - 1) * n_pad * 128 * 4 : 0;
+  return split_k > 1 ? (split_k - 1) * 128 * split_row_floats(n_pad) * 4 : 0;
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xmap,

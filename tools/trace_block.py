@@ -71,6 +71,14 @@ for spec in a.cfgs.split(";"):
                 c = c[~np.isnan(c)]
                 if len(c):
                     print(f"  {nm:28s} {who:8s} {c.min():6.1f} {np.median(c):6.1f} {c.max():6.1f}")
+    if np.any(~np.isnan(rel[:, 44])):
+        lead = np.array([i % 4 == 0 for i in np.flatnonzero(used)])
+        for base, nm in ((44, "leader q: after wait"), (48, "leader q: after loop"), (52, "leader q: after arrives")):
+            for qq in range(4):
+                c = rel[lead, base + qq]
+                c = c[~np.isnan(c)]
+                if len(c):
+                    print(f"  {nm} {qq}  {c.min():6.1f} {np.median(c):6.1f} {c.max():6.1f}")
     # coarse per-CTA listing of the slowest 5
     order = np.argsort(-rel[:, 2])[:8]
     for c in order:
