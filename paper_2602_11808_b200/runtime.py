@@ -55,6 +55,9 @@ def library_path() -> str:
 
 
 def _load() -> C.CDLL:
+    override = os.environ.get("DFK_LIB")  # A/B timing of another build (tools/)
+    if override:
+        return C.CDLL(override)
     path = _build.LIB
     if not os.path.exists(path) or _build._stale():
         try:
@@ -164,6 +167,8 @@ _sigs = {
 }
 EXPORTED_SYMBOLS = tuple(_sigs)
 for _name, (_args, _res) in _sigs.items():
+    if os.environ.get("DFK_LIB") and not hasattr(lib, _name):
+        continue  # an older build under A/B test
     _f = getattr(lib, _name)
     _f.argtypes = _args
     _f.restype = _res
