@@ -231,13 +231,19 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   DFK_TRY(ensure_buf(ctx->sched, 64, true, ctx->stream));
   a->dynamic = 1;
   a->sched = static_cast<int*>(ctx->sched.p);
-  // Enough down chunks for ~2 per CTA (small TP shards), at most 32 K blocks
-  // (512 KiB) each and at least 4.
-  const int per_tile = std::max(1, (2 * grid + w->dn_tiles - 1) / w->dn_tiles);
-  const int auto_chunk = (w->dn_kblocks + per_tile - 1) / per_tile;
-  a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb
-                                 : std::max(1, std::min({w->dn_kblocks, 32,
-                                                         std::max(4, auto_chunk)}));
+  // 32-K-block (512 KiB) down chunks measured best on full-size weights; a
+  // shard with few down tiles gets smaller chunks so that there are at least
+  // ~1.5 pieces per CTA (but never under 4 K blocks).
+  int chunk = std::min(w->dn_kblocks, 32);
+  const int64_t pieces = static_cast<int64_t>(w->dn_tiles) *
+                         ((w->dn_kblocks + chunk - 1) / chunk);
+  if (pieces * 2 < 3LL * grid) {
+    const int per_tile =
+        std::max(1, (3 * grid + 2 * w->dn_tiles - 1) / (2 * w->dn_tiles));
+    chunk = std::max(std::min(4, w->dn_kblocks),
+                     (w->dn_kblocks + per_tile - 1) / per_tile);
+  }
+  a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
   return DFK_OK;
 }
 
