@@ -113,10 +113,7 @@ typedef struct dfk_config {
                            (tiles, then fixed-size down chunks) instead of
                            the static byte-balanced plan                    */
   int32_t chunk_kb;     /* K blocks per dynamic down chunk (0 = auto)      */
-  int32_t tiles_per_piece; /* dynamic tcgen05 path: weight tiles streamed
-                           against one activation stage (1 or 2; 0 = auto:
-                           2 when the batch pads to >= 32)                */
-  int32_t reserved[1];
+  int32_t reserved[2];
   char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
 } dfk_config;
 

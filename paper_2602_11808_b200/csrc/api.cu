@@ -76,7 +76,7 @@ std::string config_label(const dfk_config& c) {
   if (c.variant == DFK_VARIANT_TWO_KERNEL) return "two_kernel_cublaslt";
   if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
   if (c.block_kernel) {
-    if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_tpp" << c.tiles_per_piece << "_";
+    if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
     if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
@@ -149,22 +149,20 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
   return DFK_OK;
 }
 
-int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int tpp = 1,
-               int split_k = 1) {
+int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int split_k = 1) {
   const int avail =
       ctx->max_smem_optin - 1024 - 1024 - split_red_bytes(n_pad, split_k);
-  int s = avail / stream_stage_bytes(n_pad, kbs, tpp);
+  int s = avail / stream_stage_bytes(n_pad, kbs);
   return std::min(s, 32);
 }
 
 // Bigger ring stages stream faster (tools/stream_probe.cu, profiles/): take
 // the largest stage (up to 4 x 16 KiB weight blocks) that still leaves 3
 // slots in shared memory.
-int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int tpp = 1,
-             int split_k = 1) {
+int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int split_k = 1) {
   if (requested > 0) return std::min(requested, 4);
   for (int kbs = 4; kbs > 1; --kbs)
-    if (max_stages(ctx, n_pad, kbs, tpp, split_k) >= 3) return kbs;
+    if (max_stages(ctx, n_pad, kbs, split_k) >= 3) return kbs;
   return 1;
 }
 
@@ -261,12 +259,11 @@ int effective_split(const dfk_config& cfg, const dfk_weights_s* w, int64_t nb) {
 // Clusters of `split` CTAs that can be co-resident for this launch shape.
 int cluster_cap(int mode, const StreamArgs& a) {
   if (a.split_k <= 1) return 1 << 30;
-  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.tpp > 0 ? a.tpp : 1,
-                                     a.split_k);
+  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.split_k);
   return stream_max_clusters(mode, a.split_k, smem);
 }
 
-// Ring geometry for one launch: stage size (kbs), depth and tiles per piece.
+// Ring geometry for one launch: stage size (kbs) and depth.
 void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
                  int stages_req, const dfk_config& cfg, StreamArgs* a) {
   const int n_pad = tc ? static_cast<int>(round_up(nb, 16)) : 8;
@@ -278,20 +275,10 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   a->kb2 = w->dn_kblocks;
   a->B = static_cast<int>(nb);
   a->n_pad = n_pad;
-  // Optional: two weight tiles per activation stage (halves the X / A2
-  // re-reads; dynamic tcgen05 path only; TMEM holds 2 x tpp x N columns).
-  // Measured slower at every batch on Llama-8B (the 2 x weight smem forces
-  // 16 KiB copies and a shallow ring, profiles/r1_sweeps.md), so opt-in.
-  int tpp = 1;
-  if (tc && cfg.dynamic_sched && cfg.tiles_per_piece > 1) {
-    tpp = std::min(cfg.tiles_per_piece, 2);
-    if (2 * tpp * n_pad > 512) tpp = 1;
-  }
-  a->tpp = tpp;
   const int sk = a->split_k > 1 ? a->split_k : 1;
-  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, tpp, sk);
+  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk);
   a->trace = ctx->trace;
-  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, tpp, sk));
+  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, sk));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
 

@@ -107,14 +107,11 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx,
   };
   for (int f : fams) {
     add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
-    for (int tpp : {0}) {  // tpp=2 measured slower everywhere (profiles/)
-      dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
-      d.dynamic_sched = 1;
-      d.tiles_per_piece = tpp;
-      std::snprintf(d.label, sizeof(d.label), "%s", "");
-      std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
-      add(d);
-    }
+    dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
+    d.dynamic_sched = 1;
+    std::snprintf(d.label, sizeof(d.label), "%s", "");
+    std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
+    add(d);
   }
   const int dn_ctas[2] = {0, ctx->sm_count};  // 0 = library default (3/4 SMs)
   for (int s1f : fams)
@@ -151,7 +148,7 @@ json cfg_to_json(const dfk_config& c) {
               {"s1_split_k", c.s1_split_k},   {"down_family", c.down_family},
               {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
               {"pdl", c.pdl},                 {"dynamic_sched", c.dynamic_sched},
-              {"chunk_kb", c.chunk_kb},       {"tiles_per_piece", c.tiles_per_piece},
+              {"chunk_kb", c.chunk_kb},
               {"label", std::string(c.label)}};
 }
 
@@ -183,7 +180,6 @@ dfk_config cfg_from_json(const json& j) {
   c.kbs = get_field<int>(j, "kbs");
   c.dynamic_sched = get_field<int>(j, "dynamic_sched");
   c.chunk_kb = get_field<int>(j, "chunk_kb");
-  c.tiles_per_piece = get_field<int>(j, "tiles_per_piece");
   std::snprintf(c.label, sizeof(c.label), "%s",
                 get_field<std::string>(j, "label").c_str());
   return c;

@@ -65,9 +65,8 @@ constexpr int kMaxKbs = 4;
 // ---------------------------------------------------------------------------
 struct Piece {
   int down;  // 0 = stage-1 tile, 1 = down piece
-  int tile;  // first tile
+  int tile;
   int kb0, kb1;
-  int nt = 1;  // adjacent tiles covered (tpp)
 };
 
 struct Plan {
@@ -133,7 +132,6 @@ struct PieceIter {
         out.tile = p.q + i * p.Q;
         out.kb0 = p.krank * a.kb1 / p.split;
         out.kb1 = (p.krank + 1) * a.kb1 / p.split;
-        out.nt = 1;
         ++i;
         return true;
       }
@@ -152,7 +150,6 @@ struct PieceIter {
         out.tile = t;
         out.kb0 = kb;
         out.kb1 = kb + static_cast<int>(end - u);
-        out.nt = 1;
         u = end;
         ++i;
         return true;
@@ -172,7 +169,6 @@ struct PieceIter {
     out.tile = t;
     out.kb0 = kb;
     out.kb1 = kb + static_cast<int>(end - u);
-    out.nt = 1;
     u = end;
     ++i;
     return true;
@@ -195,25 +191,21 @@ __device__ __forceinline__ int dyn_chunks(const StreamArgs& a) {
 
 __device__ __forceinline__ bool decode_dyn(const StreamArgs& a, int mode,
                                            int64_t idx, Piece& out) {
-  const int tpp = a.tpp > 0 ? a.tpp : 1;
-  const int g1 = (a.t1 + tpp - 1) / tpp;  // stage-1 pieces (tile groups)
-  const int g2 = (a.t2 + tpp - 1) / tpp;  // down tile groups per K chunk
-  const int64_t n1 = mode != kModeDown ? g1 : 0;
-  const int64_t n2 = mode != kModeStage1 ? static_cast<int64_t>(g2) * dyn_chunks(a) : 0;
+  const int64_t n1 = mode != kModeDown ? a.t1 : 0;
+  const int64_t n2 =
+      mode != kModeStage1 ? static_cast<int64_t>(a.t2) * dyn_chunks(a) : 0;
   if (idx < n1) {
     out.down = 0;
-    out.tile = static_cast<int>(idx) * tpp;
-    out.nt = min(tpp, a.t1 - out.tile);
+    out.tile = static_cast<int>(idx);
     out.kb0 = 0;
     out.kb1 = a.kb1;
     return true;
   }
   idx -= n1;
   if (idx >= n2) return false;
-  const int kc = static_cast<int>(idx / g2);
+  const int kc = static_cast<int>(idx / a.t2);
   out.down = 1;
-  out.tile = static_cast<int>(idx % g2) * tpp;
-  out.nt = min(tpp, a.t2 - out.tile);
+  out.tile = static_cast<int>(idx % a.t2);
   out.kb0 = kc * a.chunk_kb;
   out.kb1 = min(a.kb2, out.kb0 + a.chunk_kb);
   return true;
@@ -251,8 +243,7 @@ struct PieceReader {
     out.tile = v.x;
     out.kb0 = v.y;
     out.kb1 = v.z;
-    out.down = v.w & 0xFF;
-    out.nt = v.w >> 8;
+    out.down = v.w;
     return true;
   }
 };
@@ -426,9 +417,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
   const bool leader = lane_id() == 0;
   const uint64_t policy = policy_evict_first();
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
-  const int tpp = a.tpp > 0 ? a.tpp : 1;
-  const uint32_t wtile = static_cast<uint32_t>(a.kbs) * kBlockBytes;  // per tile
-  const uint32_t wbytes_all = static_cast<uint32_t>(tpp) * wtile;
+  const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
   struct Pend {
     int kb, nb, down, pk0, pk1;
   };
@@ -477,8 +466,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
         __syncwarp();
       }
       if (leader) {
-        pq->q[slot] = make_int4(pc.tile, pc.kb0, pc.kb1,
-                                valid ? (pc.down | (pc.nt << 8)) : -1);
+        pq->q[slot] = make_int4(pc.tile, pc.kb0, pc.kb1, valid ? pc.down : -1);
         mbar_arrive(&pq->full[slot]);
       }
     }
@@ -496,18 +484,13 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       }
       uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
       if (leader) {
-        mbar_arrive_expect_tx(
-            &full[slot],
-            static_cast<uint32_t>(nb) *
-                (static_cast<uint32_t>(pc.nt) * kBlockBytes + xblk));
-        // nb consecutive K blocks of one tile are contiguous in the pack; one
-        // copy per tile of the piece.
-        for (int j = 0; j < pc.nt; ++j) {
-          bulk_g2s(st + j * wtile,
-                   wbase + (static_cast<int64_t>(pc.tile + j) * kbt + kb) *
-                               static_cast<int64_t>(kBlockBytes),
-                   static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
-        }
+        mbar_arrive_expect_tx(&full[slot],
+                              static_cast<uint32_t>(nb) * (kBlockBytes + xblk));
+        // nb consecutive K blocks of one tile are contiguous in the pack.
+        bulk_g2s(st,
+                 wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
+                             static_cast<int64_t>(kBlockBytes),
+                 static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
       }
       if (!waited) {
         pend[npend++] = {kb, nb, pc.down, pc.kb0, pc.kb1};
@@ -649,9 +632,7 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
                                           uint32_t tmem_base, PieceQueue* pq) {
   const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>(a.n_pad));
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
-  const int tpp = a.tpp > 0 ? a.tpp : 1;
-  const uint32_t wtile = static_cast<uint32_t>(a.kbs) * kBlockBytes;
-  const uint32_t wbytes_all = static_cast<uint32_t>(tpp) * wtile;
+  const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
   int64_t it = 0;
   int acc_it = 0;
   PieceReader pi;
@@ -661,7 +642,7 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tempty[ab], aph ^ 1u);
     tc_fence_after();
-    const uint32_t d = tmem_base + static_cast<uint32_t>(ab * tpp * a.n_pad);
+    const uint32_t d = tmem_base + static_cast<uint32_t>(ab * a.n_pad);
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
       const int slot = static_cast<int>(it % a.stages);
@@ -671,16 +652,13 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
       const uint32_t sbase =
           smem_u32(smem + static_cast<int64_t>(slot) * stage_bytes);
       for (int b = 0; b < nb; ++b) {
+        const uint32_t wb = sbase + b * kBlockBytes;
         const uint32_t xb = sbase + wbytes_all + b * xblk;
-        for (int j = 0; j < pc.nt; ++j) {
-          const uint32_t wb = sbase + j * wtile + b * kBlockBytes;
-          const uint32_t dj = d + static_cast<uint32_t>(j * a.n_pad);
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k) {
-            tc_mma_bf16(dj, umma_desc_sw128(wb + k * 32),
-                        umma_desc_sw128(xb + k * 32), idesc,
-                        (kb > pc.kb0 || b > 0 || k > 0) ? 1u : 0u);
-          }
+        for (int k = 0; k < kBlockK / 16; ++k) {
+          tc_mma_bf16(d, umma_desc_sw128(wb + k * 32),
+                      umma_desc_sw128(xb + k * 32), idesc,
+                      (kb > pc.kb0 || b > 0 || k > 0) ? 1u : 0u);
         }
       }
       tc_commit(&empty[slot]);
@@ -808,11 +786,10 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tfull[ab], aph);
     tc_fence_after();
-    const int tpp = a.tpp > 0 ? a.tpp : 1;
+    const uint32_t taddr = tmem_base +
+                           (static_cast<uint32_t>(quarter * 32) << 16) +
+                           static_cast<uint32_t>(ab * a.n_pad);
     if (!pc.down && p.split > 1) {
-      const uint32_t taddr = tmem_base +
-                             (static_cast<uint32_t>(quarter * 32) << 16) +
-                             static_cast<uint32_t>(ab * tpp * a.n_pad);
       s1_split_epilogue(a, p, pc.tile, taddr, row, lane, tid, red, red_full, red_free,
                         split_iter++);
       tc_fence_before();
@@ -823,55 +800,43 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       ++acc_it;
       continue;
     }
-    const uint32_t tbase = tmem_base +
-                           (static_cast<uint32_t>(quarter * 32) << 16) +
-                           static_cast<uint32_t>(ab * tpp * a.n_pad);
     if (!pc.down) {
       int is_up, cofs;
       s1_row_map(row, &is_up, &cofs);
-      for (int jt = 0; jt < pc.nt; ++jt) {
-        const uint32_t taddr = tbase + static_cast<uint32_t>(jt * a.n_pad);
-        const int col = (pc.tile + jt) * kS1Cols + cofs;
-        for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
-          float v[16];
-          tmem_ld16(taddr + c0, v);
+      const int col = pc.tile * kS1Cols + cofs;
+      for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
-            const int n = c0 + e;
-            if (!is_up && n < a.B && col < a.cols_valid) {
-              a.a2[n * a.a2_ld + col] = __float2bfloat16_rn(silu_f(v[e]) * up);
-            }
+        for (int e = 0; e < 16; ++e) {
+          const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
+          const int n = c0 + e;
+          if (!is_up && n < a.B && col < a.cols_valid) {
+            a.a2[n * a.a2_ld + col] = __float2bfloat16_rn(silu_f(v[e]) * up);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      if (a.flags) {
-        for (int jt = 0; jt < pc.nt; ++jt) s1_publish(a, pc.tile + jt, tid, 128);
-      }
+      if (a.flags) s1_publish(a, pc.tile, tid, 128);
     } else {
-      for (int jt = 0; jt < pc.nt; ++jt) {
-        const uint32_t taddr = tbase + static_cast<uint32_t>(jt * a.n_pad);
-        const int j = (pc.tile + jt) * kDownCols + row;
-        for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
-          float v[16];
-          tmem_ld16(taddr + c0, v);
+      const int j = pc.tile * kDownCols + row;
+      for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int n = c0 + e;
-            if (n < a.B && j < a.out_cols) {
-              atomicAdd(a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j, v[e]);
-            }
+        for (int e = 0; e < 16; ++e) {
+          const int n = c0 + e;
+          if (n < a.B && j < a.out_cols) {
+            atomicAdd(a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j, v[e]);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      for (int jt = 0; jt < pc.nt; ++jt)
-        down_finish_tile(a, p, pc.tile + jt, tid, 128, smem_flag);
+      down_finish_tile(a, p, pc.tile, tid, 128, smem_flag);
     }
     if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
     ++acc_it;
@@ -894,7 +859,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
                   const StreamArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int stage_bytes = stream_stage_bytes(a.n_pad, a.kbs, a.tpp > 0 ? a.tpp : 1);
+  const int stage_bytes = stream_stage_bytes(a.n_pad, a.kbs);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
@@ -936,8 +901,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   uint32_t tmem_cols = 0;
   if constexpr (kTC) {
     tmem_cols = 32;
-    while (tmem_cols < static_cast<uint32_t>(2 * (a.tpp > 0 ? a.tpp : 1) * a.n_pad))
-      tmem_cols <<= 1;
+    while (tmem_cols < static_cast<uint32_t>(2 * a.n_pad)) tmem_cols <<= 1;
     if (w == 1) tmem_alloc(tmem_slot, tmem_cols);
   }
   __syncthreads();
@@ -1081,8 +1045,8 @@ int stream_max_clusters(int mode, int split, int smem) {
   return n > 0 ? n : 1;
 }
 
-int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp, int split_k) {
-  return 1024 + stages * stream_stage_bytes(n_pad, kbs, tpp) + (2 * stages + 4) * 8 +
+int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k) {
+  return 1024 + stages * stream_stage_bytes(n_pad, kbs) + (2 * stages + 4) * 8 +
          static_cast<int>(sizeof(PieceQueue)) + 128 + split_red_bytes(n_pad, split_k);
 }
 
@@ -1092,12 +1056,10 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
                           cudaStream_t stream) {
   if (a.kbs < 1 || a.kbs > kMaxKbs || a.stages < 2 || a.stages > 32)
     return cudaErrorInvalidValue;
-  if (a.tpp > 1 && (!tc || !a.dynamic || 2 * a.tpp * a.n_pad > 512))
-    return cudaErrorInvalidValue;
   if (a.split_k > 1 && (!tc || a.dynamic || a.split_k > 8 || grid % a.split_k != 0))
     return cudaErrorInvalidValue;
-  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.tpp > 0 ? a.tpp : 1,
-                                     mode == kModeDown ? 1 : a.split_k);
+  const int smem =
+      stream_smem_bytes(a.n_pad, a.stages, a.kbs, mode == kModeDown ? 1 : a.split_k);
   switch (mode) {
     case kModeStage1:
       return launch_mode<kModeStage1>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);

@@ -74,10 +74,6 @@ struct StreamArgs {
   int dynamic;
   int chunk_kb;
   int* sched;
-  // Tiles per piece (dynamic tcgen05 path): a piece streams `tpp` adjacent
-  // weight tiles against ONE activation stage (tpp accumulators in TMEM), so
-  // the X / A2 block of each K block is loaded once per tpp weight tiles.
-  int tpp;
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.
@@ -88,8 +84,8 @@ constexpr int kTraceSlots = 64;
 constexpr int kPieceQueue = 8;  // producer -> consumers piece queue depth
 
 // Smem bytes of one pipeline stage (weights + activation rows).
-__host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs, int tpp = 1) {
-  return kbs * (tpp * 16384 + n_pad * 128);
+__host__ __device__ inline int stream_stage_bytes(int n_pad, int kbs) {
+  return kbs * (16384 + n_pad * 128);
 }
 
 // Stage-1 split-K reduction buffer (leader CTA of a cluster): one fp32
@@ -104,7 +100,7 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xma
                           const CUtensorMap& amap, const StreamArgs& a, int grid,
                           bool pdl, cudaStream_t stream);
 
-int stream_smem_bytes(int n_pad, int stages, int kbs, int tpp = 1, int split_k = 1);
+int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k = 1);
 int stream_max_clusters(int mode, int split, int smem);
 
 }  // namespace dfk

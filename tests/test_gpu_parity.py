@@ -48,9 +48,7 @@ def configs(rt, B):
         "dyn_block_tc_c5_ch3": rt.Config.make(block_kernel=1, dynamic_sched=1,
                                               s1_ctas=5, chunk_kb=3, kbs=2),
         "dyn_fused_tc": rt.Config.make(dynamic_sched=1, down_ctas=148, s1_ctas=148),
-        "dyn_block_tpp2": rt.Config.make(block_kernel=1, dynamic_sched=1, tiles_per_piece=2),
-        "dyn_fused_tpp2_ch5": rt.Config.make(dynamic_sched=1, tiles_per_piece=2, chunk_kb=5,
-                                             s1_ctas=9, down_ctas=13),
+        "dyn_fused_ch5": rt.Config.make(dynamic_sched=1, chunk_kb=5, s1_ctas=9, down_ctas=13),
         "fused_sk2": rt.Config.make(s1_split_k=2),
         "fused_sk4_c8": rt.Config.make(s1_split_k=4, s1_ctas=8, kbs=1),
         "block_sk2": rt.Config.make(block_kernel=1, s1_split_k=2),
