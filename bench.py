@@ -76,7 +76,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -260,6 +260,10 @@ def main():
             call(B, k * len(sweep) + j, cfgs[B])
 
     ev0, ev1 = rt.Event(), rt.Event()
+    # Clocks are sampled from the warm-up through the per-batch timings (all
+    # under kernel load): the headline region alone is shorter than the
+    # sampling period at small --steps.
+    clk = ClockSampler(local_rank).__enter__()
     for k in range(args.warmup):
         step(k)
     ctx.sync()
@@ -268,12 +272,11 @@ def main():
     launches0 = ctx.launch_count()
     barrier()
     ctx.sync()
-    with ClockSampler(local_rank) as clk:
-        ev0.record(ctx)
-        for k in range(args.steps):
-            step(k)
-        ev1.record(ctx)
-        ctx.sync()
+    ev0.record(ctx)
+    for k in range(args.steps):
+        step(k)
+    ev1.record(ctx)
+    ctx.sync()
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_ms(ev1))
     launches = ctx.launch_count() - launches0
@@ -314,6 +317,7 @@ def main():
             ctx.stage1(sets[i % len(sets)], xs[B], a2s[B], cfg=s1cfg)
 
     s1_us = {B: time_calls(B, cfgs[B], n_rep, dom_call) for B in sweep}
+    clk.__exit__(None, None, None)
     s1_bytes = {B: (block_bytes(B, DM, DF, P) if dom_block[B] else
                     2 * (B * DM + 2 * DM * (f1 - f0) + B * (f1 - f0))) for B in sweep}
     s1_achieved = sum(s1_bytes.values()) / (sum(s1_us.values()) * 1e-6) / 1e9
@@ -323,8 +327,10 @@ def main():
                 "per batch: block kernel where chosen, else fused stage-1 kernel")
     peak, peak_src = measured_peak()
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "stage1_traffic.json")
-    if os.path.exists(tp):
+    # DRAM bytes per launch of the dominant kernel from the committed ncu
+    # --set full capture (tools/ncu_summary.py traffic), averaged over the sweep.
+    tp = os.path.join(ROOT, "profiles", "block_traffic.json")
+    if os.path.exists(tp) and all(dom_block.values()) and P == 1:
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch_sweep_mean")
         except Exception:
