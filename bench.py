@@ -180,6 +180,53 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# --- config 3: Qwen2.5-7B multi-layer decode loop -----------------------------
+QWEN7_DM, QWEN7_DF = 3584, 18944
+
+
+def decode_loop(rt, ctx, ev0, ev1, layers=4, steps=8, sweep=(1, 2, 4, 8, 16, 32)):
+    """BASELINE configs[2]: Qwen2.5-7B MLP, `layers` distinct layers (4 x 407 MB
+    >> L2), `steps` decode steps with x <- Y (bf16) after every block
+    (time_decode_seconds, bench.cpp:98-115), the whole sequence captured once
+    into a CUDA graph (dfk_decode) and replayed; tokens/s = B * steps / s."""
+    dm, df = QWEN7_DM, QWEN7_DF
+    scale = 1.0 / np.sqrt(dm)
+    ws = []
+    for l in range(layers):
+        g = ctx.array((dm, df)).fill_uniform(5000 + 3 * l, -scale, scale)
+        u = ctx.array((dm, df)).fill_uniform(5001 + 3 * l, -scale, scale)
+        d = ctx.array((df, dm)).fill_uniform(5002 + 3 * l, -scale, scale)
+        ws.append(ctx.weights(g, u, d))
+        del g, u, d
+    out = {"model": "Qwen2.5-7B MLP (d_model=3584, d_ff=18944)", "layers": layers,
+           "steps": steps, "graph": True, "per_batch": {}}
+    for B in sweep:
+        x = ctx.array((B, dm)).fill_uniform(77 + B)
+        y = ctx.array((B, dm))
+        res = {}
+        for graph in (True, False):
+            for _ in range(2):
+                ctx.decode(ws, x, steps, y, graph=graph)
+            ctx.sync()
+            reps = 5
+            ev0.record(ctx)
+            for _ in range(reps):
+                ctx.decode(ws, x, steps, y, graph=graph)
+            ev1.record(ctx)
+            ctx.sync()
+            res[graph] = ev0.elapsed_ms(ev1) * 1e-3 / reps
+        t = res[True]
+        blocks = layers * steps
+        out["per_batch"][str(B)] = {
+            "tokens_per_s": round(B * steps / t, 1),
+            "us_per_block": round(t / blocks * 1e6, 2),
+            "gbs": round(block_bytes(B, dm, df) * blocks / t / 1e9, 1),
+            "eager_us_per_block": round(res[False] / blocks * 1e6, 2),
+        }
+    del ws
+    return out
+
+
 # --- GPU arm -----------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -190,6 +237,7 @@ def main():
     ap.add_argument("--sets", type=int, default=4, help="rotating weight sets")
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--sweep", default=",".join(map(str, SWEEP)))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -366,6 +414,11 @@ def main():
     e2e_ms = max_over_ranks(max(ev0.elapsed_ms(ev1), wall * 1e3))
     e2e = bytes_step * e2e_steps / (e2e_ms * 1e-3) / 1e9
 
+    # ---- config 3: multi-layer decode loop (bench.cpp:98-115), CUDA graph ----
+    decode = None
+    if P == 1 and not args.no_decode:
+        decode = decode_loop(rt, ctx, ev0, ev1)
+
     # ---- CPU baseline: reference path, rank 0, N=1 only ----
     cpu = None
     if rank == 0 and P == 1 and not args.no_cpu:
@@ -409,6 +462,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "decode_loop": decode,
         }
         print(json.dumps(line), flush=True)
     barrier()

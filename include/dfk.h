@@ -181,6 +181,19 @@ DFK_API int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
                                    const void* x_pinned_bf16, int64_t batch,
                                    float* y_pinned, const dfk_config* cfg);
 
+/* Decode loop (time_decode_seconds, bench.cpp:98-115): `steps` passes over
+ * the `n_layers` blocks `layers` (same d_model), x <- Y after every block as
+ * a bf16 chain; the last block's Y lands in y_out (bf16 [B x d_model],
+ * device).  Under TP every block is a dfk_tp_forward.  use_graph != 0
+ * captures the whole sequence into a CUDA graph on first use (after one
+ * eager pass that sizes every scratch buffer) and replays it on later calls
+ * with the same (layers, batch, steps, x, y_out, resolved config).
+ * Asynchronous on the context stream. */
+DFK_API int dfk_decode(dfk_context ctx, const dfk_weights* layers,
+                       int32_t n_layers, const void* x, int64_t batch,
+                       int32_t steps, void* y_out, const dfk_config* cfg,
+                       int32_t use_graph);
+
 /* --- scheduler (tuner.cpp semantics) ----------------------------------- */
 /* Candidate grid for (weights, B): fills up to `cap` configs, returns the
  * count in *n (default_candidates, tuner.cpp:59-88). */

@@ -763,9 +763,12 @@ int dfk_context_destroy(dfk_context ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc, &ctx->flags, &ctx->sched,
                        &ctx->counters, &ctx->concat, &ctx->tmp1, &ctx->tmp2,
-                       &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev}) {
+                       &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev,
+                       &ctx->dec[0], &ctx->dec[1], &ctx->dec_f32}) {
     if (b->p) cudaFree(b->p);
   }
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+  ctx->graphs.clear();
   for (dfk_weights_s* w : ctx->weights) free_weights(w);
   ctx->weights.clear();
   if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);

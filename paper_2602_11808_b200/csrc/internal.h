@@ -47,6 +47,12 @@ struct DeviceBuf {
   size_t bytes = 0;
 };
 
+// A captured decode sequence (decode.cpp) and its kernel launch count.
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
 }  // namespace dfk
 
 struct dfk_context_s {
@@ -93,6 +99,12 @@ struct dfk_context_s {
   // NCCL tensor parallelism.
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+
+  // Decode loop (decode.cpp): bf16 ping-pong activations, fp32 TP partial,
+  // captured sequences keyed by (layers, batch, steps, buffers, config).
+  dfk::DeviceBuf dec[2];
+  dfk::DeviceBuf dec_f32;
+  std::map<std::string, dfk::GraphEntry> graphs;
 
   // Weight handles registered on this context (freed with it).
   std::set<dfk_weights_s*> weights;

@@ -143,6 +143,8 @@ _sigs = {
     "dfk_tp_group_start": ([], C.c_int),
     "dfk_tp_group_end": ([], C.c_int),
     "dfk_tp_forward": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
+    "dfk_decode": ([_vp, C.POINTER(_vp), C.c_int32, _vp, _i64, C.c_int32, _vp,
+                    C.POINTER(Config), C.c_int32], C.c_int),
     "dfk_balanced_range": ([_i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)],
                            C.c_int),
     "dfk_block_bytes": ([_i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)], C.c_int),
@@ -477,6 +479,16 @@ class Context:
     def tp_init(self, uid: bytes, rank: int, nranks: int):
         buf = C.create_string_buffer(uid, 128)
         _check(lib.dfk_tp_init(self.h, buf, rank, nranks))
+
+    def decode(self, layers, x: DeviceArray, steps: int, y: DeviceArray,
+               cfg: Optional[Config] = None, graph: bool = True):
+        """`steps` passes over `layers`, x <- Y (bf16) after every block
+        (time_decode_seconds, bench.cpp:98-115); the last Y lands in y (bf16).
+        graph=True captures the sequence into a CUDA graph once and replays it."""
+        assert y.dtype == BF16 and x.dtype == BF16
+        arr = (_vp * len(layers))(*[w.h for w in layers])
+        _check(lib.dfk_decode(self.h, arr, len(layers), x.ptr, x.shape[0], steps, y.ptr,
+                              self._cfg(cfg), 1 if graph else 0))
 
     def tp_forward(self, w: Weights, x: DeviceArray, y: DeviceArray,
                    cfg: Optional[Config] = None):

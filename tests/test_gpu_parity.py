@@ -226,6 +226,55 @@ def test_bf16_output_and_layer_chain(rt, ctx, oracle_lib):
     assert rel_err(y_gpu, xr) <= 2 * TOL
 
 
+@pytest.mark.parametrize("B,L,steps", [(4, 3, 2), (1, 1, 3), (17, 2, 1), (2, 1, 1)])
+def test_decode_loop_eager_and_graph(rt, ctx, oracle_lib, B, L, steps):
+    """dfk_decode (time_decode_seconds, bench.cpp:98-115): `steps` passes over
+    L layers with x <- Y (bf16), eagerly and replayed from a captured CUDA
+    graph (twice: the replay must not see the previous replay's stage-1
+    flags), vs the oracle chain fed the same bf16-rounded activations."""
+    dm, df = 384, 1280
+    layers = [instance(oracle_lib, 300 + l, B, dm, df)[1:] for l in range(L)]
+    x0 = instance(oracle_lib, 299, B, dm, df)[0]
+    ws = [ctx.weights(wg, wu, wd) for (wu, wg, wd) in layers]
+    xr = x0
+    for _ in range(steps):
+        for (wu, wg, wd) in layers:
+            xr = oracle_lib.quantize_bf16(oracle_lib.forward(xr, wu, wg, wd)[1])[0]
+    xd = ctx.array((B, dm)).upload(x0)
+    for graph in (False, True, True, True):
+        y = ctx.array((B, dm))
+        ctx.decode(ws, xd, steps, y, graph=graph)
+        ctx.sync()
+        assert rel_err(y.download(), xr) <= 2 * TOL, (graph, rel_err(y.download(), xr))
+    for cfg in (rt.Config.make(), rt.Config.make(block_kernel=1),
+                rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)):
+        y = ctx.array((B, dm))
+        for _ in range(2):
+            ctx.decode(ws, xd, steps, y, cfg=cfg, graph=True)
+        ctx.sync()
+        assert rel_err(y.download(), xr) <= 2 * TOL, cfg.label
+
+
+def test_decode_graph_interleaved_with_eager_calls(rt, ctx, oracle_lib):
+    """Graph replays and eager block launches interleave on one context (the
+    block-kernel epoch protocol, decode.cpp header)."""
+    B, dm, df = 3, 256, 768
+    (wu, wg, wd) = instance(oracle_lib, 310, B, dm, df)[1:]
+    x0 = instance(oracle_lib, 311, B, dm, df)[0]
+    w = ctx.weights(wg, wu, wd)
+    y1 = oracle_lib.quantize_bf16(oracle_lib.forward(x0, wu, wg, wd)[1])[0]
+    y2 = oracle_lib.quantize_bf16(oracle_lib.forward(y1, wu, wg, wd)[1])[0]
+    xd = ctx.array((B, dm)).upload(x0)
+    yg = ctx.array((B, dm))
+    ye = ctx.array((B, dm), rt.F32)
+    for i in range(4):
+        ctx.decode([w], xd, 2, yg, graph=True)
+        ctx.forward(w, xd, ye)
+        ctx.sync()
+        assert rel_err(yg.download(), y2) <= 2 * TOL, i
+        assert rel_err(ye.download(), oracle_lib.forward(x0, wu, wg, wd)[1]) <= TOL, i
+
+
 def test_forward_host_matches_device_path(rt, ctx, oracle_lib):
     x, wu, wg, wd = instance(oracle_lib, 13, 6, 384, 1024)
     w = ctx.weights(wg, wu, wd)
