@@ -113,7 +113,11 @@ typedef struct dfk_config {
                            (tiles, then fixed-size down chunks) instead of
                            the static byte-balanced plan                    */
   int32_t chunk_kb;     /* K blocks per dynamic down chunk (0 = auto)      */
-  int32_t reserved[2];
+  int32_t s1_chunk_kb;  /* K blocks per dynamic stage-1 piece: stream-K
+                           over d_model with fp32 partial sums (0 = auto:
+                           split only when the shard has fewer stage-1
+                           tiles than CTAs)                                */
+  int32_t reserved[1];
   char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
 } dfk_config;
 

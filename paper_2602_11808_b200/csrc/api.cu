@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -77,6 +78,7 @@ std::string config_label(const dfk_config& c) {
   if (c.variant == DFK_VARIANT_FOUR_KERNEL) return "four_kernel_cublaslt";
   if (c.block_kernel) {
     if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
+    if (c.dynamic_sched && c.s1_chunk_kb) o << "s1k" << c.s1_chunk_kb << "_";
     if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
@@ -84,6 +86,7 @@ std::string config_label(const dfk_config& c) {
     return o.str();
   }
   if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
+  if (c.dynamic_sched && c.s1_chunk_kb) o << "s1k" << c.s1_chunk_kb << "_";
   if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
   o << "fused_s1" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
     << c.s1_stages << "_c" << c.s1_ctas << "_dn"
@@ -223,6 +226,11 @@ Launch launch_shape(int family) {
   return {tc, tc ? 256 : 8};
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
                  int grid, StreamArgs* a) {
   if (!cfg.dynamic_sched) return DFK_OK;
@@ -231,17 +239,46 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   a->sched = static_cast<int*>(ctx->sched.p);
   // 32-K-block (512 KiB) down chunks measured best on full-size weights; a
   // shard with few down tiles gets smaller chunks so that there are at least
-  // ~1.5 pieces per CTA (but never under 4 K blocks).
+  // ~1.5 pieces per CTA -- but never under max(4, N/4) K blocks: every piece
+  // ends in 128 x N fp32 red.adds, which at large N cost more than the
+  // extra balance buys (tools/tp_shard_sweep.py, profiles/r1b_tp_shards.md).
   int chunk = std::min(w->dn_kblocks, 32);
   const int64_t pieces = static_cast<int64_t>(w->dn_tiles) *
                          ((w->dn_kblocks + chunk - 1) / chunk);
   if (pieces * 2 < 3LL * grid) {
     const int per_tile =
         std::max(1, (3 * grid + 2 * w->dn_tiles - 1) / (2 * w->dn_tiles));
-    chunk = std::max(std::min(4, w->dn_kblocks),
+    chunk = std::max(std::min(std::max(4, a->n_pad / 4), w->dn_kblocks),
                      (w->dn_kblocks + per_tile - 1) / per_tile);
   }
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
+  // Stage-1 stream-K: a shard with fewer stage-1 tiles than CTAs splits
+  // every tile's K range so that ~1.5 x grid stage-1 pieces keep all SMs
+  // streaming (s1_chunk_kb > 0 forces a chunk; >= K blocks = whole tiles).
+  int s1c = w->s1_kblocks;
+  if (cfg.s1_chunk_kb > 0) {
+    s1c = std::min(cfg.s1_chunk_kb, w->s1_kblocks);
+  } else if (w->s1_tiles < grid) {
+    // About 1.3 stage-1 pieces per CTA (rounded to whole pieces per tile),
+    // each >= 256 KiB (16 K blocks; 512 KiB at N > 16, where the 128 x N
+    // partial-sum red.adds per piece cost more) -- the best of a chunk-size
+    // sweep over the TP shards of SURVEY §8e (profiles/r1b_tp_shards.md).
+    const int per_tile =
+        std::max(1, static_cast<int>(std::lround(1.3 * grid / w->s1_tiles)));
+    const int min_kb = a->n_pad > 16 ? 32 : 16;
+    s1c = std::max(std::min(min_kb, w->s1_kblocks),
+                   (w->s1_kblocks + per_tile - 1) / per_tile);
+  }
+  a->s1_chunk = s1c;
+  if (s1c < w->s1_kblocks) {
+    DFK_TRY(ensure_buf(ctx->s1acc,
+                       static_cast<size_t>(w->s1_tiles) * a->n_pad * kBlockRows * 4,
+                       true, ctx->stream));
+    DFK_TRY(ensure_buf(ctx->s1cnt, static_cast<size_t>(w->s1_tiles) * 4, true,
+                       ctx->stream));
+    a->s1acc = static_cast<float*>(ctx->s1acc.p);
+    a->s1cnt = static_cast<int*>(ctx->s1cnt.p);
+  }
   return DFK_OK;
 }
 
@@ -278,6 +315,9 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   const int sk = a->split_k > 1 ? a->split_k : 1;
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk);
   a->trace = ctx->trace;
+  // 12 K blocks (192 KiB) of L2 prefetch: the measured optimum (A/B sweep
+  // 0..60, profiles/r1b_tuning.md).
+  a->pf_kb = env_int("DFK_PF_KB", 12);
   const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, sk));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
@@ -325,11 +365,25 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     const int sk = a.split_k;
     // Clusters of sk CTAs; as many clusters as keep every cluster at the
     // same tile count, never more than can be co-resident.
-    int clusters = cfg.s1_ctas > 0 ? cfg.s1_ctas / sk
-                                   : balanced_grid(w->s1_tiles, ctx->sm_count / sk);
-    clusters = std::max(1, std::min({clusters, w->s1_tiles, cluster_cap(kModeStage1, a)}));
-    const int grid = clusters * sk;
-    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
+    int grid;
+    if (cfg.dynamic_sched && sk == 1) {
+      // Dynamic: whole tiles on the balanced grid, or -- a shard with fewer
+      // tiles than 7/8 of the SMs -- stream-K pieces over 7/8 of the SMs.
+      grid = cfg.s1_ctas > 0 ? cfg.s1_ctas
+             : w->s1_tiles < ctx->sm_count * 7 / 8
+                 ? ctx->sm_count * 7 / 8
+                 : balanced_grid(w->s1_tiles, ctx->sm_count);
+      grid = std::max(1, std::min(grid, ctx->sm_count));
+      DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
+      const int per_tile = (w->s1_kblocks + a.s1_chunk - 1) / a.s1_chunk;
+      grid = std::min(grid, w->s1_tiles * per_tile);
+    } else {
+      int clusters = cfg.s1_ctas > 0 ? cfg.s1_ctas / sk
+                                     : balanced_grid(w->s1_tiles, ctx->sm_count / sk);
+      clusters =
+          std::max(1, std::min({clusters, w->s1_tiles, cluster_cap(kModeStage1, a)}));
+      grid = clusters * sk;
+    }
     cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
                                   grid, cfg.pdl != 0, ctx->stream);
     if (e != cudaSuccess)
@@ -764,7 +818,8 @@ int dfk_context_destroy(dfk_context ctx) {
   for (DeviceBuf* b : {&ctx->a2, &ctx->xpad, &ctx->a2pad, &ctx->yacc, &ctx->flags, &ctx->sched,
                        &ctx->counters, &ctx->concat, &ctx->tmp1, &ctx->tmp2,
                        &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev,
-                       &ctx->dec[0], &ctx->dec[1], &ctx->dec_f32}) {
+                       &ctx->dec[0], &ctx->dec[1], &ctx->dec_f32, &ctx->s1acc,
+                       &ctx->s1cnt}) {
     if (b->p) cudaFree(b->p);
   }
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);

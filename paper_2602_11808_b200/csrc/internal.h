@@ -75,6 +75,8 @@ struct dfk_context_s {
   dfk::DeviceBuf counters; // per-tile down arrival counters (kept zero)
   dfk::DeviceBuf flags;    // per-stage-1-tile completion flags (block kernel)
   dfk::DeviceBuf sched;    // dynamic-scheduler counters (kept zero between launches)
+  dfk::DeviceBuf s1acc;    // stage-1 stream-K fp32 partial sums (kept all-zero)
+  dfk::DeviceBuf s1cnt;    // stage-1 stream-K per-tile arrival counters (kept zero)
   unsigned epoch = 0;      // block-kernel launch epoch (flag value)
   unsigned long long* trace = nullptr;  // dfk_set_trace buffer
   int64_t trace_slots = 0;

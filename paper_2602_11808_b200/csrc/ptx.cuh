@@ -148,6 +148,12 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // ----------------------------------------------------------------------------
 // Programmatic dependent launch.
 // ----------------------------------------------------------------------------
+// Bulk prefetch of global memory into L2 (no shared memory, no barrier).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }

@@ -123,8 +123,23 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx,
         std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
         add(c);
       }
-  // Fewer stage-1 tiles than SMs (tensor-parallel shards): split each tile's
-  // K over a cluster (DSMEM reduction), static plan.
+  // Fewer stage-1 tiles than SMs (tensor-parallel shards): stream-K over
+  // d_model on the dynamic block kernel (fp32 partial sums in L2) at a few
+  // stage-1 / down chunk sizes ...
+  if (w->s1_tiles < ctx->sm_count) {
+    const int kb = w->s1_kblocks;
+    for (int s1k : {0, (kb + 1) / 2, (kb + 2) / 3, std::max(8, (kb + 3) / 4), 1 << 20})
+      for (int ck : {0, 16}) {
+        dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 1, 1);
+        c.dynamic_sched = 1;
+        c.s1_chunk_kb = s1k;
+        c.chunk_kb = ck;
+        std::snprintf(c.label, sizeof(c.label), "%s", "");
+        std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+        add(c);
+      }
+  }
+  // ... and split each tile's K over a cluster (DSMEM reduction), static plan.
   if (w->s1_tiles < ctx->sm_count && B <= 64) {
     for (int sk : {2, 4}) {
       if (w->s1_kblocks % sk) continue;
@@ -148,7 +163,7 @@ json cfg_to_json(const dfk_config& c) {
               {"s1_split_k", c.s1_split_k},   {"down_family", c.down_family},
               {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
               {"pdl", c.pdl},                 {"dynamic_sched", c.dynamic_sched},
-              {"chunk_kb", c.chunk_kb},
+              {"chunk_kb", c.chunk_kb},       {"s1_chunk_kb", c.s1_chunk_kb},
               {"label", std::string(c.label)}};
 }
 
@@ -180,6 +195,7 @@ dfk_config cfg_from_json(const json& j) {
   c.kbs = get_field<int>(j, "kbs");
   c.dynamic_sched = get_field<int>(j, "dynamic_sched");
   c.chunk_kb = get_field<int>(j, "chunk_kb");
+  c.s1_chunk_kb = j.contains("s1_chunk_kb") ? j["s1_chunk_kb"].get<int>() : 0;
   std::snprintf(c.label, sizeof(c.label), "%s",
                 get_field<std::string>(j, "label").c_str());
   return c;

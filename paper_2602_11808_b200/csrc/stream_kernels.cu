@@ -189,16 +189,28 @@ __device__ __forceinline__ int dyn_chunks(const StreamArgs& a) {
   return (a.kb2 + a.chunk_kb - 1) / a.chunk_kb;
 }
 
+// Stage-1 pieces per tile (stream-K over d_model when s1_chunk < kb1).
+__device__ __forceinline__ int s1_pieces(const StreamArgs& a) {
+  return a.s1_chunk > 0 && a.s1_chunk < a.kb1 ? (a.kb1 + a.s1_chunk - 1) / a.s1_chunk
+                                               : 1;
+}
+
+// Piece index -> piece.  Stage-1 pieces first, tile-major (every K chunk of
+// tile 0, then tile 1, ...), so tiles complete in order; then the down
+// pieces, chunk-major (all t2 tiles of K chunk 0, then chunk 1, ...), so the
+// earliest-published A2 is consumed first.
 __device__ __forceinline__ bool decode_dyn(const StreamArgs& a, int mode,
                                            int64_t idx, Piece& out) {
-  const int64_t n1 = mode != kModeDown ? a.t1 : 0;
+  const int s1c = s1_pieces(a);
+  const int64_t n1 = mode != kModeDown ? static_cast<int64_t>(a.t1) * s1c : 0;
   const int64_t n2 =
       mode != kModeStage1 ? static_cast<int64_t>(a.t2) * dyn_chunks(a) : 0;
   if (idx < n1) {
     out.down = 0;
-    out.tile = static_cast<int>(idx);
-    out.kb0 = 0;
-    out.kb1 = a.kb1;
+    out.tile = static_cast<int>(idx / s1c);
+    const int kc = static_cast<int>(idx % s1c);
+    out.kb0 = s1c > 1 ? kc * a.s1_chunk : 0;
+    out.kb1 = s1c > 1 ? min(a.kb1, out.kb0 + a.s1_chunk) : a.kb1;
     return true;
   }
   idx -= n1;
@@ -386,6 +398,71 @@ __device__ __forceinline__ void s1_publish(const StreamArgs& a, int tile,
   if (tid == 0) st_release(a.flags + tile, a.epoch);
 }
 
+// Stage-1 stream-K: add this CTA's partial gate/up sums of tile t (one
+// value per (row, n)) to the fp32 workspace.  mutant == 1 (the reference's
+// SiluPerKChunk negative control, verification.cpp:84-124) instead adds
+// SiLU(gate_part) * up_part into the gate slot: must fail parity.
+__device__ __forceinline__ float* s1acc_at(const StreamArgs& a, int t, int n) {
+  return a.s1acc + (static_cast<int64_t>(t) * a.n_pad + n) * kBlockRows;
+}
+
+// Tail of a partial stage-1 piece: the CTA adding the tile's last piece
+// turns the full sums into A2, re-zeroes the workspace and publishes.
+__device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
+                                               int tid, int nthr,
+                                               int* smem_flag) {
+  __threadfence();
+  named_bar(1, nthr);
+  if (tid == 0) {
+    const int old = atomicAdd(&a.s1cnt[t], 1);
+    *smem_flag = (old == s1_pieces(a) - 1) ? 1 : 0;
+  }
+  named_bar(1, nthr);
+  if (*smem_flag) {
+    __threadfence();
+    // Work item (n, c4): A2 columns 4*c4 .. 4*c4+3 of batch row n; its gate
+    // sums are 4 consecutive workspace rows, the up sums the 4 rows 16 below.
+    // Loads are issued 4 items deep before any store (L2 round trips).
+    const int total = a.B * (kS1Cols / 4);
+    for (int base = tid; base < total; base += 4 * nthr) {
+      float4 g[4], u[4];
+      float* ptr[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int idx = base + k * nthr;
+        ptr[k] = nullptr;
+        if (idx < total) {
+          const int n = idx >> 4, c4 = idx & 15;
+          ptr[k] = s1acc_at(a, t, n) + 32 * (c4 >> 2) + 4 * (c4 & 3);
+          g[k] = __ldcg(reinterpret_cast<const float4*>(ptr[k]));
+          u[k] = __ldcg(reinterpret_cast<const float4*>(ptr[k] + 16));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int idx = base + k * nthr;
+        if (idx < total) {
+          const int n = idx >> 4, c4 = idx & 15;
+          const float gv[4] = {g[k].x, g[k].y, g[k].z, g[k].w};
+          const float uv[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int col = t * kS1Cols + 4 * c4 + e;
+            if (col < a.cols_valid)
+              a.a2[n * a.a2_ld + col] =
+                  __float2bfloat16_rn(a.mutant == 1 ? gv[e] : silu_f(gv[e]) * uv[e]);
+          }
+          __stcg(reinterpret_cast<float4*>(ptr[k]), make_float4(0.f, 0.f, 0.f, 0.f));
+          __stcg(reinterpret_cast<float4*>(ptr[k] + 16), make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
+    }
+    if (tid == 0) a.s1cnt[t] = 0;
+    if (a.flags) s1_publish(a, t, tid, nthr);
+  }
+  named_bar(1, nthr);
+}
+
 // ---------------------------------------------------------------------------
 // Producer (all of warp 0; lane 0 issues the copies).  In kModeBlock the
 // warp checks the stage-1 completion flags a down piece depends on
@@ -409,6 +486,23 @@ __device__ __forceinline__ void ensure_ready(const StreamArgs& a,
   rc.hi = hi;
 }
 
+// Non-blocking form of ensure_ready (whole warp): true, and the range
+// cached, when every flag in [lo, hi) is published.
+__device__ __forceinline__ bool check_ready(const StreamArgs& a, ReadyCache& rc,
+                                            int lo, int hi) {
+  if (!a.flags || (lo >= rc.lo && hi <= rc.hi)) return true;
+  bool ok = true;
+  for (int j = lo + static_cast<int>(lane_id()); j < hi; j += 32)
+    ok = ok && ld_acquire(a.flags + j) == a.epoch;
+  ok = __all_sync(0xffffffffu, ok);
+  if (ok) {
+    fence_proxy_async_global();
+    rc.lo = lo;
+    rc.hi = hi;
+  }
+  return ok;
+}
+
 __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                                         const CUtensorMap* xmap,
                                         const CUtensorMap* amap, uint8_t* smem,
@@ -418,10 +512,15 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
   const uint64_t policy = policy_evict_first();
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
   const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
+  // Stages whose weight copies are issued but whose activation loads wait:
+  // before griddepcontrol.wait (PDL), or -- down pieces -- until the stage-1
+  // tiles they read have published.  Weight streaming never waits for
+  // either: it runs ahead until the ring wraps onto a deferred stage.
   struct Pend {
-    int kb, nb, down, pk0, pk1;
+    int slot, kb, nb, down, pk0, pk1;
+    int64_t it;
   };
-  Pend pend[32];
+  Pend pend[32];  // stages <= 32, never more than a ring's worth deferred
   int npend = 0;
   ReadyCache rc;
   int64_t it = 0;
@@ -433,16 +532,34 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       tma_load_2d(xs + b * xblk, down ? amap : xmap, (kb + b) * kBlockK, 0, bar);
     }
   };
-  // griddepcontrol.wait, then the activation loads deferred so far.
-  auto release_deferred = [&]() {
-    if (waited) return;
-    pdl_wait();
-    waited = true;
+  Piece first{};
+  int first_issued = 0;  // K blocks of the first piece already in the ring
+  // Issue every deferred activation load: griddepcontrol.wait first (before
+  // it, the next pf_kb K blocks of the first piece go to L2), then block on
+  // the readiness of each deferred down stage.
+  auto flush = [&]() {
+    if (!waited) {
+      if (leader && a.pf_kb > 0 && first.kb1 > first.kb0) {
+        const uint8_t* wb = first.down ? a.w2 : a.w1;
+        const int kbt = first.down ? a.kb2 : a.kb1;
+        const int k0 = first.kb0 + first_issued;
+        const int k1 = min(first.kb1, k0 + a.pf_kb);
+        for (int kb = k0; kb < k1; kb += 4) {
+          const int nb = min(4, k1 - kb);
+          bulk_prefetch_l2(wb + (static_cast<int64_t>(first.tile) * kbt + kb) *
+                                    static_cast<int64_t>(kBlockBytes),
+                           static_cast<uint32_t>(nb) * kBlockBytes);
+        }
+      }
+      pdl_wait();
+      waited = true;
+    }
     for (int j = 0; j < npend; ++j) {
       if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
-      act_loads(smem + static_cast<int64_t>(j) * stage_bytes + wbytes_all,
-                pend[j].kb, pend[j].nb, pend[j].down, &full[j]);
+      act_loads(smem + static_cast<int64_t>(pend[j].slot) * stage_bytes + wbytes_all,
+                pend[j].kb, pend[j].nb, pend[j].down, &full[pend[j].slot]);
     }
+    npend = 0;
   };
   for (int qi = 0;; ++qi) {
     Piece pc;
@@ -452,7 +569,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     } else {
       int64_t idx = blockIdx.x;
       if (qi > 0) {
-        release_deferred();  // no global atomics before the previous grid ends
+        if (!waited) flush();  // no global atomics before the previous grid ends
         int got = 0;
         if (leader) got = atomicAdd(a.sched, 1);
         idx = static_cast<int64_t>(gridDim.x) + __shfl_sync(0xffffffffu, got, 0);
@@ -471,6 +588,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       }
     }
     if (!valid) break;
+    if (qi == 0) first = pc;
     if (leader) trace_stamp(a, 3 + 2 * qi);
     const uint8_t* wbase = pc.down ? a.w2 : a.w1;
     const int kbt = pc.down ? a.kb2 : a.kb1;
@@ -479,6 +597,9 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       const int slot = static_cast<int>(it % a.stages);
       const uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
       if (it >= a.stages) {
+        // The slot about to be reused holds a deferred stage: its consumer
+        // cannot finish before we issue its activations.
+        if (npend > 0 && pend[0].it <= it - a.stages) flush();
         if (leader) mbar_wait(&empty[slot], phase ^ 1u);
         __syncwarp();
       }
@@ -492,17 +613,19 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                              static_cast<int64_t>(kBlockBytes),
                  static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
       }
-      if (!waited) {
-        pend[npend++] = {kb, nb, pc.down, pc.kb0, pc.kb1};
-        if (it + 1 >= a.stages) release_deferred();  // ring full of weights
+      // Activation loads stay in stage order: defer while anything is
+      // deferred, before the PDL wait, or while this down piece's A2 is not
+      // yet published (non-blocking check).
+      if (!waited || npend > 0 || (pc.down && !check_ready(a, rc, pc.kb0, pc.kb1))) {
+        if (qi == 0 && !waited) first_issued += nb;
+        pend[npend++] = {slot, kb, nb, pc.down, pc.kb0, pc.kb1, it};
         continue;
       }
-      if (pc.down) ensure_ready(a, rc, pc.kb0, pc.kb1);
       act_loads(st + wbytes_all, kb, nb, pc.down, &full[slot]);
     }
   }
   if (leader) trace_stamp(a, 1);
-  release_deferred();  // fewer stages of work than ring slots
+  flush();  // fewer stages of work than ring slots / deferred tail
 }
 
 // ---------------------------------------------------------------------------
@@ -589,7 +712,23 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
         acc[r][n] = v;
       }
 
-    if (!pc.down) {
+    if (!pc.down && (pc.kb0 > 0 || pc.kb1 < a.kb1)) {
+      // stream-K piece: partial sums to the workspace
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = gemv_row(r, mw, q);
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          float v = acc[r][n];
+          if (a.mutant == 1) {
+            const float up = __shfl_xor_sync(0xffffffffu, v, 16);
+            v = q < 2 ? silu_f(v) * up : 0.f;
+          }
+          if (c == 0 && n < a.B) atomicAdd(s1acc_at(a, pc.tile, n) + row, v);
+        }
+      }
+      s1_finish_tile(a, pc.tile, tid, nthr, smem_flag);
+    } else if (!pc.down) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int col = pc.tile * kS1Cols + r * 16 + 2 * mw + q;
@@ -800,7 +939,30 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       ++acc_it;
       continue;
     }
-    if (!pc.down) {
+    if (!pc.down && (pc.kb0 > 0 || pc.kb1 < a.kb1)) {
+      // stream-K piece: partial gate/up sums to the workspace
+      float* base = s1acc_at(a, pc.tile, 0) + row;
+      for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float val = v[e];
+          if (a.mutant == 1) {
+            const float up = __shfl_xor_sync(0xffffffffu, val, 16);
+            int is_up, cofs;
+            s1_row_map(row, &is_up, &cofs);
+            val = is_up ? 0.f : silu_f(val) * up;
+          }
+          const int n = c0 + e;
+          if (n < a.B) atomicAdd(base + static_cast<int64_t>(n) * kBlockRows, val);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      s1_finish_tile(a, pc.tile, tid, 128, smem_flag);
+    } else if (!pc.down) {
       int is_up, cofs;
       s1_row_map(row, &is_up, &cofs);
       const int col = pc.tile * kS1Cols + cofs;

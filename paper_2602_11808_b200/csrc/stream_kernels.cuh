@@ -74,6 +74,20 @@ struct StreamArgs {
   int dynamic;
   int chunk_kb;
   int* sched;
+  // Stage-1 stream-K (dynamic path): a stage-1 piece covers s1_chunk K
+  // blocks of one tile (s1_chunk >= kb1 or 0: whole tiles).  Partial
+  // gate/up accumulators go to the fp32 workspace s1acc [t1][n_pad][128]
+  // with red.global.add; the CTA adding a tile's last piece (s1cnt arrival
+  // counter) applies SiLU*up to the FULL sums, writes A2, publishes the
+  // tile's flag and re-zeroes its workspace and counter.  Lets every SM
+  // stream stage-1 weights when a (TP) shard has fewer tiles than SMs.
+  int s1_chunk;
+  float* s1acc;
+  int* s1cnt;
+  // K blocks of the first piece prefetched into L2 (cp.async.bulk.prefetch)
+  // beyond the smem ring BEFORE griddepcontrol.wait: under PDL the HBM
+  // stream of this launch starts during the previous launch's tail.
+  int pf_kb;
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.

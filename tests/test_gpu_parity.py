@@ -49,6 +49,10 @@ def configs(rt, B):
                                               s1_ctas=5, chunk_kb=3, kbs=2),
         "dyn_fused_tc": rt.Config.make(dynamic_sched=1, down_ctas=148, s1_ctas=148),
         "dyn_fused_ch5": rt.Config.make(dynamic_sched=1, chunk_kb=5, s1_ctas=9, down_ctas=13),
+        "dyn_block_s1k3": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_chunk_kb=3),
+        "dyn_fused_s1k2_c7": rt.Config.make(dynamic_sched=1, s1_chunk_kb=2, s1_ctas=7),
+        "dyn_block_wholetiles": rt.Config.make(block_kernel=1, dynamic_sched=1,
+                                               s1_chunk_kb=1 << 20),
         "fused_sk2": rt.Config.make(s1_split_k=2),
         "fused_sk4_c8": rt.Config.make(s1_split_k=4, s1_ctas=8, kbs=1),
         "block_sk2": rt.Config.make(block_kernel=1, s1_split_k=2),
@@ -66,6 +70,10 @@ def configs(rt, B):
         out["dyn_block_gemv"] = rt.Config.make(block_kernel=1, dynamic_sched=1,
                                                s1_family=rt.FAMILY_GEMV,
                                                down_family=rt.FAMILY_GEMV)
+        out["dyn_block_gemv_s1k2"] = rt.Config.make(block_kernel=1, dynamic_sched=1,
+                                                    s1_chunk_kb=2,
+                                                    s1_family=rt.FAMILY_GEMV,
+                                                    down_family=rt.FAMILY_GEMV)
     return out
 
 
@@ -434,3 +442,30 @@ def test_split_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, split):
         assert rel_err(a2.download(), a2_ref) <= TOL
         ctx.stage1(w, xd, a2, cfg=bad)
         assert rel_err(a2.download(), a2_ref) > 5 * TOL
+
+
+@pytest.mark.parametrize("fam", ["tc", "gemv"])
+def test_stage1_stream_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, fam):
+    """Stage-1 stream-K (fp32 partial gate/up sums in a workspace, SiLU*up by
+    the CTA adding the tile's last piece): correct, and its SiluPerKChunk
+    mutant (verification.cpp:84-124) must FAIL parity."""
+    B, dm, df = 4, 1024, 1024
+    x, wu, wg, wd = instance(oracle_lib, 90, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    xd = ctx.array((B, dm)).upload(x)
+    f = rt.FAMILY_TC if fam == "tc" else rt.FAMILY_GEMV
+    for block in (0, 1):
+        kw = dict(block_kernel=block, dynamic_sched=1, s1_chunk_kb=5, s1_family=f,
+                  down_family=f)
+        a2 = ctx.array((B, df))
+        ctx.stage1(w, xd, a2, cfg=rt.Config.make(**kw))
+        assert rel_err(a2.download(), a2_ref) <= TOL
+        ctx.stage1(w, xd, a2, cfg=rt.Config.make(mutant=1, **kw))
+        assert rel_err(a2.download(), a2_ref) > 10 * TOL
+        y = ctx.array((B, dm), rt.F32)
+        ctx.forward(w, xd, y, cfg=rt.Config.make(**kw))
+        assert rel_err(y.download(), y_ref) <= TOL
+        # the workspace is left all-zero: a second correct call still passes
+        ctx.stage1(w, xd, a2, cfg=rt.Config.make(**kw))
+        assert rel_err(a2.download(), a2_ref) <= TOL
