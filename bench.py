@@ -262,8 +262,15 @@ def main():
 
     P = world
     ctx = rt.Context(local_rank)
+    tp_mode = None
     if P > 1:
+        # NCCL (the unfused-collective comparator) and the fused all-reduce's
+        # symmetric workspaces over NVLink peer memory (used when every rank
+        # can map its peers).
         ctx.tp_init(tp_host.exchange_uid(dist, rank), rank, P)
+        sweep_max = max(int(b) for b in args.sweep.split(","))
+        tp_mode = ("fused-nvlink" if tp_host.setup_fused(dist, ctx, rank, P, sweep_max, DM)
+                   else "nccl")
     f0, f1 = tp_host.shard_range(DF, P, rank)
 
     def barrier():
@@ -298,10 +305,15 @@ def main():
 
     def call(B, i, cfg=None):
         w = sets[i % len(sets)]
-        if P > 1:
+        if tp_mode == "fused-nvlink":
+            ctx.tp_forward_fused(w, xs[B], ys[B], cfg=cfg)
+        elif P > 1:
             ctx.tp_forward(w, xs[B], ys[B], cfg=cfg)
         else:
             ctx.forward(w, xs[B], ys[B], cfg=cfg)
+
+    def nccl_call(B, i, cfg=None):
+        ctx.tp_forward(sets[i % len(sets)], xs[B], ys[B], cfg=cfg)
 
     def step(k):
         for j, B in enumerate(sweep):
@@ -349,6 +361,9 @@ def main():
     us = {B: time_calls(B, cfgs[B], n_rep) for B in sweep}
     two = rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)
     us_unfused = {B: time_calls(B, two, n_rep) for B in sweep}
+    # TP: the same block with NCCL's all-reduce as a separate collective.
+    us_nccl = ({B: time_calls(B, cfgs[B], n_rep, nccl_call) for B in sweep}
+               if tp_mode == "fused-nvlink" else None)
 
     # ---- roofline: the dominant kernel alone ----
     # Block kernel chosen -> the whole block is one launch; otherwise the fused
@@ -449,6 +464,9 @@ def main():
             "gbs_per_batch": {str(B): round(block_bytes(B, DM, DF, P) * P / (us[B] * 1e-6) / 1e9, 1)
                               for B in sweep},
             "unfused_us_per_call": {str(B): round(us_unfused[B], 2) for B in sweep},
+            "tp_allreduce": tp_mode,
+            "nccl_allreduce_us_per_call": ({str(B): round(us_nccl[B], 2) for B in sweep}
+                                           if us_nccl else None),
             "speedup_vs_unfused": {str(B): round(us_unfused[B] / us[B], 3) for B in sweep},
             "chosen": chosen,
             "roofline": {"bound": "hbm", "achieved": round(s1_achieved, 1), "peak": peak,

@@ -171,7 +171,9 @@ DFK_API int dfk_forward(dfk_context ctx, dfk_weights w, const void* x,
                         const dfk_config* cfg);
 /* Reference-facing call with HOST buffers (synchronous): converts X
  * (x_dtype F64/F32/BF16) to bf16, copies it in, runs dfk_forward (or
- * dfk_tp_forward when the context has a TP communicator), copies Y out and
+ * the TP block -- dfk_tp_forward_fused when the symmetric workspaces are
+ * set up, else dfk_tp_forward when the context has a TP communicator),
+ * copies Y out and
  * converts it to y_dtype. */
 DFK_API int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
                              int32_t x_dtype, int64_t batch, void* y,
@@ -188,7 +190,8 @@ DFK_API int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
 /* Decode loop (time_decode_seconds, bench.cpp:98-115): `steps` passes over
  * the `n_layers` blocks `layers` (same d_model), x <- Y after every block as
  * a bf16 chain; the last block's Y lands in y_out (bf16 [B x d_model],
- * device).  Under TP every block is a dfk_tp_forward.  use_graph != 0
+ * device).  Under TP every block is a dfk_tp_forward_fused (or, with only
+ * an NCCL communicator, a dfk_tp_forward).  use_graph != 0
  * captures the whole sequence into a CUDA graph on first use (after one
  * eager pass that sizes every scratch buffer) and replays it on later calls
  * with the same (layers, batch, steps, x, y_out, resolved config).
@@ -238,6 +241,36 @@ DFK_API int dfk_tp_group_end(void);
  * collective of the compound scheme, tp.cpp:140-167). */
 DFK_API int dfk_tp_forward(dfk_context ctx, dfk_weights w, const void* x,
                            int64_t batch, float* y, const dfk_config* cfg);
+/* --- fused TP all-reduce over NVLink peer memory ----------------------- */
+/* The block's one collective inside the block kernel:
+ * down tile t is owned by rank t % P; every rank red.adds its fp32 partial
+ * sums into the owner's workspace over NVLink, the CTA completing a tile
+ * writes the full-sum Y into every rank's workspace, and each rank's launch
+ * ends once all of its Y tiles are written.  Replaces dfk_tp_forward's
+ * separate ncclAllReduce (tp.cpp:140-167 / simulated_all_reduce :90-105).
+ *
+ * dfk_tp_sym_create: allocates this rank's symmetric workspace for
+ *   batch <= max_batch (<= 256) and d_model (% 4 == 0); writes its 64-byte
+ *   CUDA IPC handle to ipc_handle64 (may be NULL).
+ * dfk_tp_sym_open: multi-process -- handles = nranks x 64 bytes in rank
+ *   order (every rank's dfk_tp_sym_create output, exchanged by the caller).
+ * dfk_tp_sym_attach: one process driving n contexts (on n devices, or
+ *   several contexts on ONE device as an emulation of n ranks).
+ * dfk_tp_forward_fused: this rank's shard, Y (fp32 [B x d_model], device)
+ *   = the full sum over ranks.  Every rank must issue it with the same
+ *   batch; a rank waits at most 4 s for its peers, then the launch fails.
+ *   When ONE process drives several ranks, allocate every buffer before
+ *   issuing the ranks' calls (a cudaMalloc may wait for the device, i.e. for
+ *   a rank that waits for a peer not launched yet). */
+DFK_API int dfk_tp_sym_create(dfk_context ctx, int64_t max_batch,
+                              int64_t d_model, void* ipc_handle64);
+DFK_API int dfk_tp_sym_open(dfk_context ctx, const void* handles, int rank,
+                            int nranks);
+DFK_API int dfk_tp_sym_attach(dfk_context* ctxs, int n);
+DFK_API int dfk_tp_forward_fused(dfk_context ctx, dfk_weights w,
+                                 const void* x, int64_t batch, float* y,
+                                 const dfk_config* cfg);
+
 /* balanced_ranges(extent, parts)[index] (tp.cpp:8-29). */
 DFK_API int dfk_balanced_range(int64_t extent, int64_t parts, int64_t index,
                                int64_t* begin, int64_t* end);

@@ -476,7 +476,7 @@ void block_plan(int G, const dfk_weights_s* w, StreamArgs* a) {
 // the grid never exceeds the SM count.
 int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
                 __nv_bfloat16* a2, int64_t a2_ld, void* y, int64_t y_ld,
-                bool y_bf16, const dfk_config& cfg) {
+                bool y_bf16, const dfk_config& cfg, const StreamArgs* tp) {
   const Launch L = launch_shape(cfg.s1_family);
   const void* xp;
   int64_t x_ld;
@@ -497,6 +497,19 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
+    if (tp) {  // fused TP all-reduce (tp.cpp): peer workspaces and outputs
+      a.tp_rank = tp->tp_rank;
+      a.tp_size = tp->tp_size;
+      a.tp_total_kb = tp->tp_total_kb;
+      a.tp_error = tp->tp_error;
+      for (int r = 0; r < kMaxTp; ++r) {
+        a.tp_yacc[r] = tp->tp_yacc[r];
+        a.tp_cnt[r] = tp->tp_cnt[r];
+        a.tp_done[r] = tp->tp_done[r];
+        a.tp_y[r] = tp->tp_y[r];
+      }
+      a.yacc_ld = tp->yacc_ld;
+    }
     a.flags = static_cast<unsigned*>(ctx->flags.p);
     if (++ctx->epoch == 0) ++ctx->epoch;
     a.epoch = ctx->epoch;
@@ -739,7 +752,7 @@ int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   auto* a2 = static_cast<__nv_bfloat16*>(ctx->a2.p);
   if (cfg.variant == DFK_VARIANT_FUSED && cfg.block_kernel) {
     return block_fused(ctx, w, x, B, a2, a2_ld, y, w->d_model,
-                       y_dtype == DFK_BF16, cfg);
+                       y_dtype == DFK_BF16, cfg, nullptr);
   }
   if (cfg.variant == DFK_VARIANT_FUSED) {
     DFK_TRY(stage1_fused(ctx, w, x, B, a2, a2_ld, cfg));
@@ -749,6 +762,15 @@ int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   // Unfused comparators want a dense X (ld = d_model) and dense A2.
   DFK_TRY(stage1_unfused(ctx, w, x, B, a2, w->d_ff, cfg.variant));
   return down_unfused(ctx, w, a2, B, y, y_dtype == DFK_BF16);
+}
+
+int block_fused_tp(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
+                   void* y, const dfk_config& cfg, const StreamArgs* tp) {
+  const int64_t a2_ld = round_up(w->d_ff, 8);
+  DFK_TRY(ensure_buf(ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
+                     ctx->stream));
+  return block_fused(ctx, w, x, B, static_cast<__nv_bfloat16*>(ctx->a2.p), a2_ld, y,
+                     w->d_model, false, cfg, tp);
 }
 
 }  // namespace dfk
@@ -788,6 +810,14 @@ int dfk_context_create(int device, void* stream, dfk_context* out) {
                     prop.name + " sm_" + std::to_string(prop.major) +
                     std::to_string(prop.minor));
   }
+  // Load every kernel now (lazy loading would do it at first launch, where
+  // it can wait for the device; see preload_aux_kernels).
+  {
+    cudaError_t e = preload_stream_kernels();
+    if (e == cudaSuccess) e = preload_aux_kernels();
+    if (e != cudaSuccess)
+      return fail(DFK_ERR_CUDA, std::string("kernel preload: ") + cudaGetErrorString(e));
+  }
   auto* ctx = new dfk_context_s();
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
@@ -824,6 +854,9 @@ int dfk_context_destroy(dfk_context ctx) {
   }
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
   ctx->graphs.clear();
+  for (int r = 0; r < 8; ++r)
+    if (ctx->tp_peer_ipc[r] && ctx->tp_peer[r]) cudaIpcCloseMemHandle(ctx->tp_peer[r]);
+  if (ctx->tp_sym.p) cudaFree(ctx->tp_sym.p);
   for (dfk_weights_s* w : ctx->weights) free_weights(w);
   ctx->weights.clear();
   if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
@@ -1053,9 +1086,9 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
   DFK_TRY(ensure_buf(ctx->hy_dev, yb, false, ctx->stream));
   DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, hx, xb, cudaMemcpyHostToDevice,
                            ctx->stream));
-  if (ctx->comm) {
-    DFK_TRY(dfk_tp_forward(ctx, w, ctx->hx_dev.p, batch,
-                           static_cast<float*>(ctx->hy_dev.p), cfg));
+  if (tp_active(ctx)) {
+    DFK_TRY(tp_block(ctx, w, ctx->hx_dev.p, batch,
+                     static_cast<float*>(ctx->hy_dev.p), cfg));
   } else {
     DFK_TRY(forward_impl(ctx, w, ctx->hx_dev.p, batch, ctx->hy_dev.p, DFK_F32,
                          cfg));
@@ -1092,9 +1125,9 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
   DFK_TRY(ensure_buf(ctx->hy_dev, yb, false, ctx->stream));
   DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, x_pinned_bf16, xb,
                            cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->comm) {
-    DFK_TRY(dfk_tp_forward(ctx, w, ctx->hx_dev.p, batch,
-                           static_cast<float*>(ctx->hy_dev.p), cfg));
+  if (tp_active(ctx)) {
+    DFK_TRY(tp_block(ctx, w, ctx->hx_dev.p, batch,
+                     static_cast<float*>(ctx->hy_dev.p), cfg));
   } else {
     DFK_TRY(forward_impl(ctx, w, ctx->hx_dev.p, batch, ctx->hy_dev.p, DFK_F32,
                          cfg));

@@ -225,6 +225,34 @@ unsigned grid_for(int64_t total, int threads) {
 
 }  // namespace
 
+// Force-load every kernel of this translation unit (CUDA lazy loading would
+// otherwise load a module at its first launch, which can wait for the
+// device -- fatal between the launches of ranks that wait for each other).
+cudaError_t preload_aux_kernels() {
+  const void* fns[] = {
+      reinterpret_cast<const void*>(pack_stage1_kernel<double>),
+      reinterpret_cast<const void*>(pack_stage1_kernel<float>),
+      reinterpret_cast<const void*>(pack_stage1_kernel<__nv_bfloat16>),
+      reinterpret_cast<const void*>(pack_down_kernel<double>),
+      reinterpret_cast<const void*>(pack_down_kernel<float>),
+      reinterpret_cast<const void*>(pack_down_kernel<__nv_bfloat16>),
+      reinterpret_cast<const void*>(unpack_stage1_kernel),
+      reinterpret_cast<const void*>(unpack_down_kernel),
+      reinterpret_cast<const void*>(pad_rows_kernel),
+      reinterpret_cast<const void*>(silu_mul_kernel),
+      reinterpret_cast<const void*>(silu_kernel),
+      reinterpret_cast<const void*>(mul_kernel),
+      reinterpret_cast<const void*>(fill_uniform_kernel),
+      reinterpret_cast<const void*>(flush_kernel),
+      reinterpret_cast<const void*>(f32_to_bf16_kernel)};
+  for (const void* f : fns) {
+    cudaFuncAttributes at;
+    const cudaError_t e = cudaFuncGetAttributes(&at, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_pack_stage1(const void* w_gate, const void* w_up, int dtype,
                                int64_t d_model, int64_t d_ff_total,
                                int64_t ff_begin, int64_t d_ff, int tiles,

@@ -31,11 +31,11 @@ namespace {
 // all-reduced and rounded to bf16.
 int chain_block(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
                 int64_t B, void* y_bf16, const dfk_config* cfg) {
-  if (ctx->comm && ctx->nranks > 1) {
+  if (tp_active(ctx)) {
     const size_t n = static_cast<size_t>(B * w->d_model);
     DFK_TRY(ensure_buf(ctx->dec_f32, n * 4, false, ctx->stream));
     float* yf = static_cast<float*>(ctx->dec_f32.p);
-    DFK_TRY(dfk_tp_forward(ctx, w, x, B, yf, cfg));
+    DFK_TRY(tp_block(ctx, w, x, B, yf, cfg));
     cudaError_t e = launch_f32_to_bf16(yf, static_cast<__nv_bfloat16*>(y_bf16),
                                        static_cast<int64_t>(n), ctx->stream);
     if (e != cudaSuccess) return fail(DFK_ERR_CUDA, cudaGetErrorString(e));
@@ -50,6 +50,14 @@ int run_chain(dfk_context_s* ctx, dfk_weights_s* const* layers, int L,
               const dfk_config* cfg) {
   const int64_t total = static_cast<int64_t>(L) * steps;
   const size_t bytes = static_cast<size_t>(B * layers[0]->d_model) * 2;
+  // Every scratch buffer of the chain exists before the first launch: a
+  // cudaMalloc between launches may wait for the device, which under the
+  // fused TP all-reduce would wait for this rank's peers (themselves waiting
+  // for our next launch when one process drives several ranks).
+  DFK_TRY(ensure_buf(ctx->dec[0], bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx->dec[1], bytes, false, ctx->stream));
+  if (tp_active(ctx))
+    DFK_TRY(ensure_buf(ctx->dec_f32, bytes * 2, false, ctx->stream));
   const void* cur = x;
   int64_t k = 0;
   for (int s = 0; s < steps; ++s) {

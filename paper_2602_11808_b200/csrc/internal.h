@@ -102,6 +102,14 @@ struct dfk_context_s {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
 
+  // Fused TP all-reduce (tp.cpp): this rank's symmetric workspace
+  // (IPC-exportable) and every rank's workspace base as seen from here.
+  dfk::DeviceBuf tp_sym;
+  int64_t tp_max_b = 0, tp_dm = 0;
+  int tp_sym_rank = 0, tp_sym_size = 0;
+  void* tp_peer[8] = {};
+  bool tp_peer_ipc[8] = {};
+
   // Decode loop (decode.cpp): bf16 ping-pong activations, fp32 TP partial,
   // captured sequences keyed by (layers, batch, steps, buffers, config).
   dfk::DeviceBuf dec[2];
@@ -165,6 +173,7 @@ cudaError_t launch_fill_uniform_bf16(__nv_bfloat16* p, int64_t n,
 cudaError_t launch_flush(void* p, size_t bytes, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n,
                                cudaStream_t s);
+cudaError_t preload_aux_kernels();
 
 // api.cu helpers used by the scheduler / TP translation units.
 int resolve_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
@@ -173,6 +182,17 @@ void default_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
                     dfk_config* out);
 int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
                  int64_t B, void* y, int y_dtype, const dfk_config* cfg);
+struct StreamArgs;
+// One tensor-parallel block into fp32 Y (tp.cpp): the fused all-reduce when
+// the symmetric workspaces are set up, else the NCCL all-reduce, else
+// (single rank) the plain block.
+int tp_block(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
+             float* y, const dfk_config* cfg);
+bool tp_active(const dfk_context_s* ctx);
+// The block kernel with the fused TP all-reduce (tp.cpp): `tp` carries the
+// tp_* fields of StreamArgs; y is this rank's symmetric output.
+int block_fused_tp(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
+                   void* y, const dfk_config& cfg, const StreamArgs* tp);
 int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s);
 std::string config_label(const dfk_config& c);
 

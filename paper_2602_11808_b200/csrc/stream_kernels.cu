@@ -327,15 +327,92 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Cross-rank waits give up (error flag + trap: the launch fails instead of
+// hanging the GPU) after 4 s.
+__device__ __forceinline__ void tp_spin_check(const StreamArgs& a,
+                                              unsigned long long t0) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (t - t0 > 4000000000ull) {
+    if (a.tp_error) atomicExch(a.tp_error, 1);
+    __threadfence_system();
+    __trap();
+  }
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Down epilogue tail: publish this CTA's piece of tile t; the CTA adding the
 // last piece converts the tile to the output dtype and re-zeroes it.
+// Fused-TP tail of a down piece of tile t (nk K blocks): see StreamArgs.
+__device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int nk,
+                                               int tid, int nthr, int* smem_flag) {
+  const int o = t % a.tp_size;
+  __threadfence_system();
+  named_bar(1, nthr);
+  if (tid == 0) {
+    const int old = atomicAdd_system(a.tp_cnt[o] + t, nk);
+    *smem_flag = (old + nk == a.tp_total_kb) ? 1 : 0;
+  }
+  named_bar(1, nthr);
+  if (*smem_flag) {
+    __threadfence_system();
+    float* acc = a.tp_yacc[o];
+    const int col0 = t * kDownCols;
+    const int nvec = a.B * (kDownCols / 4);
+    for (int base = tid; base < nvec; base += 4 * nthr) {
+      float4 v[4];
+      float4* q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * nthr;
+        q[u] = nullptr;
+        if (idx < nvec) {
+          const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
+          q[u] = reinterpret_cast<float4*>(acc + static_cast<int64_t>(n) * a.yacc_ld + j);
+          v[u] = __ldcg(q[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * nthr;
+        if (idx < nvec) {
+          const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
+          if (j < a.out_cols) {  // out_cols is a multiple of 4 in TP mode
+            for (int r = 0; r < a.tp_size; ++r)
+              *reinterpret_cast<float4*>(a.tp_y[r] + n * a.y_ld + j) = v[u];
+          }
+          __stcg(q[u], make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+      }
+    }
+    if (tid == 0) a.tp_cnt[o][t] = 0;
+    __threadfence_system();
+    named_bar(1, nthr);
+    if (tid < a.tp_size) atomicAdd_system(a.tp_done[tid], 1);
+  }
+  named_bar(1, nthr);
+}
+
+__device__ __forceinline__ float* down_acc(const StreamArgs& a, int t) {
+  return a.tp_size > 1 ? a.tp_yacc[t % a.tp_size] : a.yacc;
+}
+
 __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
-                                                 const Plan& p, int t, int tid,
-                                                 int nthr, int* smem_flag) {
+                                                 const Plan& p, int t, int nk,
+                                                 int tid, int nthr, int* smem_flag) {
+  if (a.tp_size > 1) {
+    tp_finish_tile(a, t, nk, tid, nthr, smem_flag);
+    return;
+  }
   __threadfence();
   named_bar(1, nthr);
   if (tid == 0) {
@@ -749,12 +826,12 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
           if (c == 0 && n < a.B && j < a.out_cols) {
-            atomicAdd(a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j,
+            atomicAdd(down_acc(a, pc.tile) + static_cast<int64_t>(n) * a.yacc_ld + j,
                       acc[r][n]);
           }
         }
       }
-      down_finish_tile(a, p, pc.tile, tid, nthr, smem_flag);
+      down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, nthr, smem_flag);
     }
     if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
   }
@@ -984,6 +1061,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       if (a.flags) s1_publish(a, pc.tile, tid, 128);
     } else {
       const int j = pc.tile * kDownCols + row;
+      float* yacc = down_acc(a, pc.tile);
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + c0, v);
@@ -991,14 +1069,14 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
         for (int e = 0; e < 16; ++e) {
           const int n = c0 + e;
           if (n < a.B && j < a.out_cols) {
-            atomicAdd(a.yacc + static_cast<int64_t>(n) * a.yacc_ld + j, v[e]);
+            atomicAdd(yacc + static_cast<int64_t>(n) * a.yacc_ld + j, v[e]);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      down_finish_tile(a, p, pc.tile, tid, 128, smem_flag);
+      down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, 128, smem_flag);
     }
     if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
     ++acc_it;
@@ -1094,9 +1172,18 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
 
   __syncthreads();
   if (a.dynamic && threadIdx.x == 0) {
-    // The last CTA out re-arms the work counter for the next launch.
+    // The last CTA out re-arms the work counter for the next launch; under
+    // the fused TP all-reduce it first waits until every down tile of this
+    // rank's Y has been written (by whichever rank finished it).
     __threadfence();
     if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      if (kMode == kModeBlock && a.tp_size > 1) {
+        int* done = a.tp_done[a.tp_rank];
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+        while (ld_acquire_sys(done) < a.t2) tp_spin_check(a, t0);
+        *done = 0;
+      }
       a.sched[0] = 0;
       a.sched[1] = 0;
       __threadfence();
@@ -1177,6 +1264,27 @@ cudaError_t launch_mode(bool tc, int nb, const CUtensorMap& xmap,
 }
 
 }  // namespace
+
+// Force-load (see preload_aux_kernels) and opt in every instantiation.
+cudaError_t preload_stream_kernels() {
+  const void* fns[] = {
+#define DFK_K(m) \
+  reinterpret_cast<const void*>(stream_kernel<m, true, 0>),  \
+      reinterpret_cast<const void*>(stream_kernel<m, false, 1>), \
+      reinterpret_cast<const void*>(stream_kernel<m, false, 2>), \
+      reinterpret_cast<const void*>(stream_kernel<m, false, 4>), \
+      reinterpret_cast<const void*>(stream_kernel<m, false, 8>)
+      DFK_K(kModeStage1), DFK_K(kModeDown), DFK_K(kModeBlock)
+#undef DFK_K
+  };
+  for (const void* f : fns) {
+    cudaFuncAttributes at;
+    cudaError_t e = cudaFuncGetAttributes(&at, f);
+    if (e == cudaSuccess) e = allow_max_smem(f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 // How many clusters of `split` CTAs (with this kernel's smem) can be
 // co-resident; clusters beyond it would run in a second wave (and, in the

@@ -17,6 +17,8 @@ namespace dfk {
 //              it published its completion flag (epoch-tagged).
 enum StreamMode : int { kModeStage1 = 0, kModeDown = 1, kModeBlock = 2 };
 
+constexpr int kMaxTp = 8;  // ranks of the fused TP all-reduce
+
 struct StreamArgs {
   // Stage-1 pack ([W_gate|W_up] interleaved): t1 tiles x kb1 K blocks.
   const uint8_t* w1;
@@ -88,6 +90,23 @@ struct StreamArgs {
   // beyond the smem ring BEFORE griddepcontrol.wait: under PDL the HBM
   // stream of this launch starts during the previous launch's tail.
   int pf_kb;
+  // Fused tensor-parallel all-reduce (kModeBlock + dynamic, tp_size > 1):
+  // down tile t is OWNED by rank t % tp_size.  Every rank red.adds its
+  // partial sums of tile t into the owner's fp32 workspace tp_yacc[owner]
+  // over NVLink peer memory and counts the K blocks it contributed on the
+  // owner's tp_cnt[owner][t]; the CTA (on any rank) that completes the
+  // tile's tp_total_kb K blocks reads the full sums, writes Y into EVERY
+  // rank's tp_y[r] (the all-gather), re-zeroes the owner's workspace and
+  // counter and bumps every rank's tp_done[r].  A rank's launch ends when
+  // its tp_done reaches t2 (spun on by its last CTA out, then reset), so Y
+  // on every rank is the full sum when the kernel completes: the block's one
+  // collective runs inside the kernel, overlapped with the down stream.
+  int tp_rank, tp_size, tp_total_kb;
+  float* tp_yacc[kMaxTp];
+  int* tp_cnt[kMaxTp];
+  int* tp_done[kMaxTp];
+  float* tp_y[kMaxTp];
+  int* tp_error;  // set before __trap() when a cross-rank wait times out
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.
@@ -116,5 +135,6 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xma
 
 int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k = 1);
 int stream_max_clusters(int mode, int split, int smem);
+cudaError_t preload_stream_kernels();
 
 }  // namespace dfk

@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "internal.h"
+#include "layout.cuh"
+#include "stream_kernels.cuh"
 
 using namespace dfk;
 
@@ -23,7 +25,58 @@ int nccl_fail(ncclResult_t r, const char* what) {
   return fail(DFK_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
 }
 
+// One symmetric workspace per rank, identical layout on every rank (so a
+// peer's buffers are at the same offsets from its base): fp32 down
+// accumulator [max_b x t2*128], per-tile K-block counters, the done counter,
+// an error flag, and the full-sum Y [max_b x d_model] fp32.
+struct SymLayout {
+  size_t yacc, cnt, done, err, y, total;
+  int t2;
+};
+
+size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+
+SymLayout sym_layout(int64_t max_b, int64_t dm) {
+  SymLayout L;
+  L.t2 = static_cast<int>((dm + kDownCols - 1) / kDownCols);
+  size_t off = 0;
+  L.yacc = off;
+  off = align256(off + static_cast<size_t>(max_b) * L.t2 * kDownCols * 4);
+  L.cnt = off;
+  off = align256(off + static_cast<size_t>(L.t2) * 4);
+  L.done = off;
+  off = align256(off + 4);
+  L.err = off;
+  off = align256(off + 4);
+  L.y = off;
+  off = align256(off + static_cast<size_t>(max_b * dm) * 4);
+  L.total = off;
+  return L;
+}
+
+void close_peers(dfk_context_s* ctx) {
+  for (int r = 0; r < 8; ++r) {
+    if (ctx->tp_peer_ipc[r] && ctx->tp_peer[r]) cudaIpcCloseMemHandle(ctx->tp_peer[r]);
+    ctx->tp_peer[r] = nullptr;
+    ctx->tp_peer_ipc[r] = false;
+  }
+}
+
 }  // namespace
+
+namespace dfk {
+
+bool tp_active(const dfk_context_s* ctx) {
+  return ctx->tp_sym_size > 1 || (ctx->comm && ctx->nranks > 1);
+}
+
+int tp_block(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
+             float* y, const dfk_config* cfg) {
+  if (ctx->tp_sym_size > 1) return dfk_tp_forward_fused(ctx, w, x, B, y, cfg);
+  return dfk_tp_forward(ctx, w, x, B, y, cfg);
+}
+
+}  // namespace dfk
 
 extern "C" {
 
@@ -103,6 +156,147 @@ int dfk_tp_forward(dfk_context ctx, dfk_weights w, const void* x,
                       ncclSum, ctx->comm, ctx->stream);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
   }
+  return DFK_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused TP all-reduce over NVLink peer memory.
+// ---------------------------------------------------------------------------
+int dfk_tp_sym_create(dfk_context ctx, int64_t max_batch, int64_t d_model,
+                      void* ipc_handle64) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  if (max_batch < 1 || max_batch > 256 || d_model < 4 || d_model % 4)
+    return fail(DFK_ERR_SHAPE, "fused TP needs 1 <= max_batch <= 256 and d_model % 4 == 0");
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  close_peers(ctx);
+  if (ctx->tp_sym.p) {
+    cudaFree(ctx->tp_sym.p);
+    ctx->tp_sym = {};
+  }
+  const SymLayout L = sym_layout(max_batch, d_model);
+  DFK_CUDA(cudaMalloc(&ctx->tp_sym.p, L.total));
+  ctx->tp_sym.bytes = L.total;
+  DFK_CUDA(cudaMemsetAsync(ctx->tp_sym.p, 0, L.total, ctx->stream));
+  DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->tp_max_b = max_batch;
+  ctx->tp_dm = d_model;
+  ctx->tp_sym_rank = 0;
+  ctx->tp_sym_size = 1;
+  ctx->tp_peer[0] = ctx->tp_sym.p;
+  if (ipc_handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaIpcMemHandle_t h;
+    DFK_CUDA(cudaIpcGetMemHandle(&h, ctx->tp_sym.p));
+    std::memcpy(ipc_handle64, &h, sizeof(h));
+  }
+  return DFK_OK;
+}
+
+int dfk_tp_sym_open(dfk_context ctx, const void* handles, int rank, int nranks) {
+  if (!ctx || !handles) return fail(DFK_ERR_INVALID, "null argument");
+  if (!ctx->tp_sym.p) return fail(DFK_ERR_INVALID, "dfk_tp_sym_create first");
+  if (nranks < 1 || nranks > kMaxTp || rank < 0 || rank >= nranks)
+    return fail(DFK_ERR_INVALID, "bad rank/nranks (fused TP supports up to 8 ranks)");
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  close_peers(ctx);
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) {
+      ctx->tp_peer[r] = ctx->tp_sym.p;
+      continue;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      close_peers(ctx);
+      return fail(DFK_ERR_CUDA, std::string("cudaIpcOpenMemHandle(rank ") +
+                                    std::to_string(r) + "): " + cudaGetErrorString(e));
+    }
+    ctx->tp_peer[r] = p;
+    ctx->tp_peer_ipc[r] = true;
+  }
+  ctx->tp_sym_rank = rank;
+  ctx->tp_sym_size = nranks;
+  return DFK_OK;
+}
+
+int dfk_tp_sym_attach(dfk_context* ctxs, int n) {
+  if (!ctxs || n < 1 || n > kMaxTp) return fail(DFK_ERR_INVALID, "bad context list");
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || !ctxs[i]->tp_sym.p)
+      return fail(DFK_ERR_INVALID, "every context needs dfk_tp_sym_create first");
+    if (ctxs[i]->tp_max_b != ctxs[0]->tp_max_b || ctxs[i]->tp_dm != ctxs[0]->tp_dm)
+      return fail(DFK_ERR_SHAPE, "symmetric workspaces differ in max_batch / d_model");
+  }
+  for (int i = 0; i < n; ++i) {
+    DFK_CUDA(cudaSetDevice(ctxs[i]->device));
+    close_peers(ctxs[i]);
+    for (int j = 0; j < n; ++j) {
+      if (ctxs[j]->device != ctxs[i]->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[j]->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+        } else if (e != cudaSuccess) {
+          return fail(DFK_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") +
+                                        cudaGetErrorString(e));
+        }
+      }
+      ctxs[i]->tp_peer[j] = ctxs[j]->tp_sym.p;
+    }
+    ctxs[i]->tp_sym_rank = i;
+    ctxs[i]->tp_sym_size = n;
+  }
+  return DFK_OK;
+}
+
+int dfk_tp_forward_fused(dfk_context ctx, dfk_weights w, const void* x,
+                         int64_t batch, float* y, const dfk_config* cfg) {
+  if (!ctx || !w) return fail(DFK_ERR_INVALID, "null handle");
+  if (w->ctx != ctx) return fail(DFK_ERR_INVALID, "weights belong to another context");
+  if (!x || !y) return fail(DFK_ERR_INVALID, "null activation pointer");
+  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
+  if (ctx->tp_sym_size < 1 || !ctx->tp_sym.p)
+    return fail(DFK_ERR_INVALID, "dfk_tp_sym_create / _open / _attach first");
+  const int P = ctx->tp_sym_size;
+  if (P == 1) return forward_impl(ctx, w, x, batch, y, DFK_F32, cfg);
+  if (batch > ctx->tp_max_b)
+    return fail(DFK_ERR_SHAPE, "batch exceeds the symmetric workspace's max_batch");
+  if (w->d_model != ctx->tp_dm)
+    return fail(DFK_ERR_SHAPE, "weights' d_model differs from the symmetric workspace");
+  dfk_config c;
+  DFK_TRY(resolve_config(ctx, w, batch, cfg, &c));
+  c.variant = DFK_VARIANT_FUSED;  // the all-reduce lives in the block kernel
+  c.block_kernel = 1;
+  c.dynamic_sched = 1;
+  c.s1_split_k = 1;
+  // Down K blocks contributed to every tile by all ranks (shards may differ
+  // by one column, balanced_ranges tp.cpp:8-29).
+  int total_kb = 0;
+  for (int r = 0; r < P; ++r) {
+    int64_t b = 0, e = 0;
+    DFK_TRY(dfk_balanced_range(w->d_ff_total, P, r, &b, &e));
+    total_kb += static_cast<int>((e - b + kBlockK - 1) / kBlockK);
+  }
+  const SymLayout L = sym_layout(ctx->tp_max_b, ctx->tp_dm);
+  StreamArgs t = {};
+  t.tp_rank = ctx->tp_sym_rank;
+  t.tp_size = P;
+  t.tp_total_kb = total_kb;
+  t.yacc_ld = L.t2 * kDownCols;
+  for (int r = 0; r < P; ++r) {
+    auto* base = static_cast<uint8_t*>(ctx->tp_peer[r]);
+    if (!base) return fail(DFK_ERR_INVALID, "peer workspace missing");
+    t.tp_yacc[r] = reinterpret_cast<float*>(base + L.yacc);
+    t.tp_cnt[r] = reinterpret_cast<int*>(base + L.cnt);
+    t.tp_done[r] = reinterpret_cast<int*>(base + L.done);
+    t.tp_y[r] = reinterpret_cast<float*>(base + L.y);
+  }
+  auto* own = static_cast<uint8_t*>(ctx->tp_sym.p);
+  t.tp_error = reinterpret_cast<int*>(own + L.err);
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  DFK_TRY(block_fused_tp(ctx, w, x, batch, own + L.y, c, &t));
+  DFK_CUDA(cudaMemcpyAsync(y, own + L.y, static_cast<size_t>(batch * w->d_model) * 4,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
   return DFK_OK;
 }
 

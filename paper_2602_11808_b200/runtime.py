@@ -145,6 +145,10 @@ _sigs = {
     "dfk_tp_group_start": ([], C.c_int),
     "dfk_tp_group_end": ([], C.c_int),
     "dfk_tp_forward": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
+    "dfk_tp_sym_create": ([_vp, _i64, _i64, _vp], C.c_int),
+    "dfk_tp_sym_open": ([_vp, _vp, C.c_int, C.c_int], C.c_int),
+    "dfk_tp_sym_attach": ([C.POINTER(_vp), C.c_int], C.c_int),
+    "dfk_tp_forward_fused": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
     "dfk_decode": ([_vp, C.POINTER(_vp), C.c_int32, _vp, _i64, C.c_int32, _vp,
                     C.POINTER(Config), C.c_int32], C.c_int),
     "dfk_balanced_range": ([_i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)],
@@ -491,6 +495,32 @@ class Context:
         arr = (_vp * len(layers))(*[w.h for w in layers])
         _check(lib.dfk_decode(self.h, arr, len(layers), x.ptr, x.shape[0], steps, y.ptr,
                               self._cfg(cfg), 1 if graph else 0))
+
+    # --- fused TP all-reduce over NVLink peer memory ---
+    def tp_sym_create(self, max_batch: int, d_model: int) -> bytes:
+        """Allocate this rank's symmetric workspace; returns its IPC handle."""
+        h = (C.c_char * 64)()
+        _check(lib.dfk_tp_sym_create(self.h, max_batch, d_model, h))
+        return bytes(h)
+
+    def tp_sym_open(self, handles, rank: int, nranks: int):
+        """Multi-process: every rank's handle (rank order)."""
+        blob = b"".join(handles)
+        assert len(blob) == 64 * nranks
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        _check(lib.dfk_tp_sym_open(self.h, buf, rank, nranks))
+
+    @staticmethod
+    def tp_sym_attach(ctxs):
+        """One process driving several contexts (rank i = ctxs[i])."""
+        arr = (_vp * len(ctxs))(*[c.h for c in ctxs])
+        _check(lib.dfk_tp_sym_attach(arr, len(ctxs)))
+
+    def tp_forward_fused(self, w: Weights, x: DeviceArray, y: DeviceArray,
+                         cfg: Optional[Config] = None):
+        assert y.dtype == F32
+        _check(lib.dfk_tp_forward_fused(self.h, w.h, x.ptr, x.shape[0], y.ptr,
+                                        self._cfg(cfg)))
 
     def tp_forward(self, w: Weights, x: DeviceArray, y: DeviceArray,
                    cfg: Optional[Config] = None):

@@ -9,7 +9,10 @@ it can be exercised on CPU with the gloo backend (tests/test_tp_gloo.py):
 * exchange_uid — rank 0's 128-byte NCCL unique id broadcast to every rank;
 * max_over_ranks — the bench contract's max-over-ranks timing reduction;
 * sum_partials — the compound scheme's single all-reduce of partial Y for
-                 host-resident fp64 partials (the check the gloo test runs).
+                 host-resident fp64 partials (the check the gloo test runs);
+* setup_fused  — the fused all-reduce's symmetric workspaces: every rank's
+                 64-byte CUDA IPC handle all-gathered, peers opened, and the
+                 ranks agree (all or none) on using it.
 """
 from __future__ import annotations
 
@@ -54,3 +57,30 @@ def sum_partials(dist, partial: np.ndarray) -> np.ndarray:
     t = torch.from_numpy(np.ascontiguousarray(partial, dtype=np.float64).copy())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.numpy()
+
+
+def setup_fused(dist, ctx, rank: int, world: int, max_batch: int, d_model: int) -> bool:
+    """dfk_tp_sym_create on every rank, all-gather the IPC handles,
+    dfk_tp_sym_open; True only if every rank succeeded (then all ranks use
+    dfk_tp_forward_fused, otherwise all keep the NCCL all-reduce)."""
+    ok = 1
+    handle = b"\0" * 64
+    try:
+        handle = ctx.tp_sym_create(max_batch, d_model)
+    except Exception:  # noqa: BLE001
+        ok = 0
+    handles = [handle]
+    if dist is not None:
+        handles = [None] * world
+        dist.all_gather_object(handles, handle)
+    if ok:
+        try:
+            ctx.tp_sym_open(handles, rank, world)
+        except Exception:  # noqa: BLE001
+            ok = 0
+    if dist is not None:
+        import torch
+        t = torch.tensor([ok], dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = int(t.item())
+    return bool(ok)

@@ -469,3 +469,71 @@ def test_stage1_stream_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, fam):
         # the workspace is left all-zero: a second correct call still passes
         ctx.stage1(w, xd, a2, cfg=rt.Config.make(**kw))
         assert rel_err(a2.download(), a2_ref) <= TOL
+
+
+@pytest.mark.parametrize("P,B", [(2, 1), (3, 5), (4, 17), (8, 2)])
+def test_tp_fused_allreduce_emulated_ranks(rt, oracle_lib, P, B):
+    """The fused TP all-reduce (dfk_tp_forward_fused: owner-tile red.adds
+    over peer memory, in-kernel all-gather, done counters) with P ranks
+    emulated by P contexts on one GPU (their own streams, launched back to
+    back, synchronised once): every rank's Y is the full block within the
+    bf16 tolerance (test_tp.cpp:74-112; NCCL/peer summation order differs
+    from device order), repeatedly (the workspace and counters re-arm)."""
+    dm, df = 512, 1600 + P  # uneven shards
+    x, wu, wg, wd = instance(oracle_lib, 400 + P, B, dm, df)
+    _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    ctxs = [rt.Context(0) for _ in range(P)]
+    try:
+        for c in ctxs:
+            c.tp_sym_create(32, dm)
+        rt.Context.tp_sym_attach(ctxs)
+        ws, xs, ys = [], [], []
+        for p, c in enumerate(ctxs):
+            b, e = rt.balanced_range(df, P, p)
+            ws.append(c.weights(wg, wu, wd, ff_range=(b, e)))
+            xs.append(c.array((B, dm)).upload(x))
+            ys.append(c.array((B, dm), rt.F32))
+        for rep in range(3):
+            for p, c in enumerate(ctxs):
+                c.tp_forward_fused(ws[p], xs[p], ys[p])
+            for c in ctxs:
+                c.sync()
+            for p in range(P):
+                assert rel_err(ys[p].download(), y_ref) <= TOL, (rep, p)
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def test_tp_fused_decode_graph_emulated_ranks(rt, oracle_lib):
+    """dfk_decode under the fused TP all-reduce (2 emulated ranks on one GPU):
+    2 layers x 2 steps, eager then graph-replayed, every rank's final Y is
+    the oracle chain (x <- Y in bf16)."""
+    P, B, dm, df = 2, 3, 384, 1000
+    layers = [instance(oracle_lib, 500 + l, B, dm, df)[1:] for l in range(2)]
+    x0 = instance(oracle_lib, 499, B, dm, df)[0]
+    xr = x0
+    for _ in range(2):
+        for (wu, wg, wd) in layers:
+            xr = oracle_lib.quantize_bf16(oracle_lib.forward(xr, wu, wg, wd)[1])[0]
+    ctxs = [rt.Context(0) for _ in range(P)]
+    try:
+        for c in ctxs:
+            c.tp_sym_create(8, dm)
+        rt.Context.tp_sym_attach(ctxs)
+        ws = []
+        for p, c in enumerate(ctxs):
+            b, e = rt.balanced_range(df, P, p)
+            ws.append([c.weights(wg, wu, wd, ff_range=(b, e)) for (wu, wg, wd) in layers])
+        xs = [c.array((B, dm)).upload(x0) for c in ctxs]
+        ys = [c.array((B, dm)) for c in ctxs]
+        for graph in (False, True, True):
+            for p, c in enumerate(ctxs):
+                c.decode(ws[p], xs[p], 2, ys[p], graph=graph)
+            for c in ctxs:
+                c.sync()
+            for p in range(P):
+                assert rel_err(ys[p].download(), xr) <= 2 * TOL, (graph, p)
+    finally:
+        for c in ctxs:
+            c.close()
