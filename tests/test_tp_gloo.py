@@ -72,3 +72,57 @@ def test_tp_world2_gloo(world):
         assert uid_ok
         assert tmax == float(world)          # max over ranks
         assert err_full <= 1e-12 and err_golden <= 1e-12
+
+
+class _FakeSymCtx:
+    """Stands in for a Context on a CPU box: records the IPC-handle exchange
+    of tp_host.setup_fused; `fail_open` makes this rank's peer mapping fail."""
+
+    def __init__(self, rank, fail_open):
+        self.rank, self.fail_open, self.opened = rank, fail_open, None
+
+    def tp_sym_create(self, max_batch, d_model):
+        return bytes([self.rank]) * 64
+
+    def tp_sym_open(self, handles, rank, world):
+        if self.fail_open:
+            raise RuntimeError("cudaIpcOpenMemHandle failed")
+        self.opened = list(handles)
+
+
+def _sym_worker(rank, world, port, fail_rank, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_11808_b200 import tp_host
+        c = _FakeSymCtx(rank, rank == fail_rank)
+        ok = tp_host.setup_fused(dist, c, rank, world, 64, 4096)
+        out_q.put((rank, ok, c.opened))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_fused_tp_handle_exchange_gloo(fail_rank):
+    """setup_fused: every rank receives every rank's 64-byte handle in rank
+    order, and the ranks agree -- one rank failing to map its peers makes ALL
+    ranks keep the NCCL all-reduce (a split decision would deadlock)."""
+    import multiprocessing as mp
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_worker, args=(r, world, port, fail_rank, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, opened in res:
+        assert ok == (fail_rank < 0)
+        if rank != fail_rank:
+            assert opened == [bytes([r]) * 64 for r in range(world)]
