@@ -310,6 +310,10 @@ DFK_API int dfk_flush_l2(dfk_context ctx);
 DFK_API int dfk_set_trace(dfk_context ctx, void* buf, int64_t slots);
 /* Number of hot-path kernel launches issued by this context so far. */
 DFK_API int dfk_launch_count(dfk_context ctx, int64_t* n);
+/* Synchronises the context stream, then cudaProfilerStart (start != 0) or
+ * cudaProfilerStop: brackets the launches an `ncu --profile-from-start off`
+ * capture sees (the traffic-model assertion, tests/test_traffic_ncu.py). */
+DFK_API int dfk_profiler_range(dfk_context ctx, int32_t start);
 
 #ifdef __cplusplus
 }

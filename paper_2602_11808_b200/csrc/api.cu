@@ -13,6 +13,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_profiler_api.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1258,6 +1259,13 @@ int dfk_set_trace(dfk_context ctx, void* buf, int64_t slots) {
 int dfk_launch_count(dfk_context ctx, int64_t* n) {
   if (!ctx || !n) return fail(DFK_ERR_INVALID, "null argument");
   *n = ctx->launches;
+  return DFK_OK;
+}
+
+int dfk_profiler_range(dfk_context ctx, int32_t start) {
+  if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+  DFK_CUDA(start ? cudaProfilerStart() : cudaProfilerStop());
   return DFK_OK;
 }
 

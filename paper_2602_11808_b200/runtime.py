@@ -149,6 +149,7 @@ _sigs = {
     "dfk_tp_sym_open": ([_vp, _vp, C.c_int, C.c_int], C.c_int),
     "dfk_tp_sym_attach": ([C.POINTER(_vp), C.c_int], C.c_int),
     "dfk_tp_forward_fused": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
+    "dfk_profiler_range": ([_vp, C.c_int32], C.c_int),
     "dfk_decode": ([_vp, C.POINTER(_vp), C.c_int32, _vp, _i64, C.c_int32, _vp,
                     C.POINTER(Config), C.c_int32], C.c_int),
     "dfk_balanced_range": ([_i64, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)],
@@ -485,6 +486,9 @@ class Context:
     def tp_init(self, uid: bytes, rank: int, nranks: int):
         buf = C.create_string_buffer(uid, 128)
         _check(lib.dfk_tp_init(self.h, buf, rank, nranks))
+
+    def profiler_range(self, start: bool):
+        _check(lib.dfk_profiler_range(self.h, 1 if start else 0))
 
     def decode(self, layers, x: DeviceArray, steps: int, y: DeviceArray,
                cfg: Optional[Config] = None, graph: bool = True):
