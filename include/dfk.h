@@ -180,9 +180,12 @@ DFK_API int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
                              int32_t y_dtype, const dfk_config* cfg);
 
 /* Asynchronous host-buffer call for pipelined callers: X is bf16 in PINNED
- * host memory, Y is fp32 in PINNED host memory; enqueues H2D(X), the block
- * (or TP block) and D2H(Y) on the context stream and returns.  Buffers must
- * stay valid until dfk_context_sync. */
+ * host memory, Y is fp32 in PINNED host memory.  Enqueues, on the context
+ * stream, a staging kernel that pulls X over PCIe into a device ring slot
+ * (programmatic-dependent launch: it overlaps the previous block) and the
+ * block, which writes Y straight into the pinned buffer (zero-copy); under
+ * TP, H2D(X), the TP block and D2H(Y).  Buffers must stay valid until
+ * dfk_context_sync. */
 DFK_API int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
                                    const void* x_pinned_bf16, int64_t batch,
                                    float* y_pinned, const dfk_config* cfg);

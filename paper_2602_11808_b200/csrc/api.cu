@@ -341,6 +341,7 @@ void fill_down(dfk_context_s* ctx, dfk_weights_s* w, void* y, int64_t b0,
                 : static_cast<void*>(static_cast<float*>(y) + b0 * y_ld);
   a->y_ld = y_ld;
   a->y_bf16 = y_bf16 ? 1 : 0;
+  a->y_vec4 = !y_bf16 && y_ld % 4 == 0 && (reinterpret_cast<uintptr_t>(a->y) & 15) == 0;
   a->out_cols = static_cast<int>(w->d_model);
 }
 
@@ -855,6 +856,8 @@ int dfk_context_destroy(dfk_context ctx) {
   }
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
   ctx->graphs.clear();
+  for (HostSlot& sl : ctx->host_slots)
+    if (sl.x.p) cudaFree(sl.x.p);
   for (int r = 0; r < 8; ++r)
     if (ctx->tp_peer_ipc[r] && ctx->tp_peer[r]) cudaIpcCloseMemHandle(ctx->tp_peer[r]);
   if (ctx->tp_sym.p) cudaFree(ctx->tp_sym.p);
@@ -1120,6 +1123,33 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
   if (!x_pinned_bf16 || !y_pinned) return fail(DFK_ERR_INVALID, "null host pointer");
   const size_t xb = static_cast<size_t>(batch * w->d_model) * 2;
   const size_t yb = static_cast<size_t>(batch * w->d_model) * 4;
+  if (!tp_active(ctx) && xb % 16 == 0) {
+    // Zero-copy chain: a staging kernel pulls X over PCIe into a ring slot
+    // (PDL: overlapping the previous block), the block writes Y straight
+    // into the caller's pinned buffer -- kernels only, no memcpy or event
+    // between the blocks, so consecutive calls stay PDL-chained.  (A copy
+    // stream + events variant measured slower: the events between kernels
+    // break the PDL chain, tools/e2e_probe.py.)
+    cudaPointerAttributes ax{}, ay{};
+    DFK_CUDA(cudaPointerGetAttributes(&ax, x_pinned_bf16));
+    DFK_CUDA(cudaPointerGetAttributes(&ay, y_pinned));
+    if (!ax.devicePointer || !ay.devicePointer)
+      return fail(DFK_ERR_INVALID, "forward_host_async needs pinned (cudaMallocHost) buffers");
+    HostSlot& sl = ctx->host_slots[ctx->host_next];
+    ctx->host_next = (ctx->host_next + 1) % kHostSlots;
+    if (sl.x.bytes < xb) {
+      // Grow every slot at once (geometrically): a reallocation waits for
+      // the device, so it must not recur as batch sizes rotate over slots.
+      DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+      const size_t nb = std::max<size_t>({xb, 2 * sl.x.bytes, 64 * 1024});
+      for (HostSlot& o : ctx->host_slots) DFK_TRY(ensure_buf(o.x, nb, false, ctx->stream));
+    }
+    cudaError_t e = launch_stage_rows(ax.devicePointer, sl.x.p, static_cast<int64_t>(xb),
+                                      ctx->stream);
+    if (e != cudaSuccess) return fail(DFK_ERR_CUDA, cudaGetErrorString(e));
+    ctx->launches++;
+    return forward_impl(ctx, w, sl.x.p, batch, ay.devicePointer, DFK_F32, cfg);
+  }
   // Stream order makes one staging pair safe: the next call's H2D runs after
   // this call's kernels, its kernels after this call's D2H.
   DFK_TRY(ensure_buf(ctx->hx_dev, xb, false, ctx->stream));

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "internal.h"
@@ -216,6 +217,19 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in,
   }
 }
 
+// Host-buffer path: copies X (bf16, 16-byte units) from mapped pinned host
+// memory into a device staging slot, then joins the programmatic-dependent
+// chain: it lets the next block kernel pre-launch immediately and waits for
+// the previous kernel only AFTER its copy -- so the PCIe read of call i+1's
+// X overlaps call i's block.
+__global__ void stage_rows_kernel(const uint4* __restrict__ src,
+                                  uint4* __restrict__ dst, int64_t n16) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int64_t i = gtid(); i < n16; i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 unsigned grid_for(int64_t total, int threads) {
   int64_t g = (total + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -244,7 +258,8 @@ cudaError_t preload_aux_kernels() {
       reinterpret_cast<const void*>(mul_kernel),
       reinterpret_cast<const void*>(fill_uniform_kernel),
       reinterpret_cast<const void*>(flush_kernel),
-      reinterpret_cast<const void*>(f32_to_bf16_kernel)};
+      reinterpret_cast<const void*>(f32_to_bf16_kernel),
+      reinterpret_cast<const void*>(stage_rows_kernel)};
   for (const void* f : fns) {
     cudaFuncAttributes at;
     const cudaError_t e = cudaFuncGetAttributes(&at, f);
@@ -369,6 +384,22 @@ cudaError_t launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n,
                                cudaStream_t s) {
   f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, out, n);
   return cudaGetLastError();
+}
+
+cudaError_t launch_stage_rows(const void* src, void* dst, int64_t bytes,
+                              cudaStream_t s) {
+  const int64_t n16 = bytes / 16;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(16, (n16 + 255) / 256 + 1)));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, stage_rows_kernel, static_cast<const uint4*>(src),
+                            static_cast<uint4*>(dst), n16);
 }
 
 }  // namespace dfk

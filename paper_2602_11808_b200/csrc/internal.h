@@ -47,6 +47,12 @@ struct DeviceBuf {
   size_t bytes = 0;
 };
 
+// One X staging slot of the host-buffer forward (dfk_forward_host_async).
+struct HostSlot {
+  DeviceBuf x;
+};
+constexpr int kHostSlots = 8;
+
 // A captured decode sequence (decode.cpp) and its kernel launch count.
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
@@ -85,6 +91,8 @@ struct dfk_context_s {
   dfk::DeviceBuf lt_ws;    // cuBLASLt workspace
   dfk::DeviceBuf flush;    // L2 flush buffer
   dfk::DeviceBuf hx_dev, hy_dev;  // forward_host device staging
+  dfk::HostSlot host_slots[dfk::kHostSlots];
+  int host_next = 0;
   void* hx_pinned = nullptr;
   size_t hx_pinned_bytes = 0;
   void* hy_pinned = nullptr;
@@ -174,6 +182,8 @@ cudaError_t launch_flush(void* p, size_t bytes, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n,
                                cudaStream_t s);
 cudaError_t preload_aux_kernels();
+cudaError_t launch_stage_rows(const void* src, void* dst, int64_t bytes,
+                              cudaStream_t s);
 
 // api.cu helpers used by the scheduler / TP translation units.
 int resolve_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,

@@ -445,14 +445,20 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
         if (idx < nvec) {
           const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
           const float vv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          if (a.y_vec4 && j + 3 < a.out_cols) {
+            // one 16-byte store (Y may live in mapped host memory: whole
+            // PCIe write lines instead of 4-byte partial ones)
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.y) + n * a.y_ld + j) = v[u];
+          } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (j + e < a.out_cols) {
-              if (a.y_bf16) {
-                reinterpret_cast<__nv_bfloat16*>(a.y)[n * a.y_ld + j + e] =
-                    __float2bfloat16_rn(vv[e]);
-              } else {
-                reinterpret_cast<float*>(a.y)[n * a.y_ld + j + e] = vv[e];
+            for (int e = 0; e < 4; ++e) {
+              if (j + e < a.out_cols) {
+                if (a.y_bf16) {
+                  reinterpret_cast<__nv_bfloat16*>(a.y)[n * a.y_ld + j + e] =
+                      __float2bfloat16_rn(vv[e]);
+                } else {
+                  reinterpret_cast<float*>(a.y)[n * a.y_ld + j + e] = vv[e];
+                }
               }
             }
           }

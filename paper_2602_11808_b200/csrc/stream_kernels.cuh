@@ -50,6 +50,7 @@ struct StreamArgs {
   void* y;
   int64_t y_ld;
   int y_bf16;
+  int y_vec4;  // fp32 Y, 16-byte aligned rows: float4 stores
   int out_cols;
   // kModeBlock: per-stage-1-tile completion flags and this launch's epoch.
   unsigned* flags;
