@@ -316,6 +316,12 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   const int sk = a->split_k > 1 ? a->split_k : 1;
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk);
   a->trace = ctx->trace;
+  // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
+  a->nacc = 1;
+  if (tc && sk == 1) {
+    int n = std::max(1, std::min(env_int("DFK_NACC", 1), 256 / n_pad));
+    a->nacc = n >= 4 ? 4 : n >= 2 ? 2 : 1;
+  }
   // 12 K blocks (192 KiB) of L2 prefetch: the measured optimum (A/B sweep
   // 0..60, profiles/r1b_tuning.md).
   a->pf_kb = env_int("DFK_PF_KB", 12);

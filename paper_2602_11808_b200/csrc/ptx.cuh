@@ -297,6 +297,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Sum of `nacc` accumulators `stride` TMEM columns apart (the independent
+// MMA chains of one tile), 16 columns from taddr.
+__device__ __forceinline__ void tmem_ld16_sum(uint32_t taddr, int nacc, uint32_t stride,
+                                              float (&v)[16]) {
+  tmem_ld16(taddr, v);
+  for (int j = 1; j < nacc; ++j) {
+    float t[16];
+    tmem_ld16(taddr + static_cast<uint32_t>(j) * stride, t);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += t[i];
+  }
+}
+
 // UMMA shared-memory descriptor for a K-major, 128B-swizzled operand whose
 // 8-row groups are 1024 B apart (rows 128 B = 64 bf16 of K).
 // Fields (sm100): start>>4 [0,14), LBO>>4 [16,30) (unused for SW128 K-major,

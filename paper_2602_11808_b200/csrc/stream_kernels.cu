@@ -847,14 +847,53 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
 // ---------------------------------------------------------------------------
 // tcgen05 MMA issuer (one lane of warp 1).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
-                                          uint8_t* smem, int stage_bytes,
-                                          uint64_t* full, uint64_t* empty,
-                                          uint64_t* tfull, uint64_t* tempty,
-                                          uint32_t tmem_base, PieceQueue* pq) {
+// One ring stage of MMAs: NB K blocks x 4 K16 steps, fully unrolled, the
+// smem descriptors advanced by constant adds (the start-address field is
+// addr >> 4 in the low bits), MMA i into accumulator chain i % NACC.  The
+// single issuing thread is on the streaming critical path (a slot is freed
+// only when its MMAs retire), so this loop is kept branch- and divide-free.
+template <int NB, int NACC>
+__device__ __forceinline__ void mma_stage(uint32_t d, uint64_t dw, uint64_t dx,
+                                          uint32_t idesc, uint32_t xblk16,
+                                          uint32_t chain_cols, bool zero) {
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+#pragma unroll
+    for (int k = 0; k < kBlockK / 16; ++k) {
+      constexpr int kSteps = kBlockK / 16;
+      const int i = b * kSteps + k;
+      const uint64_t ad = dw + static_cast<uint64_t>((b * kBlockBytes + k * 32) >> 4);
+      const uint64_t bd = dx + static_cast<uint64_t>(b * xblk16 + ((k * 32) >> 4));
+      tc_mma_bf16(d + static_cast<uint32_t>(i % NACC) * chain_cols, ad, bd, idesc,
+                  (zero && i < NACC) ? 0u : 1u);
+    }
+  }
+}
+
+template <int NACC>
+__device__ __forceinline__ void mma_stage_nb(int nb, uint32_t d, uint64_t dw, uint64_t dx,
+                                             uint32_t idesc, uint32_t xblk16,
+                                             uint32_t chain_cols, bool zero) {
+  switch (nb) {
+    case 1: mma_stage<1, NACC>(d, dw, dx, idesc, xblk16, chain_cols, zero); break;
+    case 2: mma_stage<2, NACC>(d, dw, dx, idesc, xblk16, chain_cols, zero); break;
+    case 3: mma_stage<3, NACC>(d, dw, dx, idesc, xblk16, chain_cols, zero); break;
+    default: mma_stage<4, NACC>(d, dw, dx, idesc, xblk16, chain_cols, zero); break;
+  }
+}
+
+template <int NACC>
+__device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
+                                         uint8_t* smem, int stage_bytes,
+                                         uint64_t* full, uint64_t* empty,
+                                         uint64_t* tfull, uint64_t* tempty,
+                                         uint32_t tmem_base, PieceQueue* pq) {
   const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>(a.n_pad));
-  const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
+  const uint32_t xblk16 = static_cast<uint32_t>(a.n_pad) * 128u / 16u;
   const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
+  const uint32_t chain_cols = static_cast<uint32_t>(a.n_pad);
+  const uint64_t desc0 = umma_desc_sw128(0);
+  const uint32_t smem0 = smem_u32(smem);
   int64_t it = 0;
   int acc_it = 0;
   PieceReader pi;
@@ -864,29 +903,37 @@ __device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tempty[ab], aph ^ 1u);
     tc_fence_after();
-    const uint32_t d = tmem_base + static_cast<uint32_t>(ab * a.n_pad);
+    const uint32_t d = tmem_base + static_cast<uint32_t>(ab * NACC * a.n_pad);
+    int slot = static_cast<int>(it % a.stages);
+    uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
-      const int slot = static_cast<int>(it % a.stages);
-      const uint32_t phase = static_cast<uint32_t>((it / a.stages) & 1);
       mbar_wait(&full[slot], phase);
       tc_fence_after();
-      const uint32_t sbase =
-          smem_u32(smem + static_cast<int64_t>(slot) * stage_bytes);
-      for (int b = 0; b < nb; ++b) {
-        const uint32_t wb = sbase + b * kBlockBytes;
-        const uint32_t xb = sbase + wbytes_all + b * xblk;
-#pragma unroll
-        for (int k = 0; k < kBlockK / 16; ++k) {
-          tc_mma_bf16(d, umma_desc_sw128(wb + k * 32),
-                      umma_desc_sw128(xb + k * 32), idesc,
-                      (kb > pc.kb0 || b > 0 || k > 0) ? 1u : 0u);
-        }
-      }
+      const uint32_t sbase = smem0 + static_cast<uint32_t>(slot * stage_bytes);
+      const uint64_t dw = desc0 + (sbase >> 4);
+      const uint64_t dx = desc0 + ((sbase + wbytes_all) >> 4);
+      mma_stage_nb<NACC>(nb, d, dw, dx, idesc, xblk16, chain_cols, kb == pc.kb0);
       tc_commit(&empty[slot]);
+      if (++slot == a.stages) {
+        slot = 0;
+        phase ^= 1u;
+      }
     }
     tc_commit(&tfull[ab]);
     ++acc_it;
+  }
+}
+
+__device__ __forceinline__ void mma_issue(const StreamArgs& a, const Plan& p,
+                                          uint8_t* smem, int stage_bytes,
+                                          uint64_t* full, uint64_t* empty,
+                                          uint64_t* tfull, uint64_t* tempty,
+                                          uint32_t tmem_base, PieceQueue* pq) {
+  switch (a.nacc) {
+    case 4: mma_loop<4>(a, p, smem, stage_bytes, full, empty, tfull, tempty, tmem_base, pq); break;
+    case 2: mma_loop<2>(a, p, smem, stage_bytes, full, empty, tfull, tempty, tmem_base, pq); break;
+    default: mma_loop<1>(a, p, smem, stage_bytes, full, empty, tfull, tempty, tmem_base, pq);
   }
 }
 
@@ -1008,9 +1055,11 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tfull[ab], aph);
     tc_fence_after();
+    const int nacc = a.nacc > 0 ? a.nacc : 1;
+    const uint32_t astr = static_cast<uint32_t>(a.n_pad);
     const uint32_t taddr = tmem_base +
                            (static_cast<uint32_t>(quarter * 32) << 16) +
-                           static_cast<uint32_t>(ab * a.n_pad);
+                           static_cast<uint32_t>(ab * nacc * a.n_pad);
     if (!pc.down && p.split > 1) {
       s1_split_epilogue(a, p, pc.tile, taddr, row, lane, tid, red, red_full, red_free,
                         split_iter++);
@@ -1027,7 +1076,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       float* base = s1acc_at(a, pc.tile, 0) + row;
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
-        tmem_ld16(taddr + c0, v);
+        tmem_ld16_sum(taddr + c0, nacc, astr, v);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           float val = v[e];
@@ -1051,7 +1100,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       const int col = pc.tile * kS1Cols + cofs;
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
-        tmem_ld16(taddr + c0, v);
+        tmem_ld16_sum(taddr + c0, nacc, astr, v);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
@@ -1070,7 +1119,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       float* yacc = down_acc(a, pc.tile);
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
-        tmem_ld16(taddr + c0, v);
+        tmem_ld16_sum(taddr + c0, nacc, astr, v);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int n = c0 + e;
@@ -1147,7 +1196,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   uint32_t tmem_cols = 0;
   if constexpr (kTC) {
     tmem_cols = 32;
-    while (tmem_cols < static_cast<uint32_t>(2 * a.n_pad)) tmem_cols <<= 1;
+    const int nacc = a.nacc > 0 ? a.nacc : 1;
+    while (tmem_cols < static_cast<uint32_t>(2 * nacc * a.n_pad)) tmem_cols <<= 1;
     if (w == 1) tmem_alloc(tmem_slot, tmem_cols);
   }
   __syncthreads();
@@ -1333,6 +1383,8 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
   if (a.kbs < 1 || a.kbs > kMaxKbs || a.stages < 2 || a.stages > 32)
     return cudaErrorInvalidValue;
   if (a.split_k > 1 && (!tc || a.dynamic || a.split_k > 8 || grid % a.split_k != 0))
+    return cudaErrorInvalidValue;
+  if (a.nacc > 4 || (a.nacc > 1 && (a.split_k > 1 || 2 * a.nacc * a.n_pad > 512)))
     return cudaErrorInvalidValue;
   const int smem =
       stream_smem_bytes(a.n_pad, a.stages, a.kbs, mode == kModeDown ? 1 : a.split_k);

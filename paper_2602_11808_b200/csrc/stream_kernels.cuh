@@ -51,6 +51,10 @@ struct StreamArgs {
   int64_t y_ld;
   int y_bf16;
   int y_vec4;  // fp32 Y, 16-byte aligned rows: float4 stores
+  // tcgen05: independent accumulators per tile (MMA k of a K block goes to
+  // accumulator k % nacc), so consecutive MMAs do not serialise on one
+  // accumulator; the epilogue sums them.  TMEM = 2 x nacc x n_pad columns.
+  int nacc;
   int out_cols;
   // kModeBlock: per-stage-1-tile completion flags and this launch's epoch.
   unsigned* flags;

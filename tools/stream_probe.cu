@@ -13,6 +13,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "ptx.cuh"
@@ -59,6 +60,51 @@ __global__ void __launch_bounds__(64, 1)
   }
 }
 
+// Same as bulk_stream, but PDL-chained: the first ring is issued before
+// griddepcontrol.wait (as the block kernel does), dependents launch at once.
+__global__ void __launch_bounds__(64, 1)
+    bulk_stream_pdl(const uint8_t* __restrict__ src, size_t per_cta, int chunk,
+                    int stages, unsigned* sink) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(stages) * chunk);
+  uint64_t* empty = full + stages;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  const uint8_t* base = src + blockIdx.x * per_cta;
+  const long n = static_cast<long>(per_cta / chunk);
+  const uint64_t pol = policy_evict_first();
+  if (threadIdx.x == 0) {
+    for (long it = 0; it < n; ++it) {
+      const int s = static_cast<int>(it % stages);
+      const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+      if (it == stages) pdl_wait();
+      if (it >= stages) mbar_wait(&empty[s], ph ^ 1u);
+      mbar_arrive_expect_tx(&full[s], chunk);
+      bulk_g2s(smem + size_t(s) * chunk, base + it * chunk, chunk, &full[s], pol);
+    }
+    if (n <= stages) pdl_wait();
+  } else if (threadIdx.x == 32) {
+    unsigned acc = 0;
+    for (long it = 0; it < n; ++it) {
+      const int s = static_cast<int>(it % stages);
+      const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+      mbar_wait(&full[s], ph);
+      acc ^= *reinterpret_cast<volatile unsigned*>(smem + size_t(s) * chunk);
+      mbar_arrive(&empty[s]);
+    }
+    if (acc == 0x12345678u) sink[blockIdx.x] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(512) ldg_stream(const uint4* __restrict__ src,
                                                    size_t n16, unsigned* sink) {
   unsigned acc = 0;
@@ -80,6 +126,7 @@ __global__ void __launch_bounds__(512) ldg_stream(const uint4* __restrict__ src,
 
 int main(int argc, char** argv) {
   const size_t total = size_t(1) << 30;  // 1 GiB >> L2
+  const bool launch_mode = argc > 1 && std::string(argv[1]) == "launch";
   uint8_t* buf;
   unsigned* sink;
   cudaMalloc(&buf, total + (64 << 20));
@@ -107,6 +154,39 @@ int main(int argc, char** argv) {
     }
     return best;
   };
+  if (launch_mode) {
+    // Per-launch cost of a 352 MB stream (the Llama-8B block's bytes) over
+    // rotating quarter-GiB windows, 40 back-to-back launches, with and
+    // without PDL: the floor for a single-launch block of this size.
+    cudaFuncSetAttribute(bulk_stream_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    const size_t per_launch = 352321536;
+    for (int pdl : {0, 1})
+      for (int grid : {129, 148})
+        for (int chunk : {32768, 65536}) {
+          const int stages = chunk == 65536 ? 3 : 6;
+          const size_t per_cta = per_launch / grid / chunk * chunk;
+          const int smem = stages * chunk + 1024 + 16 * stages + 64;
+          auto one = [&](int i) {
+            const uint8_t* src = buf + (size_t(i % 3) * (size_t(1) << 28));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(64);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at;
+            at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at.val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = &at;
+            cfg.numAttrs = pdl;
+            cudaLaunchKernelEx(&cfg, bulk_stream_pdl, src, per_cta, chunk, stages, sink);
+          };
+          float ms = time_it([&] { for (int i = 0; i < 40; ++i) one(i); });
+          printf("launch pdl=%d grid=%3d chunk=%6d stages=%d : %7.2f us/launch  %7.1f GB/s\n",
+                 pdl, grid, chunk, stages, ms * 1e3 / 40,
+                 double(per_cta) * grid * 40 / ms / 1e6);
+        }
+    return 0;
+  }
   {
     const size_t n16 = total / 16;
     for (int blocks_per_sm : {1, 2, 4}) {
