@@ -13,9 +13,10 @@ value      = algorithmic bytes of all calls / device time (GB/s, aggregate
              over ranks); bytes per call follow the reference's fused traffic
              model (traffic.cpp:70-76, 82-94) at 2 B/element.
 e2e        = the same metric through the host-buffer C-ABI call
-             (dfk_forward_host_async: X bf16 from pinned host memory, pulled
-             over PCIe by a PDL-chained staging kernel; Y fp32 written by the
-             block straight into pinned host memory; one host sync per step).
+             (dfk_forward_host_async: X bf16 from pinned host memory, H2D on a
+             side stream gated by device flags, Y fp32 D2H on a second side
+             stream once the block's last CTA flags it; one host sync per
+             step, which waits for every copy).
 roofline   = the fused stage-1 kernel (2/3 of the bytes) timed alone with
              CUDA events on its stream, against MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline = the reference CPU path (oracle/_ref, the unmodified reference

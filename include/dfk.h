@@ -180,12 +180,14 @@ DFK_API int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
                              int32_t y_dtype, const dfk_config* cfg);
 
 /* Asynchronous host-buffer call for pipelined callers: X is bf16 in PINNED
- * host memory, Y is fp32 in PINNED host memory.  Enqueues, on the context
- * stream, a staging kernel that pulls X over PCIe into a device ring slot
- * (programmatic-dependent launch: it overlaps the previous block) and the
- * block, which writes Y straight into the pinned buffer (zero-copy); under
- * TP, H2D(X), the TP block and D2H(Y).  Buffers must stay valid until
- * dfk_context_sync. */
+ * host memory, Y is fp32 in PINNED host memory.  With the (default) dynamic
+ * block kernel the copies never sit between two blocks on the context
+ * stream: X goes H2D on a side stream into a device ring slot and publishes
+ * a device flag the block waits on; the block's last CTA publishes "Y done"
+ * and a second side stream copies Y out.  Other layouts: a PDL-chained
+ * staging kernel pulls X and Y is written to the pinned buffer directly;
+ * under TP, H2D(X), the TP block, D2H(Y) in stream order.  Buffers must stay
+ * valid until dfk_context_sync (which waits for the side streams too). */
 DFK_API int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
                                    const void* x_pinned_bf16, int64_t batch,
                                    float* y_pinned, const dfk_config* cfg);

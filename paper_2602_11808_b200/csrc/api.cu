@@ -105,6 +105,20 @@ int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 // TMA descriptors (driver entry point fetched through the runtime so the
 // library does not link libcuda directly).
 // ---------------------------------------------------------------------------
+// Stream memory operations (driver API; the host-buffer forward's side
+// stream waits on / writes 32-bit device flags).
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+template <typename Fn>
+Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<Fn>(p);
+  return nullptr;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -518,6 +532,12 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
       }
       a.yacc_ld = tp->yacc_ld;
     }
+    if (ctx->pend_x_ready && b0 == 0 && B <= L.chunk) {  // host-buffer X flags
+      a.x_ready = ctx->pend_x_ready;
+      a.x_free = ctx->pend_x_free;
+      a.y_done = ctx->pend_y_done;
+      a.x_seq = ctx->pend_x_seq;
+    }
     a.flags = static_cast<unsigned*>(ctx->flags.p);
     if (++ctx->epoch == 0) ++ctx->epoch;
     a.epoch = ctx->epoch;
@@ -862,8 +882,19 @@ int dfk_context_destroy(dfk_context ctx) {
   }
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
   ctx->graphs.clear();
-  for (HostSlot& sl : ctx->host_slots)
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+  }
+  if (ctx->out_stream) {
+    cudaStreamSynchronize(ctx->out_stream);
+    cudaStreamDestroy(ctx->out_stream);
+  }
+  for (HostSlot& sl : ctx->host_slots) {
     if (sl.x.p) cudaFree(sl.x.p);
+    if (sl.y.p) cudaFree(sl.y.p);
+  }
+  if (ctx->host_flags.p) cudaFree(ctx->host_flags.p);
   for (int r = 0; r < 8; ++r)
     if (ctx->tp_peer_ipc[r] && ctx->tp_peer[r]) cudaIpcCloseMemHandle(ctx->tp_peer[r]);
   if (ctx->tp_sym.p) cudaFree(ctx->tp_sym.p);
@@ -881,6 +912,8 @@ int dfk_context_destroy(dfk_context ctx) {
 int dfk_context_sync(dfk_context ctx) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
   DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->side_stream) DFK_CUDA(cudaStreamSynchronize(ctx->side_stream));
+  if (ctx->out_stream) DFK_CUDA(cudaStreamSynchronize(ctx->out_stream));
   return DFK_OK;
 }
 
@@ -1129,6 +1162,75 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
   if (!x_pinned_bf16 || !y_pinned) return fail(DFK_ERR_INVALID, "null host pointer");
   const size_t xb = static_cast<size_t>(batch * w->d_model) * 2;
   const size_t yb = static_cast<size_t>(batch * w->d_model) * 4;
+  dfk_config rc;
+  DFK_TRY(resolve_config(ctx, w, batch, cfg, &rc));
+  static const WaitValueFn wait_value = driver_fn<WaitValueFn>("cuStreamWaitValue32");
+  static const WriteValueFn write_value = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+  if (!tp_active(ctx) && batch <= 256 && rc.variant == DFK_VARIANT_FUSED &&
+      rc.block_kernel && rc.dynamic_sched && rc.s1_split_k <= 1 && wait_value &&
+      write_value && !env_int("DFK_HOST_STAGEK", 0)) {
+    // Copy-engine X and Y: the H2D copy runs on a side stream as soon as its
+    // ring slot is free (device flag x_free >= previous user's sequence no.)
+    // and then publishes x_ready = seq; the block kernel -- still PDL-chained
+    // to the previous block, nothing in between on the context stream --
+    // waits for x_ready before its first X load, writes Y into the slot and
+    // its last CTA publishes y_done = seq, on which the side stream's D2H
+    // waits.  Both copies are off the block chain's critical path.
+    if (!ctx->side_stream) {
+      DFK_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+      DFK_CUDA(cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
+    }
+    DFK_TRY(ensure_buf(ctx->host_flags, 3 * kHostSlots * sizeof(unsigned), true, ctx->stream));
+    const int si = ctx->host_next;
+    HostSlot& sl = ctx->host_slots[si];
+    ctx->host_next = (ctx->host_next + 1) % kHostSlots;
+    if (sl.x.bytes < xb || sl.y.bytes < yb) {
+      DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+      DFK_CUDA(cudaStreamSynchronize(ctx->side_stream));
+      DFK_CUDA(cudaStreamSynchronize(ctx->out_stream));
+      const size_t nx = std::max<size_t>({xb, 2 * sl.x.bytes, 64 * 1024});
+      const size_t ny = std::max<size_t>({yb, 2 * sl.y.bytes, 128 * 1024});
+      for (HostSlot& o : ctx->host_slots) {
+        DFK_TRY(ensure_buf(o.x, nx, false, ctx->stream));
+        DFK_TRY(ensure_buf(o.y, ny, false, ctx->stream));
+      }
+      DFK_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    auto* flags = static_cast<unsigned*>(ctx->host_flags.p);
+    unsigned* x_ready = flags + si;
+    unsigned* x_free = flags + kHostSlots + si;
+    unsigned* y_done = flags + 2 * kHostSlots + si;
+    const unsigned seq = ++ctx->host_seq;
+    if (seq > static_cast<unsigned>(kHostSlots)) {  // the slot's previous user is done
+      if (wait_value(ctx->side_stream, reinterpret_cast<CUdeviceptr>(x_free),
+                     seq - kHostSlots, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(DFK_ERR_CUDA, "cuStreamWaitValue32 failed");
+    }
+    DFK_CUDA(cudaMemcpyAsync(sl.x.p, x_pinned_bf16, xb, cudaMemcpyHostToDevice,
+                             ctx->side_stream));
+    if (write_value(ctx->side_stream, reinterpret_cast<CUdeviceptr>(x_ready), seq,
+                    CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(DFK_ERR_CUDA, "cuStreamWriteValue32 failed");
+    ctx->pend_x_ready = x_ready;
+    ctx->pend_x_free = x_free;
+    ctx->pend_y_done = y_done;
+    ctx->pend_x_seq = seq;
+    const int st = forward_impl(ctx, w, sl.x.p, batch, sl.y.p, DFK_F32, &rc);
+    ctx->pend_x_ready = nullptr;
+    ctx->pend_x_free = nullptr;
+    ctx->pend_y_done = nullptr;
+    DFK_TRY(st);
+    // Y leaves on its own stream, so that the next X copies never queue
+    // behind this block's completion.  (x_free is published with y_done, so
+    // the slot's Y is not overwritten before this copy: the next user's X
+    // copy waits for x_free, its block for that X.)
+    if (wait_value(ctx->out_stream, reinterpret_cast<CUdeviceptr>(y_done), seq,
+                   CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+      return fail(DFK_ERR_CUDA, "cuStreamWaitValue32 failed");
+    DFK_CUDA(cudaMemcpyAsync(y_pinned, sl.y.p, yb, cudaMemcpyDeviceToHost,
+                             ctx->out_stream));
+    return DFK_OK;
+  }
   if (!tp_active(ctx) && xb % 16 == 0) {
     // Zero-copy chain: a staging kernel pulls X over PCIe into a ring slot
     // (PDL: overlapping the previous block), the block writes Y straight

@@ -49,7 +49,7 @@ struct DeviceBuf {
 
 // One X staging slot of the host-buffer forward (dfk_forward_host_async).
 struct HostSlot {
-  DeviceBuf x;
+  DeviceBuf x, y;
 };
 constexpr int kHostSlots = 8;
 
@@ -93,6 +93,17 @@ struct dfk_context_s {
   dfk::DeviceBuf hx_dev, hy_dev;  // forward_host device staging
   dfk::HostSlot host_slots[dfk::kHostSlots];
   int host_next = 0;
+  // Copy-engine X path of the host-buffer forward: side stream, per-slot
+  // device flags (x_ready / x_free, uint32 [kHostSlots] each), sequence no.,
+  // and the flags of the call being launched (consumed by block_fused).
+  cudaStream_t side_stream = nullptr;   // X H2D copies
+  cudaStream_t out_stream = nullptr;    // Y D2H copies
+  dfk::DeviceBuf host_flags;
+  unsigned host_seq = 0;
+  const unsigned* pend_x_ready = nullptr;
+  unsigned* pend_x_free = nullptr;
+  unsigned* pend_y_done = nullptr;
+  unsigned pend_x_seq = 0;
   void* hx_pinned = nullptr;
   size_t hx_pinned_bytes = 0;
   void* hy_pinned = nullptr;

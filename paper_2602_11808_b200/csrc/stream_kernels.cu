@@ -609,7 +609,17 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
   int64_t it = 0;
   bool waited = false;
   PieceIter pi;
+  bool x_ok = a.x_ready == nullptr;
   auto act_loads = [&](uint8_t* xs, int kb, int nb, int down, uint64_t* bar) {
+    if (!down && !x_ok) {  // (whole warp) the side stream's X copy landed?
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+      while (static_cast<int>(ld_acquire_sys(reinterpret_cast<const int*>(a.x_ready)) -
+                              static_cast<int>(a.x_seq)) < 0)
+        tp_spin_check(a, t0);
+      fence_proxy_async_global();
+      x_ok = true;
+    }
     if (!leader) return;
     for (int b = 0; b < nb; ++b) {
       tma_load_2d(xs + b * xblk, down ? amap : xmap, (kb + b) * kBlockK, 0, bar);
@@ -1233,6 +1243,11 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     // rank's Y has been written (by whichever rank finished it).
     __threadfence();
     if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      if (a.x_free) {  // device-scope release: read by stream waits / copy engines
+        __threadfence();
+        st_release(a.x_free, a.x_seq);
+        if (a.y_done) st_release(a.y_done, a.x_seq);
+      }
       if (kMode == kModeBlock && a.tp_size > 1) {
         int* done = a.tp_done[a.tp_rank];
         unsigned long long t0;

@@ -55,6 +55,14 @@ struct StreamArgs {
   // accumulator k % nacc), so consecutive MMAs do not serialise on one
   // accumulator; the epilogue sums them.  TMEM = 2 x nacc x n_pad columns.
   int nacc;
+  // Host-buffer path (dfk_forward_host_async): X arrives by a copy-engine
+  // memcpy on a side stream, which then writes x_seq to *x_ready; the
+  // producer waits for it before the first activation load, and the last CTA
+  // out stores x_seq to *x_free (the staging slot may be overwritten).
+  const unsigned* x_ready;
+  unsigned* x_free;
+  unsigned* y_done;  // x_seq stored here too: Y complete, the side stream copies it out
+  unsigned x_seq;
   int out_cols;
   // kModeBlock: per-stage-1-tile completion flags and this launch's epoch.
   unsigned* flags;
