@@ -537,3 +537,29 @@ def test_tp_fused_decode_graph_emulated_ranks(rt, oracle_lib):
     finally:
         for c in ctxs:
             c.close()
+
+
+def test_forward_host_async_ring_wraps(rt, ctx, oracle_lib):
+    """25 queued host-buffer calls (> the 8-slot staging ring, batch sizes
+    rotating so slots grow mid-stream), one sync: every call's Y matches the
+    oracle -- the side-stream X/Y copies and the device flags that order them
+    against the blocks (x_ready / x_free / y_done) never reuse a slot early."""
+    from paper_2602_11808_b200.runtime import PinnedHost, to_bf16_bits
+    dm, df = 256, 640
+    x0, wu, wg, wd = instance(oracle_lib, 70, 40, dm, df)
+    w = ctx.weights(wg, wu, wd)
+    calls = []
+    for i in range(25):
+        B = (1, 5, 33, 2, 40)[i % 5]
+        x = x0[:B] * (1.0 + 0.01 * i)
+        x = oracle_lib.quantize_bf16(x)[0]
+        px = PinnedHost((B, dm), np.uint16)
+        px.arr[...] = to_bf16_bits(x)
+        py = PinnedHost((B, dm), np.float32)
+        calls.append((x, px, py))
+    for x, px, py in calls:
+        ctx.forward_host_async(w, px.arr, py.arr)
+    ctx.sync()
+    for i, (x, px, py) in enumerate(calls):
+        _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+        assert rel_err(py.arr, y_ref) <= TOL, i
