@@ -257,7 +257,18 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   // ~1.5 pieces per CTA -- but never under max(4, N/4) K blocks: every piece
   // ends in 128 x N fp32 red.adds, which at large N cost more than the
   // extra balance buys (tools/tp_shard_sweep.py, profiles/r1b_tp_shards.md).
+  // At N <= 16 smaller chunks (~16 K blocks, a divisor of the K-block count
+  // when one exists) balance the drain better: -1 to -2 % at B = 1..16; at
+  // N >= 32 the per-piece red.adds favour 32 (chunk sweep, r1b_tuning.md).
   int chunk = std::min(w->dn_kblocks, 32);
+  if (a->n_pad <= 16 && w->dn_kblocks > 16) {
+    chunk = 16;
+    for (int c = 16; c >= 12; --c)
+      if (w->dn_kblocks % c == 0) {
+        chunk = c;
+        break;
+      }
+  }
   const int64_t pieces = static_cast<int64_t>(w->dn_tiles) *
                          ((w->dn_kblocks + chunk - 1) / chunk);
   if (pieces * 2 < 3LL * grid) {
