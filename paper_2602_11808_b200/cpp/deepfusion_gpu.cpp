@@ -500,13 +500,19 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
   int ndev = 0;
   dfk_device_count(&ndev);
   const auto xb = to_bf16(x);
-  if (plan.num_devices > 1 && plan.num_devices <= ndev) {
-    // Real multi-GPU: one context per device, ncclCommInitAll, one
-    // ncclAllReduce of the fp32 partials.
+  if (plan.num_devices > 1 && plan.num_devices <= 8 && dm % 4 == 0 && B <= 256) {
+    // One context per rank -- on its own device when there are enough, else
+    // all on device 0 (each rank's block on its own stream) -- with the
+    // fused all-reduce: partial Y reduced over peer memory INSIDE the block
+    // kernel (dfk_tp_forward_fused), the block's one collective
+    // (tp.cpp:140-167).  Every buffer exists before the first launch.
+    const bool multi = plan.num_devices <= ndev;
     std::vector<dfk_context> ctxs(static_cast<size_t>(plan.num_devices));
     for (Index p = 0; p < plan.num_devices; ++p)
-      check(dfk_context_create(static_cast<int>(p), nullptr, &ctxs[static_cast<size_t>(p)]));
-    check(dfk_tp_init_all(ctxs.data(), static_cast<int>(plan.num_devices)));
+      check(dfk_context_create(multi ? static_cast<int>(p) : 0, nullptr,
+                               &ctxs[static_cast<size_t>(p)]));
+    for (dfk_context c : ctxs) check(dfk_tp_sym_create(c, B, dm, nullptr));
+    check(dfk_tp_sym_attach(ctxs.data(), static_cast<int>(plan.num_devices)));
     std::vector<dfk_weights> hs;
     std::vector<void*> xs, ys, as;
     for (Index p = 0; p < plan.num_devices; ++p) {
@@ -525,24 +531,19 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
       ys.push_back(yp);
       as.push_back(ap);
     }
-    // Stage-1 shards (for TpResult::stage1_shards), then the block with its
-    // single all-reduce; one thread drives every rank, so the NCCL calls are
-    // grouped.
-    for (Index p = 0; p < plan.num_devices; ++p)
+    // Stage-1 shards (for TpResult::stage1_shards), synchronised, then the
+    // fused blocks issued back to back on the ranks' streams.
+    for (Index p = 0; p < plan.num_devices; ++p) {
       check(dfk_stage1(ctxs[static_cast<size_t>(p)], hs[static_cast<size_t>(p)],
                        xs[static_cast<size_t>(p)], B, as[static_cast<size_t>(p)], cfg));
-    check(dfk_tp_group_start());
-    for (Index p = 0; p < plan.num_devices; ++p) {
-      const int st = dfk_tp_forward(ctxs[static_cast<size_t>(p)], hs[static_cast<size_t>(p)],
-                                    xs[static_cast<size_t>(p)], B,
-                                    static_cast<float*>(ys[static_cast<size_t>(p)]), cfg);
-      if (st != DFK_OK) {
-        dfk_tp_group_end();
-        raise(st);
-      }
+      check(dfk_context_sync(ctxs[static_cast<size_t>(p)]));
     }
-    check(dfk_tp_group_end());
+    for (Index p = 0; p < plan.num_devices; ++p)
+      check(dfk_tp_forward_fused(ctxs[static_cast<size_t>(p)], hs[static_cast<size_t>(p)],
+                                 xs[static_cast<size_t>(p)], B,
+                                 static_cast<float*>(ys[static_cast<size_t>(p)]), cfg));
     std::vector<float> out(static_cast<size_t>(B * dm));
+    for (Index p = 0; p < plan.num_devices; ++p) check(dfk_context_sync(ctxs[static_cast<size_t>(p)]));
     for (Index p = 0; p < plan.num_devices; ++p) {
       dfk_context c = ctxs[static_cast<size_t>(p)];
       const ColRange r = plan.ff_ranges[static_cast<size_t>(p)];
@@ -564,7 +565,9 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
       dfk_context_destroy(c);
     }
   } else {
-    // One GPU: shards in sequence, fp32 partials summed in device order.
+    // Shapes the fused all-reduce does not take (d_model % 4, B > 256, more
+    // than 8 ranks): shards in sequence on one GPU, fp32 partials summed in
+    // device order.
     dfk_context c = rt().context(0);
     DevBuf xd(c, xb.size() * 2), yd(c, static_cast<size_t>(B * dm) * 4);
     check(dfk_memcpy_h2d(c, xd.p, xb.data(), xb.size() * 2));

@@ -223,6 +223,20 @@ TEST_CASE("TP equivalence across device counts, one all-reduce", t_tp) {
   CHECK(col == 7);
 }
 
+// The same equivalence on a shape the fused all-reduce takes (d_model % 4
+// == 0): run_tp_mlp's ranks reduce partial Y over peer memory inside the
+// block kernel (P contexts on one GPU when fewer devices are visible).
+TEST_CASE("TP equivalence with the in-kernel all-reduce", t_tp_fused) {
+  Instance inst = random_instance({5, 256, 900}, 79);
+  const Matrix expected = oracle_forward(inst.x, inst.w);
+  for (Index p : {2, 3, 4, 8}) {
+    const TpResult r = run_tp_mlp(inst.x, inst.w, make_plan(900, p), {VariantTag::Fused, {}, "tp"});
+    CHECK(rel_err(r.output, expected) <= 1e-2);
+    CHECK(r.log.events.size() == 1);
+    CHECK(static_cast<Index>(r.stage1_shards.size()) == p);
+  }
+}
+
 // test_tp.cpp:39-58, tp.cpp:8-29
 TEST_CASE("make_plan splits evenly and spreads the remainder", t_plan) {
   const ShardPlan even = make_plan(8, 4);
