@@ -363,7 +363,9 @@ def main():
     n_rep = max(args.steps, 10)
     us = {B: time_calls(B, cfgs[B], n_rep) for B in sweep}
     two = rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)
-    us_unfused = {B: time_calls(B, two, n_rep) for B in sweep}
+    # unfused = cuBLASLt two-kernel layout (+ NCCL's all-reduce under TP; the
+    # fused TP path always runs the block kernel)
+    us_unfused = {B: time_calls(B, two, n_rep, nccl_call if P > 1 else None) for B in sweep}
     # TP: the same block with NCCL's all-reduce as a separate collective.
     us_nccl = ({B: time_calls(B, cfgs[B], n_rep, nccl_call) for B in sweep}
                if tp_mode == "fused-nvlink" else None)
