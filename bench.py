@@ -241,6 +241,8 @@ def main():
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--tp-emulate", action="store_true",
+                    help="test aid: ranks share the visible GPUs (rank %% count), no NCCL")
     ap.add_argument("--sweep", default=",".join(map(str, SWEEP)))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -264,13 +266,15 @@ def main():
     from paper_2602_11808_b200 import tp_host
 
     P = world
-    ctx = rt.Context(local_rank)
+    dev = local_rank % rt.device_count() if args.tp_emulate else local_rank
+    ctx = rt.Context(dev)
     tp_mode = None
     if P > 1:
         # NCCL (the unfused-collective comparator) and the fused all-reduce's
         # symmetric workspaces over NVLink peer memory (used when every rank
         # can map its peers).
-        ctx.tp_init(tp_host.exchange_uid(dist, rank), rank, P)
+        if not args.tp_emulate:
+            ctx.tp_init(tp_host.exchange_uid(dist, rank), rank, P)
         sweep_max = max(int(b) for b in args.sweep.split(","))
         tp_mode = ("fused-nvlink" if tp_host.setup_fused(dist, ctx, rank, P, sweep_max, DM)
                    else "nccl")
@@ -326,7 +330,7 @@ def main():
     # Clocks are sampled from the warm-up through the per-batch timings (all
     # under kernel load): the headline region alone is shorter than the
     # sampling period at small --steps.
-    clk = ClockSampler(local_rank).__enter__()
+    clk = ClockSampler(dev).__enter__()
     for k in range(args.warmup):
         step(k)
     ctx.sync()
@@ -365,10 +369,12 @@ def main():
     two = rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)
     # unfused = cuBLASLt two-kernel layout (+ NCCL's all-reduce under TP; the
     # fused TP path always runs the block kernel)
-    us_unfused = {B: time_calls(B, two, n_rep, nccl_call if P > 1 else None) for B in sweep}
+    nccl_ok = P > 1 and not args.tp_emulate
+    us_unfused = ({B: time_calls(B, two, n_rep, nccl_call if P > 1 else None) for B in sweep}
+                  if P == 1 or nccl_ok else {B: float("nan") for B in sweep})
     # TP: the same block with NCCL's all-reduce as a separate collective.
     us_nccl = ({B: time_calls(B, cfgs[B], n_rep, nccl_call) for B in sweep}
-               if tp_mode == "fused-nvlink" else None)
+               if tp_mode == "fused-nvlink" and nccl_ok else None)
 
     # ---- roofline: the dominant kernel alone ----
     # Block kernel chosen -> the whole block is one launch; otherwise the fused
