@@ -107,3 +107,19 @@ def test_mirror_api_validation_without_gpu():
     log = df.CollectiveLog([df.CollectiveEvent(df.CollectiveKind.AllReduce, 4096)])
     assert df.comm_volume_bytes(log, 4, df.CommModel.Logical) == 8192
     assert df.comm_volume_bytes(log, 4, df.CommModel.Ring) == pytest.approx(2 * 3 / 4 * 8192)
+
+
+def test_tune_front_end_usage_errors_exit_2():
+    """The `tune` front end keeps the reference CLI's exit contract
+    (main.cpp:377-389): usage errors -> 2 (checked without a GPU: argument
+    validation happens before any device work)."""
+    from paper_2602_11808_b200 import tune
+    assert tune.main(["--batch", "1,x"]) == 2
+    assert tune.main(["--no-such-flag"]) == 2
+    assert tune.resolve_cache_path("a.json") == "a.json"
+    os.environ["DEEPFUSION_CACHE"] = "env.json"
+    try:
+        assert tune.resolve_cache_path("") == "env.json"
+    finally:
+        del os.environ["DEEPFUSION_CACHE"]
+    assert tune.resolve_cache_path("") == "deepfusion_cache.json"

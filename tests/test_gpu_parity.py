@@ -563,3 +563,19 @@ def test_forward_host_async_ring_wraps(rt, ctx, oracle_lib):
     for i, (x, px, py) in enumerate(calls):
         _, y_ref = oracle_lib.forward(x, wu, wg, wd)
         assert rel_err(py.arr, y_ref) <= TOL, i
+
+
+def test_tune_front_end_cache_round_trip(tmp_path, capsys):
+    """`python -m paper_2602_11808_b200.tune` (the reference's `deepfusion
+    tune`, main.cpp:210-236): profiles, persists, and the second run is a
+    cache hit for every batch."""
+    from paper_2602_11808_b200 import tune
+    cache = str(tmp_path / "c.json")
+    args = ["--d-model", "512", "--d-ff", "1792", "--batch", "1,4", "--runs", "3",
+            "--cache-path", cache]
+    assert tune.main(args) == 0
+    out1 = capsys.readouterr().out
+    assert out1.count("(profiled)") == 2 and f"cache: {cache}" in out1
+    assert tune.main(args) == 0
+    out2 = capsys.readouterr().out
+    assert out2.count("(cache hit, profiling skipped)") == 2
