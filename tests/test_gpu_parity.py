@@ -579,3 +579,29 @@ def test_tune_front_end_cache_round_trip(tmp_path, capsys):
     assert tune.main(args) == 0
     out2 = capsys.readouterr().out
     assert out2.count("(cache hit, profiling skipped)") == 2
+
+
+def test_weight_layouts_pack_identically(rt, ctx, oracle_lib):
+    """dfk_weights_create accepts the reference layout as fp64 / fp32 / bf16,
+    host or device (swiglu.hpp:49-57 MlpWeights, converted RNE to bf16): every
+    combination packs the same bf16 weights, so stage 1 is bit-identical."""
+    from paper_2602_11808_b200.runtime import to_bf16_bits
+    B, dm, df = 3, 200, 330
+    x, wu, wg, wd = instance(oracle_lib, 95, B, dm, df)  # bf16-exact values
+    xd = ctx.array((B, dm)).upload(x)
+    variants = {
+        "f64 host": (wg, wu, wd),
+        "f32 host": tuple(a.astype(np.float32) for a in (wg, wu, wd)),
+        "bf16 host": tuple(to_bf16_bits(a) for a in (wg, wu, wd)),
+        "bf16 device": tuple(ctx.array(a.shape).upload(a) for a in (wg, wu, wd)),
+        "f32 device": tuple(ctx.array(a.shape, rt.F32).upload(a) for a in (wg, wu, wd)),
+    }
+    outs = {}
+    for name, (g, u, d) in variants.items():
+        w = ctx.weights(g, u, d)
+        a2 = ctx.array((B, df))
+        ctx.stage1(w, xd, a2, cfg=rt.Config.make(block_kernel=0))
+        outs[name] = a2.download_bits()
+    ref = outs["f64 host"]
+    for name, bits in outs.items():
+        assert np.array_equal(bits, ref), name
