@@ -272,10 +272,12 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   const int64_t pieces = static_cast<int64_t>(w->dn_tiles) *
                          ((w->dn_kblocks + chunk - 1) / chunk);
   if (pieces * 2 < 3LL * grid) {
-    const int per_tile =
-        std::max(1, (3 * grid + 2 * w->dn_tiles - 1) / (2 * w->dn_tiles));
-    chunk = std::max(std::min(std::max(4, a->n_pad / 4), w->dn_kblocks),
-                     (w->dn_kblocks + per_tile - 1) / per_tile);
+    // ~one down piece per CTA (every piece ends in 128 x N fp32 red.adds:
+    // more, smaller pieces lose at N >= 16; sweep of the TP shards,
+    // profiles/r1b_tp_shards.md)
+    const int per_tile = std::max(
+        1, static_cast<int>(std::lround(static_cast<double>(grid) / w->dn_tiles)));
+    chunk = std::max(std::min(4, w->dn_kblocks), (w->dn_kblocks + per_tile - 1) / per_tile);
   }
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
   // Stage-1 stream-K: a shard with fewer stage-1 tiles than CTAs splits
@@ -285,13 +287,12 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   if (cfg.s1_chunk_kb > 0) {
     s1c = std::min(cfg.s1_chunk_kb, w->s1_kblocks);
   } else if (w->s1_tiles < grid) {
-    // About 1.3 stage-1 pieces per CTA (rounded to whole pieces per tile),
-    // each >= 256 KiB (16 K blocks; 512 KiB at N > 16, where the 128 x N
-    // partial-sum red.adds per piece cost more) -- the best of a chunk-size
-    // sweep over the TP shards of SURVEY §8e (profiles/r1b_tp_shards.md).
+    // About 0.87 stage-1 pieces per CTA (rounded to whole pieces per tile),
+    // each >= 256 KiB (16 K blocks): the best of chunk-size sweeps over the
+    // TP shards of SURVEY §8e at B = 1, 16, 64 (profiles/r1b_tp_shards.md).
     const int per_tile =
-        std::max(1, static_cast<int>(std::lround(1.3 * grid / w->s1_tiles)));
-    const int min_kb = a->n_pad > 16 ? 32 : 16;
+        std::max(1, static_cast<int>(std::lround(0.87 * grid / w->s1_tiles)));
+    const int min_kb = 16;
     s1c = std::max(std::min(min_kb, w->s1_kblocks),
                    (w->s1_kblocks + per_tile - 1) / per_tile);
   }
