@@ -605,3 +605,27 @@ def test_weight_layouts_pack_identically(rt, ctx, oracle_lib):
     ref = outs["f64 host"]
     for name, bits in outs.items():
         assert np.array_equal(bits, ref), name
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,B,dm,df", [
+    ("qwen2.5-7b", 1, 3584, 18944), ("qwen2.5-7b", 16, 3584, 18944),
+    ("qwen2.5-32b tp8 shard", 64, 5120, 3456), ("qwen2.5-32b tp8 shard", 2, 5120, 3456),
+    ("llama-3.1-70b tp8 shard", 1, 8192, 3584), ("llama-3.1-70b tp8 shard", 32, 8192, 3584),
+    ("llama-3.1-70b tp2 shard", 8, 8192, 14336)])
+def test_baseline_config_shapes_parity(rt, ctx, oracle_lib, name, B, dm, df):
+    """BASELINE.json configs 3-5 at full size (a TP rank's block is the block
+    of its d_ff shard, balanced_ranges tp.cpp:8-29): the library default
+    (dynamic block kernel; stage-1 stream-K on the small shards) vs the fp64
+    oracle on identical bf16 inputs, plus the tuned-candidate layouts that
+    the scheduler may pick for these shards."""
+    x, wu, wg, wd = instance(oracle_lib, 20260809 + B, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    for cfg in (None, rt.Config.make(block_kernel=1, dynamic_sched=1, s1_chunk_kb=16, chunk_kb=8),
+                rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)):
+        xd = ctx.array((B, dm)).upload(x)
+        y = ctx.array((B, dm), rt.F32)
+        ctx.forward(w, xd, y, cfg=cfg)
+        err = rel_err(y.download(), y_ref)
+        assert err <= TOL, (name, B, cfg.label if cfg else "default", err)
