@@ -339,6 +339,10 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   a->kb2 = w->dn_kblocks;
   a->B = static_cast<int>(nb);
   a->n_pad = n_pad;
+  // Activation rows a TMA box brings in: at B <= 8 only the first 8-row
+  // swizzle atom of the N=16 operand (rows 8-15 of the smem tile are left
+  // as they are: they only feed accumulator columns >= B, never stored).
+  a->xrows = (tc && nb <= 8 && env_int("DFK_XROWS8", 1)) ? 8 : n_pad;
   const int sk = a->split_k > 1 ? a->split_k : 1;
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk);
   a->trace = ctx->trace;
@@ -391,7 +395,7 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap tm;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
-                     w->d_model, nb, x_ld, a.n_pad, &tm));
+                     w->d_model, nb, x_ld, a.xrows, &tm));
     a.a2 = a2 + b0 * a2_ld;
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
@@ -442,7 +446,7 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     fill_common(ctx, w, nb, L.tc, cfg.down_stages, cfg, &a);
     CUtensorMap tm;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
-                     w->d_ff, nb, a_ld, a.n_pad, &tm));
+                     w->d_ff, nb, a_ld, a.xrows, &tm));
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
     // Default: 3/4 of the SMs with deep rings streams faster than every SM
@@ -525,8 +529,8 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap xm, am;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
-                     w->d_model, nb, x_ld, a.n_pad, &xm));
-    DFK_TRY(get_tmap(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.n_pad, &am));
+                     w->d_model, nb, x_ld, a.xrows, &xm));
+    DFK_TRY(get_tmap(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.xrows, &am));
     a.a2 = a2 + b0 * a2_ld;
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);

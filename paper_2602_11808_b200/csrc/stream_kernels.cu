@@ -699,7 +699,8 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
       if (leader) {
         mbar_arrive_expect_tx(&full[slot],
-                              static_cast<uint32_t>(nb) * (kBlockBytes + xblk));
+                              static_cast<uint32_t>(nb) *
+                                  (kBlockBytes + static_cast<uint32_t>(a.xrows) * 128u));
         // nb consecutive K blocks of one tile are contiguous in the pack.
         bulk_g2s(st,
                  wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *

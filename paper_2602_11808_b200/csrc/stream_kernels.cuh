@@ -29,6 +29,7 @@ struct StreamArgs {
   int t2, kb2;
   int B;       // batch rows present
   int n_pad;   // MMA N (tcgen05) / activation box rows (GEMV)
+  int xrows;   // rows per activation TMA box (<= n_pad; the smem tile is n_pad rows)
   int stages;  // ring depth
   // split_k (field below) > 1: stage-1 tiles are split along K over the
   // split_k CTAs of a thread-block cluster; partial gate/up accumulators are
