@@ -629,3 +629,50 @@ def test_baseline_config_shapes_parity(rt, ctx, oracle_lib, name, B, dm, df):
         ctx.forward(w, xd, y, cfg=cfg)
         err = rel_err(y.download(), y_ref)
         assert err <= TOL, (name, B, cfg.label if cfg else "default", err)
+
+
+@pytest.mark.parametrize("B", [255, 256, 257, 300])
+def test_batch_chunk_boundaries(rt, ctx, oracle_lib, B):
+    """Batches at and beyond one launch's 256 rows (the tcgen05 path splits
+    the batch into 256-row launches): parity for the default block kernel,
+    the two-kernel fused path and the TP-shard path."""
+    dm, df = 256, 768
+    x, wu, wg, wd = instance(oracle_lib, 600 + B, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    for cfg in (None, rt.Config.make(), rt.Config.make(block_kernel=1)):
+        a2, y1, y2 = run_gpu(rt, ctx, w, x, cfg)
+        assert rel_err(a2, a2_ref) <= TOL and rel_err(y1, y_ref) <= TOL, B
+        assert rel_err(y2, y_ref) <= TOL, B
+
+
+def test_contexts_on_two_host_threads(rt, oracle_lib):
+    """One context per host thread (the reference's functions are reentrant
+    on distinct outputs): two threads issue blocks concurrently
+    on their own contexts and both match the oracle."""
+    import threading
+    dm, df = 384, 1024
+    res = {}
+
+    def work(tid):
+        c = rt.Context(0)
+        try:
+            x, wu, wg, wd = instance(oracle_lib, 700 + tid, 5, dm, df)
+            _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+            w = c.weights(wg, wu, wd)
+            xd = c.array((5, dm)).upload(x)
+            y = c.array((5, dm), rt.F32)
+            errs = []
+            for _ in range(20):
+                c.forward(w, xd, y)
+            errs.append(rel_err(y.download(), y_ref))
+            res[tid] = max(errs)
+        finally:
+            c.close()
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert len(res) == 2 and all(v <= TOL for v in res.values()), res
