@@ -107,11 +107,17 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx,
   };
   for (int f : fams) {
     add(make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1));
-    dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, 0, 1, 1);
-    d.dynamic_sched = 1;
-    std::snprintf(d.label, sizeof(d.label), "%s", "");
-    std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
-    add(d);
+    // the dynamic block kernel at the library's stage size and, for the
+    // tcgen05 family, the two next-smaller stage sizes (K blocks per stage
+    // x ring depth: the "stage count" dimension of the search)
+    for (int kbs : {0, 3, 2}) {
+      if (kbs && f != DFK_FAMILY_TC) continue;
+      dfk_config d = make_cfg(DFK_VARIANT_FUSED, f, f, kbs, 1, 1);
+      d.dynamic_sched = 1;
+      std::snprintf(d.label, sizeof(d.label), "%s", "");
+      std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
+      add(d);
+    }
   }
   const int dn_ctas[2] = {0, ctx->sm_count};  // 0 = library default (3/4 SMs)
   for (int s1f : fams)
