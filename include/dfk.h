@@ -21,10 +21,19 @@
  *   run_four_kernel / run_two_kernel  swiglu.hpp:64-76        -> dfk_forward
  *                                       (DFK_VARIANT_FOUR/TWO_KERNEL)
  *   MlpWeights (+validate)  swiglu.hpp:49-57, swiglu.cpp:26-39 -> dfk_weights_create
- *   make_plan / run_tp_mlp  tp.hpp:54-79                      -> dfk_tp_init*,
- *                                                               dfk_tp_forward,
+ *   make_plan / run_tp_mlp  tp.hpp:54-79                      -> dfk_tp_sym_create /
+ *                                                               _open / _attach +
+ *                                                               dfk_tp_forward_fused
+ *                                                               (all-reduce in the
+ *                                                               kernel), or
+ *                                                               dfk_tp_init* +
+ *                                                               dfk_tp_forward (NCCL),
  *                                                               dfk_weights_create
  *                                                               (ff_begin/ff_end)
+ *   simulated_all_reduce    tp.cpp:90-105                     -> the fused all-reduce
+ *   time_decode_seconds     bench.cpp:98-115                  -> dfk_decode
+ *   forward with host Matrix (the shim's run_fused)           -> dfk_forward_host,
+ *                                                               dfk_forward_host_async
  *   balanced_ranges         tp.hpp:36, tp.cpp:8-29            -> dfk_balanced_range
  *   profile / select / Tuner::get_or_tune  tuner.hpp:103-137  -> dfk_tune
  *   cache_store / cache_lookup  tuner.hpp:102-113              -> dfk_tune (cache_path)
