@@ -25,6 +25,10 @@ cpu_baseline = the reference CPU path (oracle/_ref, the unmodified reference
 N>1 (torchrun): tensor parallel over NCCL, one rank per GPU — every rank holds
 the balanced_ranges(d_ff, N) shard and the block ends in one ncclAllReduce.
 
+Extra keys: decode_loop (configs[2]: Qwen2.5-7B, 4-layer x<-Y decode loop,
+CUDA graph) and tp_rank_blocks (configs[3]/[4]: the per-rank block of the
+Qwen2.5-32B / Llama-3.1-70B tensor-parallel shards, on this one GPU).
+
 --impl reference: the reference's own CPU implementation of the path
 (oracle/_ref/libdeepfusion_ref.so: run_fused with a single covering
 column-major tile and all host threads) on rank 0, same metric/unit.
@@ -230,6 +234,51 @@ def decode_loop(rt, ctx, ev0, ev1, layers=4, steps=8, sweep=(1, 2, 4, 8, 16, 32)
     return out
 
 
+# --- configs 4/5: the per-rank block of the tensor-parallel configs ------------
+TP_SHAPES = (("Qwen2.5-32B", 5120, 27648, (1, 2, 4, 8)),
+             ("Llama-3.1-70B", 8192, 28672, (2, 4, 8)))
+
+
+def tp_shards(rt, ctx, ev0, ev1, batches=(1, 16, 64), reps=20):
+    """BASELINE configs[3] / [4] on ONE GPU: a rank of TP=P runs the block of
+    its balanced_ranges(d_ff, P) shard (tp.cpp:8-29), so its kernel time is
+    that block's time (the all-reduce, fused in the kernel at N > 1, is not in
+    this number).  Library default config; weight sets rotated beyond 3x L2."""
+    import math
+    out = {}
+    for name, dm, df, Ps in TP_SHAPES:
+        for P in Ps:
+            b0, b1 = rt.balanced_range(df, P, 0)
+            dfs = b1 - b0
+            nsets = max(2, math.ceil(3 * 126e6 / (3 * dm * dfs * 2)))
+            s = 1.0 / np.sqrt(dm)
+            ws = []
+            for i in range(nsets):
+                g = ctx.array((dm, dfs)).fill_uniform(9000 + 3 * i, -s, s)
+                u = ctx.array((dm, dfs)).fill_uniform(9001 + 3 * i, -s, s)
+                d = ctx.array((dfs, dm)).fill_uniform(9002 + 3 * i, -s, s)
+                ws.append(ctx.weights(g, u, d))
+                del g, u, d
+            row = {}
+            for B in batches:
+                x = ctx.array((B, dm)).fill_uniform(31 + B)
+                y = ctx.array((B, dm), rt.F32)
+                for i in range(4):
+                    ctx.forward(ws[i % nsets], x, y)
+                ctx.sync()
+                ev0.record(ctx)
+                for i in range(reps):
+                    ctx.forward(ws[i % nsets], x, y)
+                ev1.record(ctx)
+                ctx.sync()
+                us = ev0.elapsed_ms(ev1) * 1e3 / reps
+                gbs = block_bytes(B, dm, dfs) / (us * 1e-6) / 1e9
+                row[str(B)] = {"us": round(us, 2), "gbs": round(gbs, 1)}
+            out[f"{name} tp{P}"] = {"d_model": dm, "d_ff_shard": dfs, "per_batch": row}
+            del ws
+    return out
+
+
 # --- GPU arm -----------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -241,6 +290,7 @@ def main():
     ap.add_argument("--no-tune", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-tp-shards", action="store_true")
     ap.add_argument("--tp-emulate", action="store_true",
                     help="test aid: ranks share the visible GPUs (rank %% count), no NCCL")
     ap.add_argument("--sweep", default=",".join(map(str, SWEEP)))
@@ -444,6 +494,9 @@ def main():
     decode = None
     if P == 1 and not args.no_decode:
         decode = decode_loop(rt, ctx, ev0, ev1)
+    shards = None
+    if P == 1 and not args.no_tp_shards:
+        shards = tp_shards(rt, ctx, ev0, ev1)
 
     # ---- CPU baseline: reference path, rank 0, N=1 only ----
     cpu = None
@@ -492,6 +545,7 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "decode_loop": decode,
+            "tp_rank_blocks": shards,
         }
         print(json.dumps(line), flush=True)
     barrier()
