@@ -60,6 +60,31 @@ def block_bytes(B, dm, df, P=1):
     return 2 * (3 * dm * df // P + 2 * B * dm + 2 * B * df // P)
 
 
+def stream_floor():
+    """The bare cp.async.bulk stream of one Llama-8B block's bytes per launch,
+    PDL-chained, on this GPU (tools/stream_probe launch): the best a single
+    launch of this size streams -- context for roofline.frac, whose peak is
+    MEASURED_PEAKS.json's copy bandwidth."""
+    exe = os.path.join(ROOT, "tools", "stream_probe")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, "launch"], capture_output=True, text=True,
+                             timeout=60).stdout
+    except Exception:  # noqa: BLE001
+        return None
+    best = None
+    for ln in out.splitlines():
+        if ln.startswith("launch pdl=1") and "GB/s" in ln:
+            us = float(ln.split(":")[1].split("us/launch")[0])
+            gbs = float(ln.split("us/launch")[1].split("GB/s")[0])
+            if best is None or gbs > best["gbs"]:
+                best = {"us_per_352MB_launch": us, "gbs": gbs,
+                        "how": "tools/stream_probe launch: bare cp.async.bulk ring, "
+                               "352 MB per launch, PDL-chained, best grid/chunk"}
+    return best
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -450,6 +475,7 @@ def main():
                 if not any(dom_block.values()) else
                 "per batch: block kernel where chosen, else fused stage-1 kernel")
     peak, peak_src = measured_peak()
+    floor = stream_floor() if P == 1 else None
     traffic = None
     # DRAM bytes per launch of the dominant kernel from the committed ncu
     # --set full capture (tools/ncu_summary.py traffic), averaged over the sweep.
@@ -537,6 +563,9 @@ def main():
                          "unit": "GB/s", "frac": round(s1_achieved / peak, 4),
                          "traffic": traffic, "kernel": dom_name,
                          "peak_source": peak_src,
+                         "stream_floor": floor,
+                         "frac_of_stream_floor": (round(s1_achieved / floor["gbs"], 4)
+                                                  if floor else None),
                          "per_batch_us": {str(B): round(s1_us[B], 2) for B in sweep}},
             "e2e": {"value": round(e2e, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": sum(B * DM * 2 for B in sweep),

@@ -83,7 +83,18 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 5) -> str:
           "-Xlinker", "-rpath,/usr/local/cuda/lib64"], verbose)
     os.replace(tmp, LIB)
     build_cpp(verbose)
+    build_probe(verbose)
     return LIB
+
+
+PROBE = os.path.join(ROOT, "tools", "stream_probe")
+
+
+def build_probe(verbose: bool = False) -> None:
+    """tools/stream_probe: the bare cp.async.bulk streaming floor that
+    bench.py reports beside the roofline (measurement aid, not product)."""
+    _run([NVCC, *ARCH, "-O3", "-std=c++17", f"-I{CSRC}",
+          os.path.join(ROOT, "tools", "stream_probe.cu"), "-o", PROBE], verbose)
 
 
 SHIM_LIB = os.path.join(LIBDIR, "libdeepfusion_b200.so")
