@@ -714,7 +714,7 @@ int check_handles(dfk_context_s* ctx, dfk_weights_s* w) {
   if (!w) return fail(DFK_ERR_INVALID, "null weights");
   if (w->ctx != ctx)
     return fail(DFK_ERR_INVALID, "weights belong to another context");
-  return DFK_OK;
+  return use_device(ctx);
 }
 
 uint16_t f32_to_bf16_bits(float f) {
@@ -927,6 +927,7 @@ int dfk_context_destroy(dfk_context ctx) {
 
 int dfk_context_sync(dfk_context ctx) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_TRY(use_device(ctx));
   DFK_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->side_stream) DFK_CUDA(cudaStreamSynchronize(ctx->side_stream));
   if (ctx->out_stream) DFK_CUDA(cudaStreamSynchronize(ctx->out_stream));
@@ -963,6 +964,7 @@ int dfk_weights_create(dfk_context ctx, const void* w_gate, const void* w_up,
                        int64_t ff_end, dfk_weights* out) {
   if (!ctx || !out) return fail(DFK_ERR_INVALID, "null argument");
   *out = nullptr;
+  DFK_TRY(use_device(ctx));
   if (d_model < 1 || d_ff < 1) {
     return fail(DFK_ERR_SHAPE, "MlpWeights: dimensions must be >= 1, got d_model=" +
                                    std::to_string(d_model) +
@@ -1344,18 +1346,21 @@ int dfk_host_free(void* p) {
 
 int dfk_memcpy_h2d(dfk_context ctx, void* dst, const void* src, size_t bytes) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_TRY(use_device(ctx));
   DFK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   return DFK_OK;
 }
 
 int dfk_memcpy_d2h(dfk_context ctx, void* dst, const void* src, size_t bytes) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_TRY(use_device(ctx));
   DFK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   return DFK_OK;
 }
 
 int dfk_memset(dfk_context ctx, void* p, int value, size_t bytes) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_TRY(use_device(ctx));
   DFK_CUDA(cudaMemsetAsync(p, value, bytes, ctx->stream));
   return DFK_OK;
 }
@@ -1363,6 +1368,7 @@ int dfk_memset(dfk_context ctx, void* p, int value, size_t bytes) {
 int dfk_fill_uniform_bf16(dfk_context ctx, void* p, int64_t n, uint64_t seed,
                           float lo, float hi) {
   if (!ctx || !p) return fail(DFK_ERR_INVALID, "null argument");
+  DFK_TRY(use_device(ctx));
   DFK_CUDA(launch_fill_uniform_bf16(static_cast<__nv_bfloat16*>(p), n, seed, lo,
                                     hi, ctx->stream));
   return DFK_OK;
@@ -1382,6 +1388,7 @@ int dfk_event_destroy(void* ev) {
 
 int dfk_event_record(dfk_context ctx, void* ev) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_TRY(use_device(ctx));
   DFK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), ctx->stream));
   return DFK_OK;
 }
@@ -1395,6 +1402,7 @@ int dfk_event_elapsed_ms(void* start, void* stop, float* ms) {
 
 int dfk_flush_l2(dfk_context ctx) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
+  DFK_TRY(use_device(ctx));
   const size_t bytes = static_cast<size_t>(std::max(ctx->l2_bytes, 1 << 20)) * 2;
   DFK_TRY(ensure_buf(ctx->flush, bytes, false, ctx->stream));
   DFK_CUDA(launch_flush(ctx->flush.p, bytes, ctx->stream));

@@ -196,6 +196,11 @@ cudaError_t preload_aux_kernels();
 cudaError_t launch_stage_rows(const void* src, void* dst, int64_t bytes,
                               cudaStream_t s);
 
+// Makes ctx's device current (one host thread may drive contexts on several
+// devices, e.g. the C++ shim's run_tp_mlp); every entry point that launches
+// or copies calls it.
+inline int use_device(dfk_context_s* ctx);
+
 // api.cu helpers used by the scheduler / TP translation units.
 int resolve_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
                    const dfk_config* in, dfk_config* out);
@@ -217,4 +222,16 @@ int block_fused_tp(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t 
 int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s);
 std::string config_label(const dfk_config& c);
 
+}  // namespace dfk
+
+namespace dfk {
+inline int use_device(dfk_context_s* ctx) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != ctx->device) {
+    const cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess)
+      return fail(DFK_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  return DFK_OK;
+}
 }  // namespace dfk

@@ -374,6 +374,7 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   if (!ctx || !w) return fail(DFK_ERR_INVALID, "null handle");
   if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
   if (warmup < 1) return fail(DFK_ERR_INVALID, "profile: warmup must be >= 1");
+  DFK_TRY(use_device(ctx));
   if (runs < 3) return fail(DFK_ERR_INVALID, "profile: runs must be >= 3");
   if (from_cache) *from_cache = 0;
   int64_t dm = w->d_model, df = w->d_ff;

@@ -46,6 +46,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "layout.cuh"
 #include "ptx.cuh"
@@ -1274,19 +1277,20 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
 // Opt every kernel instantiation in to the device's full dynamic shared
 // memory once (the per-launch amount is set in the launch config).
 cudaError_t allow_max_smem(const void* kern) {
-  static int max_optin = -1;
-  static const void* done[64];
-  static int ndone = 0;
-  for (int i = 0; i < ndone; ++i)
-    if (done[i] == kern) return cudaSuccess;
-  if (max_optin < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  }
-  const cudaError_t e = cudaFuncSetAttribute(
-      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
-  if (e == cudaSuccess && ndone < 64) done[ndone++] = kern;
+  // Function attributes are per device (context): cache by (device, kernel),
+  // under a lock (contexts may be created from several host threads).
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, kern})) return cudaSuccess;
+  int max_optin = 0;
+  e = cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin);
+  if (e == cudaSuccess) done.insert({dev, kern});
   return e;
 }
 
