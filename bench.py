@@ -240,20 +240,25 @@ def decode_loop(rt, ctx, ev0, ev1, layers=4, steps=8, sweep=(1, 2, 4, 8, 16, 32)
             for _ in range(2):
                 ctx.decode(ws, x, steps, y, graph=graph)
             ctx.sync()
-            reps = 5
-            ev0.record(ctx)
-            for _ in range(reps):
+            # 4 timed repetitions, mean +- population std of tokens/s
+            # (bench.cpp:59-67 compute_stats, "measured four times")
+            times = []
+            for _ in range(4):
+                ev0.record(ctx)
                 ctx.decode(ws, x, steps, y, graph=graph)
-            ev1.record(ctx)
-            ctx.sync()
-            res[graph] = ev0.elapsed_ms(ev1) * 1e-3 / reps
-        t = res[True]
+                ev1.record(ctx)
+                ctx.sync()
+                times.append(ev0.elapsed_ms(ev1) * 1e-3)
+            res[graph] = times
+        t = statistics.mean(res[True])
+        tps = [B * steps / v for v in res[True]]
         blocks = layers * steps
         out["per_batch"][str(B)] = {
-            "tokens_per_s": round(B * steps / t, 1),
+            "tokens_per_s": round(statistics.mean(tps), 1),
+            "tokens_per_s_std": round(statistics.pstdev(tps), 1),
             "us_per_block": round(t / blocks * 1e6, 2),
             "gbs": round(block_bytes(B, dm, df) * blocks / t / 1e9, 1),
-            "eager_us_per_block": round(res[False] / blocks * 1e6, 2),
+            "eager_us_per_block": round(statistics.mean(res[False]) / blocks * 1e6, 2),
         }
     del ws
     return out
