@@ -676,3 +676,34 @@ def test_contexts_on_two_host_threads(rt, oracle_lib):
     for t in ts:
         t.join()
     assert len(res) == 2 and all(v <= TOL for v in res.values()), res
+
+
+def test_fused_tp_and_decode_error_contract(rt, oracle_lib):
+    """Error classes of the new entry points mirror the reference's: shape
+    problems -> ShapeError (tensor.hpp:21-23), misuse -> InvalidArgument."""
+    c0, c1 = rt.Context(0), rt.Context(0)
+    try:
+        with pytest.raises(rt.ShapeError):
+            c0.tp_sym_create(300, 512)        # max_batch > 256
+        with pytest.raises(rt.ShapeError):
+            c0.tp_sym_create(8, 510)          # d_model % 4
+        x, wu, wg, wd = instance(oracle_lib, 801, 4, 512, 640)
+        w0 = c0.weights(wg, wu, wd, ff_range=(0, 320))
+        xd = c0.array((4, 512)).upload(x)
+        yd = c0.array((4, 512), rt.F32)
+        with pytest.raises(rt.InvalidArgument):
+            c0.tp_forward_fused(w0, xd, yd)   # no symmetric workspace yet
+        c0.tp_sym_create(2, 512)
+        c1.tp_sym_create(2, 512)
+        rt.Context.tp_sym_attach([c0, c1])
+        with pytest.raises(rt.ShapeError):
+            c0.tp_forward_fused(w0, xd, yd)   # batch 4 > max_batch 2
+        w_other = c0.weights(np.zeros((256, 64)), np.zeros((256, 64)), np.zeros((64, 256)))
+        y16 = c0.array((4, 512))
+        with pytest.raises(rt.ShapeError):
+            c0.decode([w0, w_other], xd.__class__(c0, (4, 512)), 1, y16)  # d_model mismatch
+        with pytest.raises(rt.InvalidArgument):
+            c0.decode([w0], c0.array((4, 512)), 0, y16)                  # steps < 1
+    finally:
+        c0.close()
+        c1.close()
