@@ -167,9 +167,9 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
   return DFK_OK;
 }
 
-int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int split_k = 1) {
-  const int avail =
-      ctx->max_smem_optin - 1024 - 1024 - split_red_bytes(n_pad, split_k);
+int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int split_k = 1, int a2_tma = 0) {
+  const int avail = ctx->max_smem_optin - 1024 - 1024 - split_red_bytes(n_pad, split_k) -
+                    a2_stage_bytes(n_pad, a2_tma);
   int s = avail / stream_stage_bytes(n_pad, kbs);
   return std::min(s, 32);
 }
@@ -177,10 +177,11 @@ int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int split_k = 1) {
 // Bigger ring stages stream faster (tools/stream_probe.cu, profiles/): take
 // the largest stage (up to 4 x 16 KiB weight blocks) that still leaves 3
 // slots in shared memory.
-int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int split_k = 1) {
+int pick_kbs(dfk_context_s* ctx, int n_pad, int requested, int split_k = 1,
+             int a2_tma = 0) {
   if (requested > 0) return std::min(requested, 4);
   for (int kbs = 4; kbs > 1; --kbs)
-    if (max_stages(ctx, n_pad, kbs, split_k) >= 3) return kbs;
+    if (max_stages(ctx, n_pad, kbs, split_k, a2_tma) >= 3) return kbs;
   return 1;
 }
 
@@ -323,8 +324,16 @@ int effective_split(const dfk_config& cfg, const dfk_weights_s* w, int64_t nb) {
 // Clusters of `split` CTAs that can be co-resident for this launch shape.
 int cluster_cap(int mode, const StreamArgs& a) {
   if (a.split_k <= 1) return 1 << 30;
-  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.split_k);
+  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs, a.split_k, a.a2_tma);
   return stream_max_clusters(mode, a.split_k, smem);
+}
+
+// Stage-1 A2 through one TMA store per tile: tcgen05 family, no cluster
+// split, and an A2 the tensor map can address (16-byte aligned base/rows).
+int want_a2_tma(const dfk_config& cfg, bool tc, int split_k, const void* a2, int64_t a2_ld) {
+  return tc && split_k <= 1 && env_int("DFK_A2_TMA", 1) &&
+         (reinterpret_cast<uintptr_t>(a2) & 15) == 0 && (a2_ld * 2) % 16 == 0 &&
+         cfg.mutant == 0;
 }
 
 // Ring geometry for one launch: stage size (kbs) and depth.
@@ -344,7 +353,7 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   // as they are: they only feed accumulator columns >= B, never stored).
   a->xrows = (tc && nb <= 8 && env_int("DFK_XROWS8", 1)) ? 8 : n_pad;
   const int sk = a->split_k > 1 ? a->split_k : 1;
-  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk);
+  a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk, a->a2_tma);
   a->trace = ctx->trace;
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
@@ -355,7 +364,7 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   // 12 K blocks (192 KiB) of L2 prefetch: the measured optimum (A/B sweep
   // 0..60, profiles/r1b_tuning.md).
   a->pf_kb = env_int("DFK_PF_KB", 12);
-  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, sk));
+  const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, sk, a->a2_tma));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
 
@@ -392,10 +401,14 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
     a.split_k = effective_split(cfg, w, nb);
+    a.a2_tma = want_a2_tma(cfg, L.tc, a.split_k, a2 + b0 * a2_ld, a2_ld);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
-    CUtensorMap tm;
+    CUtensorMap tm, am;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
                      w->d_model, nb, x_ld, a.xrows, &tm));
+    am = tm;
+    if (a.a2_tma)
+      DFK_TRY(get_tmap(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.xrows, &am));
     a.a2 = a2 + b0 * a2_ld;
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
@@ -422,7 +435,7 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
           std::max(1, std::min({clusters, w->s1_tiles, cluster_cap(kModeStage1, a)}));
       grid = clusters * sk;
     }
-    cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, tm, a,
+    cudaError_t e = launch_stream(kModeStage1, L.tc, gemv_nb(nb), tm, am, a,
                                   grid, cfg.pdl != 0, ctx->stream);
     if (e != cudaSuccess)
       return fail(DFK_ERR_CUDA, std::string("stage-1 launch: ") +
@@ -526,6 +539,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
     a.split_k = effective_split(cfg, w, nb);
+    a.a2_tma = want_a2_tma(cfg, L.tc, a.split_k, a2 + b0 * a2_ld, a2_ld);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap xm, am;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,

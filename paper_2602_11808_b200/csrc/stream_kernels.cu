@@ -1054,7 +1054,8 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
                                             uint32_t tmem_base,
                                             int* smem_flag, PieceQueue* pq,
                                             float* red, uint64_t* red_full,
-                                            uint64_t* red_free) {
+                                            uint64_t* red_free, const CUtensorMap* amap,
+                                            uint8_t* a2st) {
   const int w = static_cast<int>(warp_id());
   const int quarter = w & 3;
   const int lane = static_cast<int>(lane_id());
@@ -1108,6 +1109,42 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
       s1_finish_tile(a, pc.tile, tid, 128, smem_flag);
+    } else if (!pc.down && a.a2_tma) {
+      // A2 tile -> swizzled smem [n][64 cols] bf16 -> one TMA store.  The
+      // barrier first: the previous tile's store has been waited for by tid 0.
+      int is_up, cofs;
+      s1_row_map(row, &is_up, &cofs);
+      named_bar(1, 128);
+      for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
+        float v[16];
+        tmem_ld16_sum(taddr + c0, nacc, astr, v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
+          const int n = c0 + e;
+          if (!is_up) {
+            // row n, column cofs: 16-byte chunk (cofs / 8) XOR (n & 7)
+            const int off = n * 128 + ((((cofs >> 3) ^ (n & 7)) << 4) | ((cofs & 7) << 1));
+            *reinterpret_cast<__nv_bfloat16*>(a2st + off) =
+                __float2bfloat16_rn(silu_f(v[e]) * up);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      fence_proxy_async_shared();
+      named_bar(1, 128);
+      if (tid == 0) {
+        tma_store_2d(amap, a2st, pc.tile * kS1Cols, 0);
+        bulk_commit();
+        bulk_wait_all();
+        if (a.flags) {
+          fence_proxy_async_global();
+          __threadfence();
+          st_release(a.flags + pc.tile, a.epoch);
+        }
+      }
     } else if (!pc.down) {
       int is_up, cofs;
       s1_row_map(row, &is_up, &cofs);
@@ -1169,7 +1206,9 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int stage_bytes = stream_stage_bytes(a.n_pad, a.kbs);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + a.stages * stage_bytes);
+  // A2 staging tile right after the ring (1024-aligned: the 128B swizzle)
+  uint8_t* a2st = smem + a.stages * stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(a2st + a2_stage_bytes(a.n_pad, a.a2_tma));
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
@@ -1234,7 +1273,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
                   tmem_base, pq);
     } else {
       tc_epilogue(a, plan, tfull, tempty, tmem_base, smem_flag, pq, red, red_full,
-                  red_free);
+                  red_free, &amap, a2st);
     }
   } else {
     gemv_consume<NB>(a, plan, smem, stage_bytes, full, empty, smem_flag, pq);
@@ -1391,8 +1430,8 @@ int stream_max_clusters(int mode, int split, int smem) {
   return n > 0 ? n : 1;
 }
 
-int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k) {
-  return 1024 + stages * stream_stage_bytes(n_pad, kbs) + (2 * stages + 4) * 8 +
+int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k, int a2_tma) {
+  return 1024 + stages * stream_stage_bytes(n_pad, kbs) + a2_stage_bytes(n_pad, a2_tma) + (2 * stages + 4) * 8 +
          static_cast<int>(sizeof(PieceQueue)) + 128 + split_red_bytes(n_pad, split_k);
 }
 
@@ -1406,8 +1445,9 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
     return cudaErrorInvalidValue;
   if (a.nacc > 4 || (a.nacc > 1 && (a.split_k > 1 || 2 * a.nacc * a.n_pad > 512)))
     return cudaErrorInvalidValue;
-  const int smem =
-      stream_smem_bytes(a.n_pad, a.stages, a.kbs, mode == kModeDown ? 1 : a.split_k);
+  if (a.a2_tma && (!tc || a.split_k > 1 || mode == kModeDown)) return cudaErrorInvalidValue;
+  const int smem = stream_smem_bytes(a.n_pad, a.stages, a.kbs,
+                                     mode == kModeDown ? 1 : a.split_k, a.a2_tma);
   switch (mode) {
     case kModeStage1:
       return launch_mode<kModeStage1>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);

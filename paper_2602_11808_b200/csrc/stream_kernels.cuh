@@ -30,6 +30,10 @@ struct StreamArgs {
   int B;       // batch rows present
   int n_pad;   // MMA N (tcgen05) / activation box rows (GEMV)
   int xrows;   // rows per activation TMA box (<= n_pad; the smem tile is n_pad rows)
+  // Stage-1 A2 leaves through a swizzled smem tile and ONE TMA store per tile
+  // (amap, box 64 x xrows) instead of per-element stores (tcgen05 family,
+  // whole tiles; host sets it when A2 is TMA-addressable).
+  int a2_tma;
   int stages;  // ring depth
   // split_k (field below) > 1: stage-1 tiles are split along K over the
   // split_k CTAs of a thread-block cluster; partial gate/up accumulators are
@@ -147,7 +151,11 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xma
                           const CUtensorMap& amap, const StreamArgs& a, int grid,
                           bool pdl, cudaStream_t stream);
 
-int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k = 1);
+int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k = 1, int a2_tma = 0);
+// Bytes of the A2 staging tile (a2_tma): n_pad rows of 128 B.
+__host__ __device__ inline int a2_stage_bytes(int n_pad, int a2_tma) {
+  return a2_tma ? n_pad * 128 : 0;
+}
 int stream_max_clusters(int mode, int split, int smem);
 cudaError_t preload_stream_kernels();
 
