@@ -359,9 +359,9 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int nk,
                                                int tid, int nthr, int* smem_flag) {
   const int o = t % a.tp_size;
-  __threadfence_system();
-  named_bar(1, nthr);
+  named_bar(1, nthr);  // then one system-scope fence: see down_finish_tile
   if (tid == 0) {
+    __threadfence_system();
     const int old = atomicAdd_system(a.tp_cnt[o] + t, nk);
     *smem_flag = (old + nk == a.tp_total_kb) ? 1 : 0;
   }
@@ -416,9 +416,12 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
     tp_finish_tile(a, t, nk, tid, nthr, smem_flag);
     return;
   }
-  __threadfence();
+  // Release pattern: every thread's red.adds are ordered before the CTA
+  // barrier; ONE thread's gpu-scope fence (cumulative through the barrier)
+  // then orders them all before its counter increment.
   named_bar(1, nthr);
   if (tid == 0) {
+    __threadfence();
     const int old = atomicAdd(&a.counters[t], 1);
     *smem_flag = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
   }
@@ -497,9 +500,9 @@ __device__ __forceinline__ float* s1acc_at(const StreamArgs& a, int t, int n) {
 __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
                                                int tid, int nthr,
                                                int* smem_flag) {
-  __threadfence();
-  named_bar(1, nthr);
+  named_bar(1, nthr);  // then one fence: see down_finish_tile
   if (tid == 0) {
+    __threadfence();
     const int old = atomicAdd(&a.s1cnt[t], 1);
     *smem_flag = (old == s1_pieces(a) - 1) ? 1 : 0;
   }
