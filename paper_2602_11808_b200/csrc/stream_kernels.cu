@@ -620,8 +620,9 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     if (!down && !x_ok) {  // (whole warp) the side stream's X copy landed?
       unsigned long long t0;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-      while (static_cast<int>(ld_acquire_sys(reinterpret_cast<const int*>(a.x_ready)) -
-                              static_cast<int>(a.x_seq)) < 0)
+      // gpu scope: the flag and the X bytes are written by this GPU's copy
+      // engine / stream front end, visible in its L2
+      while (static_cast<int>(ld_acquire(a.x_ready) - a.x_seq) < 0)
         tp_spin_check(a, t0);
       fence_proxy_async_global();
       x_ok = true;
