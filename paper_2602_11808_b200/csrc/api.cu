@@ -260,8 +260,9 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   // extra balance buys (tools/tp_shard_sweep.py, profiles/r1b_tp_shards.md).
   // At N <= 16 smaller chunks (~16 K blocks, a divisor of the K-block count
   // when one exists) balance the drain better: -1 to -2 % at B = 1..16; at
-  // N >= 32 the per-piece red.adds favour 32 (chunk sweep, r1b_tuning.md).
-  int chunk = std::min(w->dn_kblocks, 32);
+  // N >= 32, 24 K blocks (sweep 16..36 on the full grid: -2 to -5 % against
+  // 32 once the epilogues became straight-line code, profiles/r1c_epilogue.md).
+  int chunk = std::min(w->dn_kblocks, a->n_pad <= 16 ? 32 : 24);
   if (a->n_pad <= 16 && w->dn_kblocks > 16) {
     chunk = 16;
     for (int c = 16; c >= 12; --c)
@@ -280,6 +281,8 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
         1, static_cast<int>(std::lround(static_cast<double>(grid) / w->dn_tiles)));
     chunk = std::max(std::min(4, w->dn_kblocks), (w->dn_kblocks + per_tile - 1) / per_tile);
   }
+  static const int env_chunk = env_int("DFK_DN_CHUNK", 0);
+  if (env_chunk > 0) chunk = std::min(env_chunk, w->dn_kblocks);
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
   // Stage-1 stream-K: a shard with fewer stage-1 tiles than CTAs splits
   // every tile's K range so that ~1.5 x grid stage-1 pieces keep all SMs
@@ -355,6 +358,7 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   const int sk = a->split_k > 1 ? a->split_k : 1;
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk, a->a2_tma);
   a->trace = ctx->trace;
+  if (a->trace) a->trace_s0 = env_int("DFK_TRACE_S0", 24);
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
   if (tc && sk == 1) {
@@ -572,18 +576,21 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     if (++ctx->epoch == 0) ++ctx->epoch;
     a.epoch = ctx->epoch;
     a.mutant = cfg.mutant;
-    // Static plan: the balanced stage-1 grid; dynamic: 7/8 of the SMs (the
-    // measured optimum, profiles/) -- never more CTAs than SMs, since down
-    // pieces spin on other CTAs' stage-1 flags.
-    // Dynamic: 7/8 of the SMs; static: the balanced stage-1 grid but at least
-    // 3/4 of the SMs (the down work needs the CTAs even when the shard has
-    // few stage-1 tiles) -- always co-resident (down pieces spin on other
-    // CTAs' stage-1 flags): never more CTAs than SMs or resident clusters.
+    // Dynamic: 7/8 of the SMs at N <= 16 (the idle eighth starts the next
+    // PDL launch's weight stream early; measured optimum, profiles/), every
+    // SM at N >= 32 on shards with a full stage-1 wave (-2 to -3 % at
+    // B = 32/64, profiles/r1c_epilogue.md).  Static: the balanced stage-1
+    // grid but at least 3/4 of the SMs (the down work needs the CTAs even
+    // when the shard has few stage-1 tiles).  Never more CTAs than SMs or
+    // resident clusters: down pieces spin on other CTAs' stage-1 flags.
+    const bool full = a.n_pad > 16 && w->s1_tiles >= ctx->sm_count;
     int grid = cfg.s1_ctas > 0 ? cfg.s1_ctas
                : cfg.dynamic_sched
-                   ? ctx->sm_count * 7 / 8
+                   ? (full ? ctx->sm_count : ctx->sm_count * 7 / 8)
                    : std::max(balanced_grid(w->s1_tiles, ctx->sm_count),
                               ctx->sm_count * 3 / 4);
+    static const int env_grid = env_int("DFK_GRID", 0);
+    if (env_grid > 0 && cfg.s1_ctas <= 0) grid = env_grid;
     grid = std::max(1, std::min(grid, ctx->sm_count));
     grid = std::min(grid / a.split_k, cluster_cap(kModeBlock, a)) * a.split_k;
     grid = std::max(grid, a.split_k);

@@ -365,11 +365,33 @@ __device__ __forceinline__ float bf16hi(uint32_t u) {
   return __uint_as_float(u & 0xFFFF0000u);
 }
 
-// silu(g) = g * sigmoid(g), stable for |g| >> 1 (no NaN: __expf saturates to
-// inf/0 and the division stays finite), mirroring tensor.hpp:155-163.
+// silu(g) = g * sigmoid(g) (tensor.hpp:155-163) with the MUFU approximations (ex2.approx,
+// rcp.approx; ~2 ulp fp32, far below the bf16 rounding of A2).  Stable for
+// |g| >> 1: exp(-g) saturates to +inf, rcp(inf) = 0, so large negative g
+// gives -0, never NaN.  Five instructions and no branch: the epilogue that
+// runs it executes once per tile from a cold instruction cache, and
+// __frcp_rn's refinement + slow-path branch tripled its code (and its
+// instruction-fetch stalls, profiles/r1b_ncu_block.md).
+// red.global.add.f32 under a predicate (no branch around it).
+__device__ __forceinline__ void red_add_f32_if(float* addr, float v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.f32 [%0], %1;\n}" ::"l"(addr),
+      "f"(v), "r"(static_cast<int>(pred))
+      : "memory");
+}
+
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, unsigned short v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ float silu_f(float g) {
-  // rcp(inf) = 0, so large negative g gives -0, never NaN.
-  return g * __frcp_rn(1.0f + __expf(-g));
+  return g * rcp_approx(1.0f + __expf(-g));
 }
 
 __device__ __forceinline__ float ld_shared_f32(const float* p) {

@@ -316,6 +316,12 @@ __device__ __forceinline__ void trace_stamp(const StreamArgs& a, int slot) {
     a.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + slot] = gtimer();
 }
 
+__device__ __forceinline__ void trace_put(const StreamArgs& a, int slot,
+                                          unsigned long long v) {
+  if (a.trace && slot < kTraceSlots)
+    a.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + slot] = v;
+}
+
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -606,7 +612,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
   // tiles they read have published.  Weight streaming never waits for
   // either: it runs ahead until the ring wraps onto a deferred stage.
   struct Pend {
-    int slot, kb, nb, down, pk0, pk1;
+    int slot, kb, nb, down, pk0, pk1, qi;
     int64_t it;
   };
   Pend pend[32];  // stages <= 32, never more than a ring's worth deferred
@@ -656,6 +662,8 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     }
     for (int j = 0; j < npend; ++j) {
       if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
+      if (leader && pend[j].kb == pend[j].pk0 && pend[j].qi < 8)
+        trace_stamp(a, 32 + pend[j].qi);
       act_loads(smem + static_cast<int64_t>(pend[j].slot) * stage_bytes + wbytes_all,
                 pend[j].kb, pend[j].nb, pend[j].down, &full[pend[j].slot]);
     }
@@ -690,7 +698,11 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     if (!valid) break;
     if (qi == 0) first = pc;
     if (leader) trace_stamp(a, 3 + 2 * qi);
-    const uint8_t* wbase = pc.down ? a.w2 : a.w1;
+    if (leader && qi < 8)
+      trace_put(a, 24 + qi,
+                (static_cast<unsigned long long>(pc.down) << 48) |
+                    (static_cast<unsigned long long>(pc.kb1 - pc.kb0) << 32) |
+                    static_cast<unsigned long long>(pc.tile));    const uint8_t* wbase = pc.down ? a.w2 : a.w1;
     const int kbt = pc.down ? a.kb2 : a.kb1;
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
@@ -713,15 +725,18 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                  wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
                              static_cast<int64_t>(kBlockBytes),
                  static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
+        if (a.trace && it >= a.trace_s0 && it < a.trace_s0 + 12)
+          trace_stamp(a, 40 + static_cast<int>(it - a.trace_s0));
       }
       // Activation loads stay in stage order: defer while anything is
       // deferred, before the PDL wait, or while this down piece's A2 is not
       // yet published (non-blocking check).
       if (!waited || npend > 0 || (pc.down && !check_ready(a, rc, pc.kb0, pc.kb1))) {
         if (qi == 0 && !waited) first_issued += nb;
-        pend[npend++] = {slot, kb, nb, pc.down, pc.kb0, pc.kb1, it};
+        pend[npend++] = {slot, kb, nb, pc.down, pc.kb0, pc.kb1, qi, it};
         continue;
       }
+      if (leader && kb == pc.kb0 && qi < 8) trace_stamp(a, 32 + qi);
       act_loads(st + wbytes_all, kb, nb, pc.down, &full[slot]);
     }
   }
@@ -927,6 +942,8 @@ __device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
       mbar_wait(&full[slot], phase);
+      if (a.trace && it >= a.trace_s0 && it < a.trace_s0 + 12)
+        trace_stamp(a, 52 + static_cast<int>(it - a.trace_s0));
       tc_fence_after();
       const uint32_t sbase = smem0 + static_cast<uint32_t>(slot * stage_bytes);
       const uint64_t dw = desc0 + (sbase >> 4);
@@ -1073,6 +1090,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
     const int ab = acc_it & 1;
     const uint32_t aph = static_cast<uint32_t>((acc_it >> 1) & 1);
     mbar_wait(&tfull[ab], aph);
+    if (tid == 0 && acc_it == 0) trace_stamp(a, 19);
     tc_fence_after();
     const int nacc = a.nacc > 0 ? a.nacc : 1;
     const uint32_t astr = static_cast<uint32_t>(a.n_pad);
@@ -1118,36 +1136,54 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       // barrier first: the previous tile's store has been waited for by tid 0.
       int is_up, cofs;
       s1_row_map(row, &is_up, &cofs);
+      // Lane pairs (l, l ^ 16) hold gate / up of the same column for 16
+      // batch rows; one exchange of 8 values gives each lane 8 (gate, up)
+      // pairs: the gate lane finishes rows n = 4j + {0, 1}, the up lane
+      // n = 4j + {2, 3} (rows 2 apart: the two lanes' 32-byte row segments
+      // fall in different banks of the swizzled tile).  Branch-free, eight
+      // independent SiLU chains, eight shared stores per 16 rows.
+      const uint32_t st_base = smem_u32(a2st) + static_cast<uint32_t>((cofs & 7) << 1);
+      const int chunk = cofs >> 3;
       named_bar(1, 128);
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16_sum(taddr + c0, nacc, astr, v);
+        if (tid == 0 && acc_it == 0 && c0 == 0) trace_stamp(a, 23);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
-          const int n = c0 + e;
-          if (!is_up) {
-            // row n, column cofs: 16-byte chunk (cofs / 8) XOR (n & 7)
-            const int off = n * 128 + ((((cofs >> 3) ^ (n & 7)) << 4) | ((cofs & 7) << 1));
-            *reinterpret_cast<__nv_bfloat16*>(a2st + off) =
-                __float2bfloat16_rn(silu_f(v[e]) * up);
-          }
+        for (int i = 0; i < 8; ++i) {
+          const int ng = (i & 1) + ((i >> 1) << 2);  // gate lane's row
+          const float send = is_up ? v[ng] : v[ng + 2];
+          const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+          const float g = is_up ? recv : v[ng];
+          const float u = is_up ? v[ng + 2] : recv;
+          const int n = c0 + ng + (is_up ? 2 : 0);
+          // row n, column cofs: 16-byte chunk (cofs / 8) XOR (n & 7)
+          st_shared_u16(st_base + static_cast<uint32_t>(n * 128 + ((chunk ^ (n & 7)) << 4)),
+                        __bfloat16_as_ushort(__float2bfloat16_rn(silu_f(g) * u)));
         }
       }
+      if (tid == 0 && acc_it == 0) trace_stamp(a, 31);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
       fence_proxy_async_shared();
       named_bar(1, 128);
       if (tid == 0) {
+        if (acc_it == 0) trace_stamp(a, 20);
         tma_store_2d(amap, a2st, pc.tile * kS1Cols, 0);
         bulk_commit();
         bulk_wait_all();
+        if (acc_it == 0) trace_stamp(a, 21);
         if (a.flags) {
+          // The bulk group's completion made the A2 writes visible to this
+          // thread; the proxy fence orders them (async proxy) before the
+          // release store, whose cumulativity publishes them to every
+          // consumer that acquires the flag (and fences its own async proxy
+          // before loading A2 by TMA, ensure_ready / check_ready).
           fence_proxy_async_global();
-          __threadfence();
           st_release(a.flags + pc.tile, a.epoch);
         }
+        if (acc_it == 0) trace_stamp(a, 22);
       }
     } else if (!pc.down) {
       int is_up, cofs;
@@ -1170,18 +1206,18 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       if (lane == 0) mbar_arrive(&tempty[ab]);
       if (a.flags) s1_publish(a, pc.tile, tid, 128);
     } else {
+      // One predicated red.global.add per (row j, batch n): straight-line
+      // code (the epilogue runs from a cold instruction cache once per piece).
       const int j = pc.tile * kDownCols + row;
-      float* yacc = down_acc(a, pc.tile);
+      const bool jok = j < a.out_cols;
+      float* yp = down_acc(a, pc.tile) + j;
+      const int64_t ld = a.yacc_ld;
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16_sum(taddr + c0, nacc, astr, v);
+        float* yc = yp + c0 * ld;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int n = c0 + e;
-          if (n < a.B && j < a.out_cols) {
-            atomicAdd(yacc + static_cast<int64_t>(n) * a.yacc_ld + j, v[e]);
-          }
-        }
+        for (int e = 0; e < 16; ++e) red_add_f32_if(yc + e * ld, v[e], jok && c0 + e < a.B);
       }
       tc_fence_before();
       __syncwarp();

@@ -127,8 +127,12 @@ struct StreamArgs {
   int* tp_error;  // set before __trap() when a cross-rank wait times out
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
-  // i < 30: [3+2i] first weight copy issued, [4+2i] piece retired.
+  // i < 8: [3+2i] piece fetched (its first weight copy follows), [4+2i]
+  // piece retired, [24+i] descriptor (down << 48 | K blocks << 32 | tile),
+  // [32+i] first activation load; ring stages trace_s0 + j, j < 12:
+  // [40+j] weight copy issued, [52+j] full barrier passed (MMA lane).
   unsigned long long* trace;
+  int trace_s0;
 };
 
 constexpr int kTraceSlots = 64;

@@ -17,7 +17,7 @@ for i in range(4):
     sets.append(ctx.weights(g, u, d)); del g, u, d
 ev0, ev1 = rt.Event(), rt.Event()
 out = []
-for B in (1, 16, 64):
+for B in [int(v) for v in os.environ.get("AB_B", "1,16,64").split(",")]:
     x = ctx.array((B, DM)).fill_uniform(5); y = ctx.array((B, DM), rt.F32)
     for i in range(8):
         ctx.forward(sets[i % 4], x, y)
@@ -26,4 +26,4 @@ for B in (1, 16, 64):
         ctx.forward(sets[i % 4], x, y)
     ev1.record(ctx); ctx.sync()
     out.append(f"B={B}:{ev0.elapsed_ms(ev1) * 1e3 / 40:.2f}us")
-print(os.environ.get("DFK_LIB", "new"), " ".join(out), flush=True)
+print(os.environ.get("AB_TAG", os.environ.get("DFK_LIB", "new")), " ".join(out), flush=True)
