@@ -369,11 +369,12 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
   if (tid == 0) {
     __threadfence_system();
     const int old = atomicAdd_system(a.tp_cnt[o] + t, nk);
-    *smem_flag = (old + nk == a.tp_total_kb) ? 1 : 0;
+    const int last = (old + nk == a.tp_total_kb) ? 1 : 0;
+    if (last) __threadfence_system();  // acquire side, shared through the barrier
+    *smem_flag = last;
   }
   named_bar(1, nthr);
   if (*smem_flag) {
-    __threadfence_system();
     float* acc = a.tp_yacc[o];
     const int col0 = t * kDownCols;
     const int nvec = a.B * (kDownCols / 4);
@@ -429,11 +430,12 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
   if (tid == 0) {
     __threadfence();
     const int old = atomicAdd(&a.counters[t], 1);
-    *smem_flag = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
+    const int last = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
+    if (last) __threadfence();  // acquire side, shared through the barrier
+    *smem_flag = last;
   }
   named_bar(1, nthr);
   if (*smem_flag) {
-    __threadfence();
     // 128 columns x B rows, 4 consecutive floats per thread and iteration;
     // loads are issued 4 deep before any store (the reads are L2 round trips).
     const int col0 = t * kDownCols;
@@ -487,8 +489,10 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
 // other SMs' TMA reads, then publish the tile's completion flag.
 __device__ __forceinline__ void s1_publish(const StreamArgs& a, int tile,
                                            int tid, int nthr) {
+  // Every writer orders its generic A2 stores before later async-proxy
+  // reads; the barrier gathers them at CTA scope and one cumulative
+  // release (tid 0) publishes them at gpu scope.
   fence_proxy_async_global();
-  __threadfence();
   named_bar(1, nthr);
   if (tid == 0) st_release(a.flags + tile, a.epoch);
 }
@@ -510,11 +514,12 @@ __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
   if (tid == 0) {
     __threadfence();
     const int old = atomicAdd(&a.s1cnt[t], 1);
-    *smem_flag = (old == s1_pieces(a) - 1) ? 1 : 0;
+    const int last = (old == s1_pieces(a) - 1) ? 1 : 0;
+    if (last) __threadfence();  // acquire side: the other pieces' sums
+    *smem_flag = last;
   }
   named_bar(1, nthr);
   if (*smem_flag) {
-    __threadfence();
     // Work item (n, c4): A2 columns 4*c4 .. 4*c4+3 of batch row n; its gate
     // sums are 4 consecutive workspace rows, the up sums the 4 rows 16 below.
     // Loads are issued 4 items deep before any store (L2 round trips).
@@ -1109,23 +1114,25 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       continue;
     }
     if (!pc.down && (pc.kb0 > 0 || pc.kb1 < a.kb1)) {
-      // stream-K piece: partial gate/up sums to the workspace
+      // stream-K piece: partial gate/up sums to the workspace (one
+      // predicated red.add per element, straight-line)
       float* base = s1acc_at(a, pc.tile, 0) + row;
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16_sum(taddr + c0, nacc, astr, v);
+        if (a.mutant == 1) {  // negative control: SiLU per K part
+          int is_up, cofs;
+          s1_row_map(row, &is_up, &cofs);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          float val = v[e];
-          if (a.mutant == 1) {
-            const float up = __shfl_xor_sync(0xffffffffu, val, 16);
-            int is_up, cofs;
-            s1_row_map(row, &is_up, &cofs);
-            val = is_up ? 0.f : silu_f(val) * up;
+          for (int e = 0; e < 16; ++e) {
+            const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
+            v[e] = is_up ? 0.f : silu_f(v[e]) * up;
           }
-          const int n = c0 + e;
-          if (n < a.B) atomicAdd(base + static_cast<int64_t>(n) * kBlockRows, val);
         }
+        float* bc = base + static_cast<int64_t>(c0) * kBlockRows;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          red_add_f32_if(bc + e * kBlockRows, v[e], c0 + e < a.B);
       }
       tc_fence_before();
       __syncwarp();
