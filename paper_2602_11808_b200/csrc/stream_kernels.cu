@@ -322,6 +322,19 @@ __device__ __forceinline__ void trace_put(const StreamArgs& a, int slot,
     a.trace[static_cast<int64_t>(blockIdx.x) * kTraceSlots + slot] = v;
 }
 
+// Release/acquire fence at gpu scope (MEMBAR.ALL.GPU; __threadfence() is
+// fence.sc.gpu, MEMBAR.SC.GPU): every counter / flag protocol here is a
+// release-acquire pattern, none needs sequential consistency.
+// Finalize loops (last arriver of a tile) issue this many 16-byte L2 loads
+// per thread before the first store.  8 measured -0.5 us at N = 64 on small
+// TP shards but +0.6 us at N <= 16 (the larger unrolled body runs from a cold
+// instruction cache), profiles/r1c_epilogue.md.
+constexpr int kFinDepth = 4;
+
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -378,11 +391,11 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
     float* acc = a.tp_yacc[o];
     const int col0 = t * kDownCols;
     const int nvec = a.B * (kDownCols / 4);
-    for (int base = tid; base < nvec; base += 4 * nthr) {
-      float4 v[4];
-      float4* q[4];
+    for (int base = tid; base < nvec; base += kFinDepth * nthr) {
+      float4 v[kFinDepth];
+      float4* q[kFinDepth];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kFinDepth; ++u) {
         const int idx = base + u * nthr;
         q[u] = nullptr;
         if (idx < nvec) {
@@ -392,7 +405,7 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kFinDepth; ++u) {
         const int idx = base + u * nthr;
         if (idx < nvec) {
           const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
@@ -418,7 +431,8 @@ __device__ __forceinline__ float* down_acc(const StreamArgs& a, int t) {
 
 __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
                                                  const Plan& p, int t, int nk,
-                                                 int tid, int nthr, int* smem_flag) {
+                                                 int tid, int nthr, int* smem_flag,
+                                                 bool stamp = false) {
   if (a.tp_size > 1) {
     tp_finish_tile(a, t, nk, tid, nthr, smem_flag);
     return;
@@ -428,23 +442,27 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
   // then orders them all before its counter increment.
   named_bar(1, nthr);
   if (tid == 0) {
-    __threadfence();
+    if (stamp) trace_stamp(a, 41);
+    fence_acq_rel_gpu();
+    if (stamp) trace_stamp(a, 42);
     const int old = atomicAdd(&a.counters[t], 1);
     const int last = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
-    if (last) __threadfence();  // acquire side, shared through the barrier
+    if (stamp) trace_stamp(a, 43);
+    if (last) fence_acq_rel_gpu();  // acquire side, shared through the barrier
     *smem_flag = last;
   }
   named_bar(1, nthr);
+  if (stamp && tid == 0) trace_put(a, 45, *smem_flag);
   if (*smem_flag) {
     // 128 columns x B rows, 4 consecutive floats per thread and iteration;
-    // loads are issued 4 deep before any store (the reads are L2 round trips).
+    // loads are issued kFinDepth deep before any store (the reads are L2 round trips).
     const int col0 = t * kDownCols;
     const int nvec = a.B * (kDownCols / 4);
-    for (int base = tid; base < nvec; base += 4 * nthr) {
-      float4 v[4];
-      float4* q[4];
+    for (int base = tid; base < nvec; base += kFinDepth * nthr) {
+      float4 v[kFinDepth];
+      float4* q[kFinDepth];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kFinDepth; ++u) {
         const int idx = base + u * nthr;
         q[u] = nullptr;
         if (idx < nvec) {
@@ -454,7 +472,7 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kFinDepth; ++u) {
         const int idx = base + u * nthr;
         if (idx < nvec) {
           const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
@@ -483,6 +501,7 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
     if (tid == 0) a.counters[t] = 0;
   }
   named_bar(1, nthr);
+  if (stamp && tid == 0) trace_stamp(a, 44);
 }
 
 // Stage-1 epilogue tail in kModeBlock: make this tile's A2 stores visible to
@@ -512,23 +531,23 @@ __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
                                                int* smem_flag) {
   named_bar(1, nthr);  // then one fence: see down_finish_tile
   if (tid == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     const int old = atomicAdd(&a.s1cnt[t], 1);
     const int last = (old == s1_pieces(a) - 1) ? 1 : 0;
-    if (last) __threadfence();  // acquire side: the other pieces' sums
+    if (last) fence_acq_rel_gpu();  // acquire side: the other pieces' sums
     *smem_flag = last;
   }
   named_bar(1, nthr);
   if (*smem_flag) {
     // Work item (n, c4): A2 columns 4*c4 .. 4*c4+3 of batch row n; its gate
     // sums are 4 consecutive workspace rows, the up sums the 4 rows 16 below.
-    // Loads are issued 4 items deep before any store (L2 round trips).
+    // Loads are issued kFinDepth items deep before any store (L2 round trips).
     const int total = a.B * (kS1Cols / 4);
-    for (int base = tid; base < total; base += 4 * nthr) {
-      float4 g[4], u[4];
-      float* ptr[4];
+    for (int base = tid; base < total; base += kFinDepth * nthr) {
+      float4 g[kFinDepth], u[kFinDepth];
+      float* ptr[kFinDepth];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kFinDepth; ++k) {
         const int idx = base + k * nthr;
         ptr[k] = nullptr;
         if (idx < total) {
@@ -539,7 +558,7 @@ __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kFinDepth; ++k) {
         const int idx = base + k * nthr;
         if (idx < total) {
           const int n = idx >> 4, c4 = idx & 15;
@@ -730,7 +749,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                  wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
                              static_cast<int64_t>(kBlockBytes),
                  static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
-        if (a.trace && it >= a.trace_s0 && it < a.trace_s0 + 12)
+        if (a.trace && a.trace_s0 >= 0 && it >= a.trace_s0 && it < a.trace_s0 + 12)
           trace_stamp(a, 40 + static_cast<int>(it - a.trace_s0));
       }
       // Activation loads stay in stage order: defer while anything is
@@ -947,7 +966,7 @@ __device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
       mbar_wait(&full[slot], phase);
-      if (a.trace && it >= a.trace_s0 && it < a.trace_s0 + 12)
+      if (a.trace && a.trace_s0 >= 0 && it >= a.trace_s0 && it < a.trace_s0 + 12)
         trace_stamp(a, 52 + static_cast<int>(it - a.trace_s0));
       tc_fence_after();
       const uint32_t sbase = smem0 + static_cast<uint32_t>(slot * stage_bytes);
@@ -1089,6 +1108,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
   const int tid = (w - 2) * 32 + lane;
   int acc_it = 0;
   int split_iter = 0;
+  bool dn_stamped = false;
   PieceReader pi;
   Piece pc;
   while (pi.next(a, p, pq, false, pc)) {
@@ -1215,6 +1235,9 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
     } else {
       // One predicated red.global.add per (row j, batch n): straight-line
       // code (the epilogue runs from a cold instruction cache once per piece).
+      const bool stamp = a.trace && a.trace_s0 < 0 && !dn_stamped;
+      dn_stamped = dn_stamped || stamp;
+      if (stamp && tid == 0) trace_stamp(a, 40);
       const int j = pc.tile * kDownCols + row;
       const bool jok = j < a.out_cols;
       float* yp = down_acc(a, pc.tile) + j;
@@ -1229,7 +1252,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, 128, smem_flag);
+      down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, 128, smem_flag, stamp);
     }
     if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
     ++acc_it;
@@ -1331,10 +1354,10 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     // The last CTA out re-arms the work counter for the next launch; under
     // the fused TP all-reduce it first waits until every down tile of this
     // rank's Y has been written (by whichever rank finished it).
-    __threadfence();
+    fence_acq_rel_gpu();
     if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
       if (a.x_free) {  // device-scope release: read by stream waits / copy engines
-        __threadfence();
+        fence_acq_rel_gpu();
         st_release(a.x_free, a.x_seq);
         if (a.y_done) st_release(a.y_done, a.x_seq);
       }
@@ -1347,7 +1370,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
       }
       a.sched[0] = 0;
       a.sched[1] = 0;
-      __threadfence();
+      fence_acq_rel_gpu();
     }
   }
   if (split) cluster_sync();  // no CTA leaves while peers may touch its smem

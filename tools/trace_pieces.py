@@ -134,6 +134,22 @@ if a.json:
 # Ring stages kTraceStage0 .. +11 (stream_kernels.cu): weight issue (40+i)
 # and full-barrier completion (52+i) -> per-stage landing latency and the
 # spacing of completions (the CTA's streaming rate).
+if int(os.environ.get("DFK_TRACE_S0", 24)) < 0:
+    # first down piece of each CTA: 40 accumulator ready, 41 red.adds issued
+    # (+ CTA barrier), 42 gpu fence done, 43 counter atomic returned, 44
+    # finish done (finalize when last), 45 = 1 if this CTA finalized
+    d = raw[:, 40:46].astype(np.int64)
+    okd = (d[:, :5] > 0).all(1)
+    if okd.any():
+        d = d[okd]
+        med = lambda x: np.median(x) / 1e3
+        fin = d[:, 5] == 1
+        print(f"down epilogue (first down piece, {int(okd.sum())} CTAs, median us): reds+bar "
+              f"{med(d[:, 1] - d[:, 0]):.2f}, fence {med(d[:, 2] - d[:, 1]):.2f}, atomic "
+              f"{med(d[:, 3] - d[:, 2]):.2f}, finish {med(d[:, 4] - d[:, 3]):.2f} "
+              f"(finalizing CTAs {int(fin.sum())}: "
+              f"{(np.median(d[fin, 4] - d[fin, 3]) / 1e3) if fin.any() else 0:.2f})")
+    sys.exit(0)
 iss = raw[:, 40:52].astype(np.int64)
 ful = raw[:, 52:64].astype(np.int64)
 ok = (iss > 0).all(1) & (ful > 0).all(1)
