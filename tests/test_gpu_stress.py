@@ -1,0 +1,62 @@
+"""Stress of the block kernel's cross-CTA protocols (stage-1 completion
+flags published after the A2 TMA store, down stream-K counters, stage-1
+stream-K counters, the work-queue reset by the last CTA): many PDL-chained
+launches with no host sync between them, inputs alternating between two
+instances so that a stale A2 / workspace / counter from the previous launch
+would show up as a wrong Y (same-input launches would hide it).
+
+Each launch's Y goes to its own buffer; all are checked against the fp64
+oracle at the north-star tolerance afterwards.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    den = np.abs(ref).max()
+    return float(np.abs(got - ref).max() / (den if den > 0 else 1.0))
+
+
+def bf16_instance(oracle_lib, seed, B, dm, df):
+    x, wu, wg, wd = oracle_lib.make_instance(seed, B, dm, df, 1.0 / np.sqrt(dm))
+    return tuple(oracle_lib.quantize_bf16(a)[0] for a in (x, wu, wg, wd))
+
+
+# (dm, df): a shard with a full stage-1 wave (A2 by TMA store + flags, chunk
+# 16/24 down pieces, full grid at N >= 32) and a small TP-like shard (stage-1
+# stream-K over d_model with its own counters).
+@pytest.mark.parametrize("dm,df", [(1024, 14336), (4096, 1792)])
+def test_block_kernel_back_to_back_alternating_inputs(oracle_lib, dm, df):
+    from paper_2602_11808_b200 import runtime as rt
+
+    ctx = rt.Context(0)
+    try:
+        _, wu, wg, wd = bf16_instance(oracle_lib, 7, 1, dm, df)
+        w = ctx.weights(wg, wu, wd)
+        batches = (1, 16, 64, 5, 33)
+        xs, refs = {}, {}
+        for B in batches:
+            for v in (0, 1):
+                x = bf16_instance(oracle_lib, 100 + 2 * B + v, B, dm, 1)[0]
+                xs[B, v] = ctx.array((B, dm)).upload(x)
+                refs[B, v] = oracle_lib.forward(x, wu, wg, wd)[1]
+        calls = [(B, (r + B) & 1) for r in range(24) for B in batches]
+        # every output buffer exists before the first launch (an allocation
+        # between launches could synchronise and hide a race)
+        outs = [ctx.array((B, dm), rt.F32) for (B, _) in calls]
+        ctx.forward(w, xs[1, 0], outs[0])  # warm-up: descriptors, smem opt-in
+        ctx.sync()
+        for (B, v), y in zip(calls, outs):
+            ctx.forward(w, xs[B, v], y)  # PDL-chained, no host sync in between
+        ctx.sync()
+        for (B, v), y in zip(calls, outs):
+            err = rel_err(y.download(), refs[B, v])
+            assert err <= TOL, (dm, df, B, v, err)
+    finally:
+        ctx.close()
