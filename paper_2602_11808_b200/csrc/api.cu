@@ -247,6 +247,24 @@ int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
+// Experiment / tuning overrides, read once per process (DESIGN.md §7 lists
+// them); the defaults are the measured optima.
+struct Knobs {
+  int a2_tma = env_int("DFK_A2_TMA", 1);            // A2 by one TMA store per tile
+  int xrows8 = env_int("DFK_XROWS8", 1);            // 8-row activation boxes at B <= 8
+  int nacc = env_int("DFK_NACC", 1);                // independent accumulator chains
+  int pf_kb = env_int("DFK_PF_KB", 12);             // K blocks prefetched to L2 before PDL wait
+  int trace_s0 = env_int("DFK_TRACE_S0", 24);       // first ring stage the trace records
+  int dn_chunk = env_int("DFK_DN_CHUNK", 0);        // down K chunk (0 = heuristic)
+  int grid = env_int("DFK_GRID", 0);                // block-kernel CTAs (0 = heuristic)
+  int host_stagek = env_int("DFK_HOST_STAGEK", 0);  // host path: staging kernel
+};
+
+const Knobs& knobs() {
+  static const Knobs k;
+  return k;
+}
+
 int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
                  int grid, StreamArgs* a) {
   if (!cfg.dynamic_sched) return DFK_OK;
@@ -281,8 +299,7 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
         1, static_cast<int>(std::lround(static_cast<double>(grid) / w->dn_tiles)));
     chunk = std::max(std::min(4, w->dn_kblocks), (w->dn_kblocks + per_tile - 1) / per_tile);
   }
-  static const int env_chunk = env_int("DFK_DN_CHUNK", 0);
-  if (env_chunk > 0) chunk = std::min(env_chunk, w->dn_kblocks);
+  if (knobs().dn_chunk > 0) chunk = std::min(knobs().dn_chunk, w->dn_kblocks);
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
   // Stage-1 stream-K: a shard with fewer stage-1 tiles than CTAs splits
   // every tile's K range so that ~1.5 x grid stage-1 pieces keep all SMs
@@ -334,7 +351,7 @@ int cluster_cap(int mode, const StreamArgs& a) {
 // Stage-1 A2 through one TMA store per tile: tcgen05 family, no cluster
 // split, and an A2 the tensor map can address (16-byte aligned base/rows).
 int want_a2_tma(const dfk_config& cfg, bool tc, int split_k, const void* a2, int64_t a2_ld) {
-  return tc && split_k <= 1 && env_int("DFK_A2_TMA", 1) &&
+  return tc && split_k <= 1 && knobs().a2_tma &&
          (reinterpret_cast<uintptr_t>(a2) & 15) == 0 && (a2_ld * 2) % 16 == 0 &&
          cfg.mutant == 0;
 }
@@ -354,20 +371,20 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   // Activation rows a TMA box brings in: at B <= 8 only the first 8-row
   // swizzle atom of the N=16 operand (rows 8-15 of the smem tile are left
   // as they are: they only feed accumulator columns >= B, never stored).
-  a->xrows = (tc && nb <= 8 && env_int("DFK_XROWS8", 1)) ? 8 : n_pad;
+  a->xrows = (tc && nb <= 8 && knobs().xrows8) ? 8 : n_pad;
   const int sk = a->split_k > 1 ? a->split_k : 1;
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk, a->a2_tma);
   a->trace = ctx->trace;
-  if (a->trace) a->trace_s0 = env_int("DFK_TRACE_S0", 24);
+  if (a->trace) a->trace_s0 = knobs().trace_s0;
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
   if (tc && sk == 1) {
-    int n = std::max(1, std::min(env_int("DFK_NACC", 1), 256 / n_pad));
+    int n = std::max(1, std::min(knobs().nacc, 256 / n_pad));
     a->nacc = n >= 4 ? 4 : n >= 2 ? 2 : 1;
   }
   // 12 K blocks (192 KiB) of L2 prefetch: the measured optimum (A/B sweep
   // 0..60, profiles/r1b_tuning.md).
-  a->pf_kb = env_int("DFK_PF_KB", 12);
+  a->pf_kb = knobs().pf_kb;
   const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, sk, a->a2_tma));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
@@ -589,8 +606,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
                    ? (full ? ctx->sm_count : ctx->sm_count * 7 / 8)
                    : std::max(balanced_grid(w->s1_tiles, ctx->sm_count),
                               ctx->sm_count * 3 / 4);
-    static const int env_grid = env_int("DFK_GRID", 0);
-    if (env_grid > 0 && cfg.s1_ctas <= 0) grid = env_grid;
+    if (knobs().grid > 0 && cfg.s1_ctas <= 0) grid = knobs().grid;
     grid = std::max(1, std::min(grid, ctx->sm_count));
     grid = std::min(grid / a.split_k, cluster_cap(kModeBlock, a)) * a.split_k;
     grid = std::max(grid, a.split_k);
@@ -1207,7 +1223,7 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
   static const WriteValueFn write_value = driver_fn<WriteValueFn>("cuStreamWriteValue32");
   if (!tp_active(ctx) && batch <= 256 && rc.variant == DFK_VARIANT_FUSED &&
       rc.block_kernel && rc.dynamic_sched && rc.s1_split_k <= 1 && wait_value &&
-      write_value && !env_int("DFK_HOST_STAGEK", 0)) {
+      write_value && !knobs().host_stagek) {
     // Copy-engine X and Y: the H2D copy runs on a side stream as soon as its
     // ring slot is free (device flag x_free >= previous user's sequence no.)
     // and then publishes x_ready = seq; the block kernel -- still PDL-chained
