@@ -331,6 +331,15 @@ __device__ __forceinline__ void trace_put(const StreamArgs& a, int slot,
 // instruction cache), profiles/r1c_epilogue.md.
 constexpr int kFinDepth = 4;
 
+// Counter increment with release (this CTA's writes, gathered by the CTA
+// barrier before it) and acquire (the other pieces' writes, for the last
+// arriver) semantics in one instruction: replaces fence + atomicAdd + fence.
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void fence_acq_rel_gpu() {
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
@@ -380,11 +389,10 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
   const int o = t % a.tp_size;
   named_bar(1, nthr);  // then one system-scope fence: see down_finish_tile
   if (tid == 0) {
-    __threadfence_system();
-    const int old = atomicAdd_system(a.tp_cnt[o] + t, nk);
-    const int last = (old + nk == a.tp_total_kb) ? 1 : 0;
-    if (last) __threadfence_system();  // acquire side, shared through the barrier
-    *smem_flag = last;
+    int old;  // release + acquire at system scope (peers' red.adds), one instruction
+    asm volatile("atom.add.acq_rel.sys.s32 %0, [%1], %2;"
+                 : "=r"(old) : "l"(a.tp_cnt[o] + t), "r"(nk) : "memory");
+    *smem_flag = (old + nk == a.tp_total_kb) ? 1 : 0;  // acquire shared by the barrier
   }
   named_bar(1, nthr);
   if (*smem_flag) {
@@ -443,13 +451,11 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
   named_bar(1, nthr);
   if (tid == 0) {
     if (stamp) trace_stamp(a, 41);
-    fence_acq_rel_gpu();
     if (stamp) trace_stamp(a, 42);
-    const int old = atomicAdd(&a.counters[t], 1);
+    const int old = atom_add_acq_rel_gpu(&a.counters[t], 1);
     const int last = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
     if (stamp) trace_stamp(a, 43);
-    if (last) fence_acq_rel_gpu();  // acquire side, shared through the barrier
-    *smem_flag = last;
+    *smem_flag = last;  // the acquire is shared through the barrier below
   }
   named_bar(1, nthr);
   if (stamp && tid == 0) trace_put(a, 45, *smem_flag);
@@ -528,16 +534,18 @@ __device__ __forceinline__ float* s1acc_at(const StreamArgs& a, int t, int n) {
 // turns the full sums into A2, re-zeroes the workspace and publishes.
 __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
                                                int tid, int nthr,
-                                               int* smem_flag) {
+                                               int* smem_flag, bool stamp = false) {
   named_bar(1, nthr);  // then one fence: see down_finish_tile
   if (tid == 0) {
-    fence_acq_rel_gpu();
-    const int old = atomicAdd(&a.s1cnt[t], 1);
+    if (stamp) trace_stamp(a, 46);
+    if (stamp) trace_stamp(a, 47);
+    const int old = atom_add_acq_rel_gpu(&a.s1cnt[t], 1);
     const int last = (old == s1_pieces(a) - 1) ? 1 : 0;
-    if (last) fence_acq_rel_gpu();  // acquire side: the other pieces' sums
-    *smem_flag = last;
+    if (stamp) trace_stamp(a, 48);
+    *smem_flag = last;  // the acquire is shared through the barrier below
   }
   named_bar(1, nthr);
+  if (stamp && tid == 0) trace_put(a, 51, *smem_flag);
   if (*smem_flag) {
     // Work item (n, c4): A2 columns 4*c4 .. 4*c4+3 of batch row n; its gate
     // sums are 4 consecutive workspace rows, the up sums the 4 rows 16 below.
@@ -577,7 +585,9 @@ __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
       }
     }
     if (tid == 0) a.s1cnt[t] = 0;
+    if (stamp && tid == 0) trace_stamp(a, 49);
     if (a.flags) s1_publish(a, t, tid, nthr);
+    if (stamp && tid == 0) trace_stamp(a, 50);
   }
   named_bar(1, nthr);
 }
@@ -1134,6 +1144,8 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       continue;
     }
     if (!pc.down && (pc.kb0 > 0 || pc.kb1 < a.kb1)) {
+      const bool s1_stamp = a.trace && a.trace_s0 < 0 && acc_it == 0;
+      if (s1_stamp && tid == 0) trace_stamp(a, 52);
       // stream-K piece: partial gate/up sums to the workspace (one
       // predicated red.add per element, straight-line)
       float* base = s1acc_at(a, pc.tile, 0) + row;
@@ -1157,7 +1169,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      s1_finish_tile(a, pc.tile, tid, 128, smem_flag);
+      s1_finish_tile(a, pc.tile, tid, 128, smem_flag, s1_stamp);
     } else if (!pc.down && a.a2_tma) {
       // A2 tile -> swizzled smem [n][64 cols] bf16 -> one TMA store.  The
       // barrier first: the previous tile's store has been waited for by tid 0.
@@ -1354,10 +1366,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     // The last CTA out re-arms the work counter for the next launch; under
     // the fused TP all-reduce it first waits until every down tile of this
     // rank's Y has been written (by whichever rank finished it).
-    fence_acq_rel_gpu();
-    if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+    if (atom_add_acq_rel_gpu(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
       if (a.x_free) {  // device-scope release: read by stream waits / copy engines
-        fence_acq_rel_gpu();
         st_release(a.x_free, a.x_seq);
         if (a.y_done) st_release(a.y_done, a.x_seq);
       }

@@ -149,6 +149,19 @@ if int(os.environ.get("DFK_TRACE_S0", 24)) < 0:
               f"{med(d[:, 3] - d[:, 2]):.2f}, finish {med(d[:, 4] - d[:, 3]):.2f} "
               f"(finalizing CTAs {int(fin.sum())}: "
               f"{(np.median(d[fin, 4] - d[fin, 3]) / 1e3) if fin.any() else 0:.2f})")
+    # first piece when it is a stage-1 stream-K piece: 52 accumulator ready,
+    # 46 red.adds issued (+ barrier), 47 fence, 48 atomic, 49 finalize done,
+    # 50 published (finalizing CTAs), 51 = 1 if this CTA finalized
+    e = raw[:, [52, 46, 47, 48, 49, 50, 51]].astype(np.int64)
+    oke = (e[:, :4] > 0).all(1)
+    if oke.any():
+        e = e[oke]
+        fin = e[:, 6] == 1
+        med = lambda x: np.median(x) / 1e3 if len(x) else 0.0
+        print(f"stage-1 stream-K epilogue (first piece, {int(oke.sum())} CTAs, median us): "
+              f"reds+bar {med(e[:, 1] - e[:, 0]):.2f}, fence {med(e[:, 2] - e[:, 1]):.2f}, "
+              f"atomic {med(e[:, 3] - e[:, 2]):.2f}; finalizing CTAs {int(fin.sum())}: "
+              f"finalize {med(e[fin, 4] - e[fin, 3]):.2f}, publish {med(e[fin, 5] - e[fin, 4]):.2f}")
     sys.exit(0)
 iss = raw[:, 40:52].astype(np.int64)
 ful = raw[:, 52:64].astype(np.int64)
