@@ -572,12 +572,22 @@ __device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
           const int n = idx >> 4, c4 = idx & 15;
           const float gv[4] = {g[k].x, g[k].y, g[k].z, g[k].w};
           const float uv[4] = {u[k].x, u[k].y, u[k].z, u[k].w};
+          float h[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int col = t * kS1Cols + 4 * c4 + e;
-            if (col < a.cols_valid)
-              a.a2[n * a.a2_ld + col] =
-                  __float2bfloat16_rn(a.mutant == 1 ? gv[e] : silu_f(gv[e]) * uv[e]);
+          for (int e = 0; e < 4; ++e) h[e] = a.mutant == 1 ? gv[e] : silu_f(gv[e]) * uv[e];
+          const int col = t * kS1Cols + 4 * c4;
+          __nv_bfloat16* dst = a.a2 + static_cast<int64_t>(n) * a.a2_ld + col;
+          if (col + 3 < a.cols_valid) {  // a2_ld % 8 == 0: 8-byte aligned
+            __nv_bfloat162 lo = __floats2bfloat162_rn(h[0], h[1]);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(h[2], h[3]);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(dst) = pk;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (col + e < a.cols_valid) dst[e] = __float2bfloat16_rn(h[e]);
           }
           __stcg(reinterpret_cast<float4*>(ptr[k]), make_float4(0.f, 0.f, 0.f, 0.f));
           __stcg(reinterpret_cast<float4*>(ptr[k] + 16), make_float4(0.f, 0.f, 0.f, 0.f));
