@@ -258,6 +258,7 @@ struct Knobs {
   int dn_chunk = env_int("DFK_DN_CHUNK", 0);        // down K chunk (0 = heuristic)
   int grid = env_int("DFK_GRID", 0);                // block-kernel CTAs (0 = heuristic)
   int host_stagek = env_int("DFK_HOST_STAGEK", 0);  // host path: staging kernel
+  int red_v4 = env_int("DFK_RED_V4", 1);            // 0 off, 1 small shards, 2 always
 };
 
 const Knobs& knobs() {
@@ -301,6 +302,9 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   }
   if (knobs().dn_chunk > 0) chunk = std::min(knobs().dn_chunk, w->dn_kblocks);
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
+  // Vector partial-sum reductions on shards with fewer stage-1 tiles than
+  // CTAs (latency-bound epilogue chains); neutral on full shards.
+  a->red_v4 = knobs().red_v4 >= 2 || (knobs().red_v4 == 1 && w->s1_tiles < grid);
   // Stage-1 stream-K: a shard with fewer stage-1 tiles than CTAs splits
   // every tile's K range so that ~1.5 x grid stage-1 pieces keep all SMs
   // streaming (s1_chunk_kb > 0 forces a chunk; >= K blocks = whole tiles).

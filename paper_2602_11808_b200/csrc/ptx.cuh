@@ -380,6 +380,16 @@ __device__ __forceinline__ void red_add_f32_if(float* addr, float v, bool pred) 
       : "memory");
 }
 
+// red.global.add.v4.f32 (16-byte aligned) under a predicate.
+__device__ __forceinline__ void red_add_v4_f32_if(float* addr, float a, float b, float c,
+                                                  float d, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n"
+      " @p red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(addr),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"(static_cast<int>(pred))
+      : "memory");
+}
+
 __device__ __forceinline__ void st_shared_u16(uint32_t addr, unsigned short v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
 }

@@ -433,6 +433,34 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
   named_bar(1, nthr);
 }
 
+// 16 accumulator values of one lane (its output row `lane`, batch rows
+// c0 .. c0+15) added into a [n][ld] fp32 workspace whose lane-consecutive
+// addresses are consecutive floats: groups of 4 lanes transpose 4 x 4 blocks
+// (two shuffle butterflies) so that each lane adds 4 consecutive floats of
+// one batch row with a single red.global.add.v4.f32.  `col0` = the address of
+// the group's first column for batch row 0 (16-byte aligned, ld % 4 == 0).
+__device__ __forceinline__ void red_rows_v4(float (&v)[16], float* col0, int64_t ld,
+                                            int c0, int nvalid, int lane) {
+  const int li = lane & 3;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    float* x = v + 4 * b;
+#pragma unroll
+    for (int st = 1; st <= 2; st <<= 1) {
+      const bool hi = (lane & st) != 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (r & st) continue;
+        const float send = hi ? x[r] : x[r | st];
+        const float recv = __shfl_xor_sync(0xffffffffu, send, st);
+        if (hi) x[r] = recv; else x[r | st] = recv;
+      }
+    }
+    const int n = c0 + 4 * b + li;
+    red_add_v4_f32_if(col0 + static_cast<int64_t>(n) * ld, x[0], x[1], x[2], x[3], n < nvalid);
+  }
+}
+
 __device__ __forceinline__ float* down_acc(const StreamArgs& a, int t) {
   return a.tp_size > 1 ? a.tp_yacc[t % a.tp_size] : a.yacc;
 }
@@ -1171,10 +1199,14 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
             v[e] = is_up ? 0.f : silu_f(v[e]) * up;
           }
         }
-        float* bc = base + static_cast<int64_t>(c0) * kBlockRows;
+        if (a.red_v4) {
+          red_rows_v4(v, base - (lane & 3), kBlockRows, c0, a.B, lane);
+        } else {
+          float* bc = base + static_cast<int64_t>(c0) * kBlockRows;
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          red_add_f32_if(bc + e * kBlockRows, v[e], c0 + e < a.B);
+          for (int e = 0; e < 16; ++e)
+            red_add_f32_if(bc + e * kBlockRows, v[e], c0 + e < a.B);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -1264,12 +1296,20 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       const bool jok = j < a.out_cols;
       float* yp = down_acc(a, pc.tile) + j;
       const int64_t ld = a.yacc_ld;
+      // v4 reductions: local workspace only, whole 4-column groups (the
+      // condition is warp-uniform: the shuffles involve all 32 lanes)
+      const bool vec = a.red_v4 && a.tp_size <= 1 &&
+                       __all_sync(0xffffffffu, j - (lane & 3) + 3 < a.out_cols);
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16_sum(taddr + c0, nacc, astr, v);
-        float* yc = yp + c0 * ld;
+        if (vec) {
+          red_rows_v4(v, yp - (lane & 3), ld, c0, a.B, lane);
+        } else {
+          float* yc = yp + c0 * ld;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) red_add_f32_if(yc + e * ld, v[e], jok && c0 + e < a.B);
+          for (int e = 0; e < 16; ++e) red_add_f32_if(yc + e * ld, v[e], jok && c0 + e < a.B);
+        }
       }
       tc_fence_before();
       __syncwarp();

@@ -133,6 +133,9 @@ struct StreamArgs {
   // [40+j] weight copy issued, [52+j] full barrier passed (MMA lane).
   unsigned long long* trace;
   int trace_s0;
+  // Partial-sum reductions (stage-1 stream-K, down pieces) as
+  // red.global.add.v4.f32 after a 4 x 4 lane transpose (small shards).
+  int red_v4;
 };
 
 constexpr int kTraceSlots = 64;
