@@ -135,7 +135,7 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx,
   if (w->s1_tiles < ctx->sm_count) {
     const int kb = w->s1_kblocks;
     for (int s1k : {0, (kb + 1) / 2, (kb + 2) / 3, std::max(8, (kb + 3) / 4), 1 << 20})
-      for (int ck : {0, 16}) {
+      for (int ck : {0, 8, 16}) {  // 8: best on Llama-8B TP=4/8 at B <= 16 (r1c)
         dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 1, 1);
         c.dynamic_sched = 1;
         c.s1_chunk_kb = s1k;

@@ -66,7 +66,7 @@ for name in a.shapes.split(","):
                     kw = {k: int(v) for k, v in (p.split("=") for p in spec.split(",") if p)}
                     cfg = rt.Config.make(**kw)
                 try:
-                    for i in range(4):
+                    for i in range(2 * nsets):  # every set once (first-use costs)
                         ctx.forward(sets[i % nsets], x, y, cfg=cfg)
                     ctx.sync()
                     ev0.record(ctx)
