@@ -135,9 +135,10 @@ if a.json:
 # and full-barrier completion (52+i) -> per-stage landing latency and the
 # spacing of completions (the CTA's streaming rate).
 if int(os.environ.get("DFK_TRACE_S0", 24)) < 0:
-    # first down piece of each CTA: 40 accumulator ready, 41 red.adds issued
-    # (+ CTA barrier), 42 gpu fence done, 43 counter atomic returned, 44
-    # finish done (finalize when last), 45 = 1 if this CTA finalized
+    # first down piece of each CTA: 40 accumulator ready, 41/42 red.adds
+    # issued (+ CTA barrier), 43 counter atom.acq_rel returned (its release
+    # MEMBAR included), 44 finish done (finalize when last), 45 = 1 if this
+    # CTA finalized
     d = raw[:, 40:46].astype(np.int64)
     okd = (d[:, :5] > 0).all(1)
     if okd.any():
@@ -150,8 +151,8 @@ if int(os.environ.get("DFK_TRACE_S0", 24)) < 0:
               f"(finalizing CTAs {int(fin.sum())}: "
               f"{(np.median(d[fin, 4] - d[fin, 3]) / 1e3) if fin.any() else 0:.2f})")
     # first piece when it is a stage-1 stream-K piece: 52 accumulator ready,
-    # 46 red.adds issued (+ barrier), 47 fence, 48 atomic, 49 finalize done,
-    # 50 published (finalizing CTAs), 51 = 1 if this CTA finalized
+    # 46/47 red.adds issued (+ barrier), 48 counter atom.acq_rel returned,
+    # 49 finalize done, 50 published (finalizing CTAs), 51 = 1 if finalized
     e = raw[:, [52, 46, 47, 48, 49, 50, 51]].astype(np.int64)
     oke = (e[:, :4] > 0).all(1)
     if oke.any():
