@@ -247,7 +247,7 @@ int env_int(const char* name, int dflt) {
   return v && *v ? std::atoi(v) : dflt;
 }
 
-// Experiment / tuning overrides, read once per process (DESIGN.md §7 lists
+// Experiment / tuning overrides, read once per process (DESIGN.md §7b lists
 // them); the defaults are the measured optima.
 struct Knobs {
   int a2_tma = env_int("DFK_A2_TMA", 1);            // A2 by one TMA store per tile

@@ -371,7 +371,7 @@ __device__ __forceinline__ float bf16hi(uint32_t u) {
 // gives -0, never NaN.  Five instructions and no branch: the epilogue that
 // runs it executes once per tile from a cold instruction cache, and
 // __frcp_rn's refinement + slow-path branch tripled its code (and its
-// instruction-fetch stalls, profiles/r1b_ncu_block.md).
+// instruction-fetch stalls, profiles/r1c_epilogue.md).
 // red.global.add.f32 under a predicate (no branch around it).
 __device__ __forceinline__ void red_add_f32_if(float* addr, float v, bool pred) {
   asm volatile(
