@@ -1,0 +1,60 @@
+"""Parity of the kernel paths the default configuration does not take, each
+selected by its environment knob (read once per process, so every case runs
+in a fresh interpreter): stage-1 tiles writing A2 with per-thread global
+stores (DFK_A2_TMA=0), full 16-row activation boxes at B <= 8 (DFK_XROWS8=0),
+v4 partial-sum reductions on full shards too (DFK_RED_V4=2) or nowhere
+(DFK_RED_V4=0), two accumulator chains (DFK_NACC=2), the full grid and
+down chunks of 8 K blocks at every N (DFK_GRID / DFK_DN_CHUNK).  Shapes
+cover a full stage-1 wave (d_ff/64 >= SMs) and a small shard, B across the
+N = 16 / 32 / 64 MMA widths.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import oracle
+from paper_2602_11808_b200 import runtime as rt
+orc = oracle.Oracle()
+ctx = rt.Context(0)
+worst = 0.0
+for dm, df in ((512, 9600), (1024, 1536)):
+    x, wu, wg, wd = (orc.quantize_bf16(a)[0] for a in
+                     orc.make_instance(31, 64, dm, df, 1.0 / np.sqrt(dm)))
+    w = ctx.weights(wg, wu, wd)
+    for B in (1, 5, 16, 33, 64):
+        _, y_ref = orc.forward(x[:B], wu, wg, wd)
+        xd = ctx.array((B, dm)).upload(x[:B])
+        y = ctx.array((B, dm), rt.F32)
+        for _ in range(3):  # back to back: the cross-CTA flags / counters
+            ctx.forward(w, xd, y)
+        err = float(np.abs(y.download() - y_ref).max() / np.abs(y_ref).max())
+        worst = max(worst, err)
+        assert err <= 1e-2, (dm, df, B, err)
+print("worst", worst)
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"DFK_A2_TMA": "0"},
+    {"DFK_XROWS8": "0"},
+    {"DFK_RED_V4": "2"},
+    {"DFK_RED_V4": "0"},
+    {"DFK_NACC": "2"},
+    {"DFK_GRID": "148", "DFK_DN_CHUNK": "8"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_knob_paths_match_oracle(env):
+    r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)],
+                       env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "worst" in r.stdout
