@@ -267,7 +267,7 @@ const Knobs& knobs() {
 }
 
 int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
-                 int grid, StreamArgs* a) {
+                 int grid, StreamArgs* a, bool down_only = false) {
   if (!cfg.dynamic_sched) return DFK_OK;
   DFK_TRY(ensure_buf(ctx->sched, 64, true, ctx->stream));
   a->dynamic = 1;
@@ -281,8 +281,11 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   // when one exists) balance the drain better: -1 to -2 % at B = 1..16; at
   // N >= 32, 24 K blocks (sweep 16..36 on the full grid: -2 to -5 % against
   // 32 once the epilogues became straight-line code, profiles/r1c_epilogue.md).
-  int chunk = std::min(w->dn_kblocks, a->n_pad <= 16 ? 32 : 24);
-  if (a->n_pad <= 16 && w->dn_kblocks > 16) {
+  // The down kernel on its own (dfk_down, no stage-1 dependency): 32 K
+  // blocks at every N (sweep 8..56 on all SMs: -11 to -18 % against 16/24,
+  // profiles/r1c_epilogue.md).
+  int chunk = std::min(w->dn_kblocks, a->n_pad <= 16 || down_only ? 32 : 24);
+  if (a->n_pad <= 16 && w->dn_kblocks > 16 && !down_only) {
     chunk = 16;
     for (int c = 16; c >= 12; --c)
       if (w->dn_kblocks % c == 0) {
@@ -487,11 +490,12 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
                      w->d_ff, nb, a_ld, a.xrows, &tm));
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
-    // Default: 3/4 of the SMs with deep rings streams faster than every SM
-    // with the same ring (measured, profiles/r1_sweeps.md).
-    int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count * 3 / 4;
+    // Default: every SM (the dynamic queue balances; 3/4 of the SMs, the
+    // first session's optimum for the static plan, is 11-18 % slower now,
+    // profiles/r1c_epilogue.md).
+    int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count;
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, U));
-    DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a));
+    DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a, true));
     cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
                                   static_cast<int>(grid), cfg.pdl != 0,
                                   ctx->stream);
