@@ -119,7 +119,9 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx,
       add(d);
     }
   }
-  const int dn_ctas[2] = {0, ctx->sm_count};  // 0 = library default (3/4 SMs)
+  // 0 = library default (every SM); 3/4 of the SMs was the default before
+  // the dynamic queue and stays a candidate
+  const int dn_ctas[2] = {0, ctx->sm_count * 3 / 4};
   for (int s1f : fams)
     for (int dnf : fams)
       for (int dc : dn_ctas) {
