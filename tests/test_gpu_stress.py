@@ -8,12 +8,16 @@ would show up as a wrong Y (same-input launches would hide it).
 Each launch's Y goes to its own buffer; all are checked against the fp64
 oracle at the north-star tolerance afterwards.
 """
+import os
+
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-2
+# rounds of the batch cycle (DFK_STRESS_ROUNDS=400: 4000 launches, measured green)
+ROUNDS = int(os.environ.get("DFK_STRESS_ROUNDS", "24"))
 
 
 def rel_err(got, ref):
@@ -46,7 +50,7 @@ def test_block_kernel_back_to_back_alternating_inputs(oracle_lib, dm, df):
                 x = bf16_instance(oracle_lib, 100 + 2 * B + v, B, dm, 1)[0]
                 xs[B, v] = ctx.array((B, dm)).upload(x)
                 refs[B, v] = oracle_lib.forward(x, wu, wg, wd)[1]
-        calls = [(B, (r + B) & 1) for r in range(24) for B in batches]
+        calls = [(B, (r + B) & 1) for r in range(ROUNDS) for B in batches]
         # every output buffer exists before the first launch (an allocation
         # between launches could synchronise and hide a race)
         outs = [ctx.array((B, dm), rt.F32) for (B, _) in calls]
