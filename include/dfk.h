@@ -36,7 +36,9 @@
  *                                                               dfk_forward_host_async
  *   balanced_ranges         tp.hpp:36, tp.cpp:8-29            -> dfk_balanced_range
  *   profile / select / Tuner::get_or_tune  tuner.hpp:103-137  -> dfk_tune
- *   cache_store / cache_lookup  tuner.hpp:102-113              -> dfk_tune (cache_path)
+ *   cache_store / cache_lookup  tuner.hpp:102-113              -> dfk_cache_store /
+ *                                                               dfk_cache_lookup (and
+ *                                                               dfk_tune's cache_path)
  *   default_candidates      tuner.hpp:55                      -> dfk_candidates
  *   default_fingerprint     tuner.hpp:116                     -> dfk_fingerprint
  *   predict_traffic         traffic.hpp:60-71 (fused, single tile)
@@ -77,7 +79,9 @@ typedef enum dfk_status {
   DFK_ERR_NOMEM = 5,
   DFK_ERR_UNSUPPORTED = 6,
   DFK_ERR_GATE = 7,        /* every scheduler candidate failed the gate */
-  DFK_ERR_CACHE = 8        /* reference CacheError */
+  DFK_ERR_CACHE = 8,       /* reference CacheError */
+  DFK_ERR_TIMEOUT = 9      /* a fused all-reduce wait on a peer gave up
+                              (reported by dfk_context_sync)               */
 } dfk_status;
 
 typedef enum dfk_dtype { DFK_F64 = 0, DFK_F32 = 1, DFK_BF16 = 2 } dfk_dtype;
@@ -112,7 +116,11 @@ typedef struct dfk_config {
   int32_t down_ctas;    /* stream-K CTAs (0 = one per SM)                  */
   int32_t pdl;          /* 1 = programmatic dependent launch between the
                            two kernels (and across calls); 0 = plain       */
-  int32_t mutant;       /* negative controls, tests only (0 = none)        */
+  int32_t mutant;       /* negative controls, tests only: 0 = none, 1 =
+                           SiLU*up per K chunk (stream-K / split-K pieces;
+                           verification.cpp:84-124), 2 = SiLU(A_gate)
+                           round-tripped through a global buffer
+                           (MaterializeIntermediate, :126-169)            */
   int32_t block_kernel; /* 1 = the whole block (stage 1 + down) in ONE
                            persistent kernel with per-tile A2 dependency
                            flags (the paper's single deeply fused kernel);
@@ -151,8 +159,12 @@ DFK_API int dfk_sm_count(dfk_context ctx, int* n);
 /* Registers one block's weights in the reference layout and prepacks them.
  * [ff_begin, ff_end) selects a tensor-parallel shard of d_ff (pass 0, d_ff
  * for the whole block): W_gate/W_up columns and W_down rows of that range
- * (tp.cpp:140-167).  Errors: DFK_ERR_SHAPE for dims < 1 or an empty /
- * out-of-range shard. */
+ * (tp.cpp:140-167).  Stage-only sets: w_down NULL registers stage 1 alone
+ * (run_fused_stage1's W_up / W_gate, fused.hpp:61-63; dfk_stage1 only),
+ * w_gate and w_up both NULL registers the down projection alone
+ * (down_projection's W_down, swiglu.hpp:90-91; dfk_down only); calls that
+ * need the missing part fail with DFK_ERR_INVALID.  Errors: DFK_ERR_SHAPE
+ * for dims < 1 or an empty / out-of-range shard. */
 DFK_API int dfk_weights_create(dfk_context ctx, const void* w_gate,
                                const void* w_up, const void* w_down,
                                int64_t d_model, int64_t d_ff, int32_t dtype,
@@ -220,6 +232,11 @@ DFK_API int dfk_decode(dfk_context ctx, const dfk_weights* layers,
  * count in *n (default_candidates, tuner.cpp:59-88). */
 DFK_API int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
                            dfk_config* out, int32_t cap, int32_t* n);
+/* The same grid for a shape (B, d_model, d_ff shard) without registered
+ * weights (the C++ shim's gpu_candidates). */
+DFK_API int dfk_candidates_shape(dfk_context ctx, int64_t batch, int64_t d_model,
+                                 int64_t d_ff, dfk_config* out, int32_t cap,
+                                 int32_t* n);
 /* Profiles every candidate on the context's GPU (CUDA-event timing: one
  * gate run, `warmup` >= 1 untimed runs, `runs` >= 3 timed runs, lower
  * median), disqualifies those deviating from the unfused cuBLASLt reference
@@ -233,6 +250,20 @@ DFK_API int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
                      const char* cache_path, int32_t warmup, int32_t runs,
                      dfk_config* chosen, int32_t* from_cache,
                      char* results_json, size_t results_len);
+/* The tuning cache on its own (cache_lookup / cache_store, tuner.hpp:102-113):
+ * one JSON document {"format_version": 1, "entries": [...]} whose entries
+ * are ScheduleEntry objects keyed by (shape.batch, shape.d_model,
+ * shape.d_ff, fingerprint).  Lookup of an absent file or key sets *found = 0;
+ * a corrupt file or another format_version is DFK_ERR_CACHE.  *needed
+ * (optional) receives the entry's size incl. the NUL; a too-small buffer is
+ * DFK_ERR_INVALID (entry_json may be NULL to query the size).  Store inserts
+ * or replaces the entry with the same key; safe across threads and
+ * processes, readers never see a partially written file. */
+DFK_API int dfk_cache_lookup(const char* path, int64_t batch, int64_t d_model,
+                             int64_t d_ff, const char* fingerprint,
+                             char* entry_json, size_t len, size_t* needed,
+                             int32_t* found);
+DFK_API int dfk_cache_store(const char* path, const char* entry_json);
 /* The configuration a NULL-cfg call with this B would use. */
 DFK_API int dfk_select_config(dfk_context ctx, dfk_weights w, int64_t batch,
                               dfk_config* out);
@@ -270,20 +301,25 @@ DFK_API int dfk_tp_forward(dfk_context ctx, dfk_weights w, const void* x,
  *   order (every rank's dfk_tp_sym_create output, exchanged by the caller).
  * dfk_tp_sym_attach: one process driving n contexts (on n devices, or
  *   several contexts on ONE device as an emulation of n ranks).
- * dfk_tp_forward_fused: this rank's shard, Y (fp32 [B x d_model], device)
- *   = the full sum over ranks.  Every rank must issue it with the same
- *   batch; a rank waits at most 4 s for its peers, then the launch fails.
- *   When ONE process drives several ranks, allocate every buffer before
- *   issuing the ranks' calls (a cudaMalloc may wait for the device, i.e. for
- *   a rank that waits for a peer not launched yet). */
+ * dfk_tp_forward_fused: this rank's shard -- the balanced_ranges(d_ff, P)
+ *   shard of its rank (anything else is DFK_ERR_INVALID) -- and Y (y_dtype
+ *   F32 or BF16 [B x d_model], device) = the full sum over ranks, written
+ *   by the block kernel itself: ONE launch per block, nothing after it.
+ *   Every rank must issue it with the same batch.  A rank waits at most 4 s
+ *   for its peers; then the launch ends with a wrong Y and the next
+ *   dfk_context_sync returns DFK_ERR_TIMEOUT (the context stays usable;
+ *   re-create the symmetric workspaces).  When ONE process drives several
+ *   ranks, allocate every buffer before issuing the ranks' calls (a
+ *   cudaMalloc may wait for the device, i.e. for a rank that waits for a
+ *   peer not launched yet). */
 DFK_API int dfk_tp_sym_create(dfk_context ctx, int64_t max_batch,
                               int64_t d_model, void* ipc_handle64);
 DFK_API int dfk_tp_sym_open(dfk_context ctx, const void* handles, int rank,
                             int nranks);
 DFK_API int dfk_tp_sym_attach(dfk_context* ctxs, int n);
 DFK_API int dfk_tp_forward_fused(dfk_context ctx, dfk_weights w,
-                                 const void* x, int64_t batch, float* y,
-                                 const dfk_config* cfg);
+                                 const void* x, int64_t batch, void* y,
+                                 int32_t y_dtype, const dfk_config* cfg);
 
 /* balanced_ranges(extent, parts)[index] (tp.cpp:8-29). */
 DFK_API int dfk_balanced_range(int64_t extent, int64_t parts, int64_t index,

@@ -21,8 +21,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 JSON_DIR = ("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/"
             "cudnn_frontend/thirdparty/nlohmann")
 
-SOURCES = ["stream_kernels.cu", "aux_kernels.cu", "api.cu", "scheduler.cpp", "tp.cpp",
-           "decode.cpp"]
+SOURCES = ["stream_kernels.cu", "aux_kernels.cu", "api.cu", "scheduler.cpp",
+           "tuning_cache.cpp", "tp.cpp", "decode.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
           "-Xcompiler", "-fvisibility=hidden", f"-I{os.path.join(ROOT, 'include')}",
@@ -99,6 +99,7 @@ def build_probe(verbose: bool = False) -> None:
 
 SHIM_LIB = os.path.join(LIBDIR, "libdeepfusion_b200.so")
 CPP_TEST = os.path.join(ROOT, "tests", "cpp", "test_deepfusion_gpu")
+CPP_TUNER_TEST = os.path.join(ROOT, "tests", "cpp", "test_tuner_gpu")
 
 
 def build_cpp(verbose: bool = False) -> None:
@@ -106,13 +107,14 @@ def build_cpp(verbose: bool = False) -> None:
     test binary; both link libdfk.so through an $ORIGIN-relative rpath."""
     cpp = os.path.join(PKG, "cpp")
     _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-Wall",
-          f"-I{os.path.join(ROOT, 'include')}", f"-I{cpp}",
+          f"-I{os.path.join(ROOT, 'include')}", f"-I{cpp}", f"-I{JSON_DIR}",
           os.path.join(cpp, "deepfusion_gpu.cpp"), "-o", SHIM_LIB,
           f"-L{LIBDIR}", "-ldfk", "-Wl,-rpath,$ORIGIN"], verbose)
-    _run(["g++", "-O2", "-std=c++20", "-Wall", f"-I{cpp}",
-          os.path.join(ROOT, "tests", "cpp", "test_deepfusion_gpu.cpp"), "-o", CPP_TEST,
-          f"-L{LIBDIR}", "-ldeepfusion_b200", "-ldfk",
-          f"-Wl,-rpath,$ORIGIN/../../paper_2602_11808_b200/lib"], verbose)
+    for src, exe in (("test_deepfusion_gpu.cpp", CPP_TEST), ("test_tuner_gpu.cpp", CPP_TUNER_TEST)):
+        _run(["g++", "-O2", "-std=c++20", "-Wall", f"-I{cpp}",
+              os.path.join(ROOT, "tests", "cpp", src), "-o", exe,
+              f"-L{LIBDIR}", "-ldeepfusion_b200", "-ldfk",
+              f"-Wl,-rpath,$ORIGIN/../../paper_2602_11808_b200/lib"], verbose)
 
 
 if __name__ == "__main__":

@@ -19,7 +19,13 @@
 //   ColRange, balanced_ranges, ShardPlan,
 //   make_plan, run_tp_mlp, TpResult,
 //   CollectiveLog, comm_volume_bytes        tp.hpp:26-101
-//   profile-driven scheduler front door     tuner.hpp:117-137 (Tuner)
+//   ReuseCounts, predicted_reuse_counts     fused.hpp:69-80
+//   scheduler: BenchmarkResult, ScheduleEntry, default_candidates,
+//     CandidateRunner, make_runner(s), ProfileOptions, profile, select,
+//     CacheError, cache_store / cache_lookup, default_fingerprint, Tuner
+//                                           tuner.hpp:26-137
+//   verification::Mutant, FusedStage1Fn,
+//     fused_stage1_for, the two mutants      verification.hpp:27-53
 //
 // Differences dictated by the hardware (documented, not hidden):
 //   * numerics are bf16 in / fp32 accumulate / bf16 A2: results match the
@@ -31,13 +37,23 @@
 //   * the AccessLedger instrumentation is not provided (its GPU counterpart
 //     is the ncu DRAM counters); Accounting is accepted for
 //     signature compatibility and ignored;
-//   * weights are prepacked on the GPU on first use, keyed by the matrices'
-//     storage and a sampled content fingerprint; call release_gpu_cache()
-//     after mutating weights in place if the sample might miss the change.
+//   * weights are prepacked on the GPU on first use and reused while the
+//     Matrix objects are unchanged: every Matrix carries a process-unique id
+//     and a version that each non-const access bumps (operator(), data(),
+//     set_zero, assignment), so an in-place edit or a new matrix at a
+//     recycled address is never served a stale pack.  At most
+//     kGpuCachedWeightSets packs stay resident (least recently used out);
+//     release_gpu_cache() drops them all;
+//   * the scheduler's correctness gate is relative at bf16 precision
+//     (kCorrectnessGateTolerance below), and its candidates can be the GPU
+//     launch configurations themselves (gpu_candidates).
 #pragma once
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <filesystem>
+#include <functional>
 #include <map>
 #include <memory>
 #include <optional>
@@ -62,27 +78,69 @@ struct GpuError : std::runtime_error {
   GpuError(int s, const std::string& m) : std::runtime_error(m), status(s) {}
 };
 
-// Dense row-major fp64 matrix (tensor.hpp:73-128 without the ledger).
+// Dense row-major fp64 matrix (tensor.hpp:73-128 without the ledger).  id()
+// is unique per matrix object (copies get a new one) and version() changes
+// with every non-const access: (id, version) names the exact contents, which
+// is what the GPU weight-pack cache keys on.
 class Matrix {
  public:
-  Matrix() = default;
+  Matrix() : id_(next_id()) {}
   Matrix(Index rows, Index cols);
+  Matrix(const Matrix& o) : rows_(o.rows_), cols_(o.cols_), data_(o.data_), id_(next_id()) {}
+  Matrix(Matrix&& o) noexcept
+      : rows_(o.rows_), cols_(o.cols_), data_(std::move(o.data_)), id_(next_id()) {
+    o.touch();
+  }
+  Matrix& operator=(const Matrix& o) {
+    rows_ = o.rows_;
+    cols_ = o.cols_;
+    data_ = o.data_;
+    touch();
+    return *this;
+  }
+  Matrix& operator=(Matrix&& o) noexcept {
+    rows_ = o.rows_;
+    cols_ = o.cols_;
+    data_ = std::move(o.data_);
+    touch();
+    o.touch();
+    return *this;
+  }
   static Matrix identity(Index n);
 
   Index rows() const { return rows_; }
   Index cols() const { return cols_; }
   Index size() const { return rows_ * cols_; }
-  double& operator()(Index i, Index j) { return data_[static_cast<size_t>(i * cols_ + j)]; }
+  double& operator()(Index i, Index j) {
+    ++version_;
+    return data_[static_cast<size_t>(i * cols_ + j)];
+  }
   double operator()(Index i, Index j) const {
     return data_[static_cast<size_t>(i * cols_ + j)];
   }
-  double* data() { return data_.data(); }
+  double* data() {
+    ++version_;
+    return data_.data();
+  }
   const double* data() const { return data_.data(); }
   void set_zero();
 
+  std::uint64_t id() const { return id_; }
+  std::uint64_t version() const { return version_; }
+
  private:
+  static std::uint64_t next_id() {
+    static std::atomic<std::uint64_t> n{1};
+    return n.fetch_add(1, std::memory_order_relaxed);
+  }
+  void touch() {
+    id_ = next_id();
+    version_ = 0;
+  }
   Index rows_ = 0, cols_ = 0;
   std::vector<double> data_;
+  std::uint64_t id_ = 0;
+  std::uint64_t version_ = 0;
 };
 
 struct MlpShape {
@@ -163,6 +221,17 @@ void run_stage1(VariantTag variant, const Matrix& x, const MlpWeights& w,
 Matrix run_variant(const KernelConfig& config, const Matrix& x,
                    const MlpWeights& w, Accounting mode = Accounting::IdealReuse);
 
+// Loop-order global read multiplicities of the fused executor
+// (fused.hpp:69-80, fused.cpp:218-239).  On the GPU the weight-stationary
+// raster is ColumnMajorTiling with one covering tile per CTA: weights are
+// read exactly once (asserted with ncu, tests/test_traffic_ncu.py).
+struct ReuseCounts {
+  std::uint64_t x_reads = 0;
+  std::uint64_t weight_reads = 0;  // W_up + W_gate combined
+  std::uint64_t a2_writes = 0;
+};
+ReuseCounts predicted_reuse_counts(const MlpShape& shape, const TileConfig& tile);
+
 // --- tensor parallelism (tp.hpp) ----------------------------------------------
 struct ColRange {
   Index begin = 0;
@@ -209,28 +278,101 @@ enum class CommModel { Logical, Ring };
 double comm_volume_bytes(const CollectiveLog& log, Index num_devices,
                          CommModel model, std::uint64_t bytes_per_element = 2);
 
-// --- scheduler (tuner.hpp) ------------------------------------------------------
-// GPU ScheduleEntry: the chosen label and the JSON of every profiled
-// candidate (the reference's BenchmarkResult list, tuner.hpp:28-50).
+// --- scheduler (tuner.hpp:26-137) ---------------------------------------------
+// Profile-driven kernel scheduler with the reference's contract: candidates
+// run strictly sequentially on seeded data (x filled first, then
+// make_random_weights), one unmeasured gate run, `warmup` unmeasured runs,
+// `runs` measured runs (steady_clock around the stage-1 callable), lower
+// median; select = argmin median, ties to deeper fusion then label; the
+// decision persisted in the versioned JSON cache.
+//
+// GPU differences: stage 1 runs in bf16 with fp32 accumulation, so the gate
+// compares against the GPU four-kernel stage 1 with a RELATIVE bound,
+// max|A2 - A2_ref| <= kCorrectnessGateTolerance * max|A2_ref|; and
+// gpu_candidates() offers the library's own launch configurations (kernel
+// family, ring stage size, stream-K chunks, cluster split-K, block kernel),
+// which make_runner / run_variant recognise by label.
+inline constexpr double kCorrectnessGateTolerance = 1e-2;
+
+struct BenchmarkResult {
+  std::string config_label;
+  VariantTag variant = VariantTag::Fused;
+  std::vector<std::int64_t> samples_ns;
+  std::int64_t median_ns = 0;  // exact lower median of samples_ns
+  int warmup_runs = 0;
+  int measured_runs = 0;
+  std::optional<std::string> disqualified;
+  bool operator==(const BenchmarkResult&) const = default;
+};
+
 struct ScheduleEntry {
   MlpShape shape;
   std::string fingerprint;
-  std::string chosen;
-  std::string results_json;
-  bool from_cache = false;
+  std::string chosen;  // label of the selected candidate
+  std::vector<BenchmarkResult> all_results;
+  std::string created_at;  // ISO-8601 UTC
+  bool operator==(const ScheduleEntry&) const = default;
 };
 
+// FourKernel, TwoKernel and the reference's fused tile grid
+// {tile_m in {1, B}} x {tile_n in {32, 128, d_ff}} x {tile_k in {32, d_model}}
+// x both loop orders, deduplicated after clamping (tuner.cpp:59-88).  On the
+// GPU every fused tile maps to the same kernels (the tile is a hint).
+std::vector<KernelConfig> default_candidates(const MlpShape& shape);
+// The GPU launch-configuration grid for this shape (dfk_candidates_shape):
+// the unfused cuBLASLt layouts plus every fused kernel configuration, each
+// labelled with the library's label.
+std::vector<KernelConfig> gpu_candidates(const MlpShape& shape);
+
+struct CandidateRunner {
+  KernelConfig config;
+  std::function<void(const Matrix&, const MlpWeights&, Matrix&)> stage1;
+};
+CandidateRunner make_runner(const KernelConfig& config);
+std::vector<CandidateRunner> make_runners(const std::vector<KernelConfig>& configs);
+
+struct ProfileOptions {
+  int warmup = 1;          // >= 1
+  int runs = 4;            // >= 3
+  std::uint64_t seed = 0;  // fixed random data, identical across candidates
+};
+
+std::vector<BenchmarkResult> profile(const std::vector<CandidateRunner>& cands,
+                                     const MlpShape& shape, const ProfileOptions& opts);
+std::vector<BenchmarkResult> profile(const std::vector<KernelConfig>& configs,
+                                     const MlpShape& shape, const ProfileOptions& opts);
+
+// Throws std::runtime_error when every candidate is disqualified.
+ScheduleEntry select(const MlpShape& shape, const std::string& fingerprint,
+                     const std::vector<BenchmarkResult>& results);
+
+inline constexpr int kCacheFormatVersion = 1;
+inline constexpr const char* kCacheEnvVar = "DEEPFUSION_CACHE";
+
+struct CacheError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// The library's tuning cache (dfk_cache_store / dfk_cache_lookup: atomic
+// replace, safe across threads and processes), reference schema.
+void cache_store(const ScheduleEntry& entry, const std::filesystem::path& path);
+std::optional<ScheduleEntry> cache_lookup(const MlpShape& shape,
+                                          const std::string& fingerprint,
+                                          const std::filesystem::path& path);
+
+// GPU descriptor: name, SM count, memory clock, driver (dfk_fingerprint).
 std::string default_fingerprint();
 
 class Tuner {
  public:
   struct Options {
-    std::string cache_path;  // empty = in-memory only
-    int warmup = 1;          // >= 1
-    int runs = 4;            // >= 3
+    std::filesystem::path cache_path;  // empty disables the cache
+    std::string fingerprint;
+    ProfileOptions profile;
   };
   explicit Tuner(Options opts) : opts_(std::move(opts)) {}
-  ScheduleEntry get_or_tune(const MlpShape& shape, const MlpWeights& w);
+  ScheduleEntry get_or_tune(const MlpShape& shape,
+                            const std::vector<KernelConfig>& candidates);
   int profile_invocations() const { return profile_invocations_; }
   bool last_was_cache_hit() const { return last_was_cache_hit_; }
 
@@ -240,7 +382,43 @@ class Tuner {
   bool last_was_cache_hit_ = false;
 };
 
-// Drops every cached GPU weight pack (e.g. after mutating weights in place).
+// The library's own on-device scheduler for real weights (dfk_tune: CUDA-
+// event timing, cold L2): picks the launch configuration later NULL-config
+// calls with this batch use; the entry's results carry per-candidate
+// samples.  cache_path empty = in memory only.
+ScheduleEntry tune_on_device(const MlpShape& shape, const MlpWeights& w,
+                             const std::filesystem::path& cache_path = {},
+                             int warmup = 1, int runs = 4);
+
+// Packs kept resident on the GPU (least recently used evicted beyond it).
+inline constexpr int kGpuCachedWeightSets = 8;
+// Drops every cached GPU weight pack.
 void release_gpu_cache();
+
+namespace verification {
+// Negative controls of the fused stage 1 (verification.hpp:27-53): a correct
+// build passes every check, each mutant must trip one.
+enum class Mutant { None, SiluPerKChunk, MaterializeIntermediate };
+std::optional<Mutant> mutant_from_string(std::string_view s);
+
+using FusedStage1Fn = std::function<void(const Matrix& x, const Matrix& w_up,
+                                         const Matrix& w_gate, const TileConfig&,
+                                         Matrix& a2)>;
+FusedStage1Fn fused_stage1_for(Mutant mutant);
+
+// GPU kernel with the SiLU*up epilogue applied per K chunk of
+// ceil(tile_k / 64) 64-wide K blocks (stream-K pieces) instead of after the
+// full reduction: deviates whenever d_model spans more than one chunk.
+void fused_stage1_silu_per_k_chunk(const Matrix& x, const Matrix& w_up,
+                                   const Matrix& w_gate, const TileConfig& tile,
+                                   Matrix& a2);
+// GPU kernel that round-trips SiLU(A_gate) through a global (HBM) buffer
+// before the multiply: numerically correct, caught by the DRAM-write check.
+void fused_stage1_materializing(const Matrix& x, const Matrix& w_up,
+                                const Matrix& w_gate, const TileConfig& tile,
+                                Matrix& a2);
+
+double max_abs_diff(const Matrix& a, const Matrix& b);
+}  // namespace verification
 
 }  // namespace deepfusion

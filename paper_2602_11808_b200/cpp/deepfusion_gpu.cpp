@@ -1,14 +1,22 @@
 // deepfusion_gpu.cpp — the reference operator API (deepfusion.hpp) on top of
 // the B200 C ABI (include/dfk.h).  Host-side only: conversion of fp64
-// matrices to/from the device, weight-pack caching, exception mapping.  All
-// arithmetic runs in libdfk.so's sm_100a kernels; there is no CPU path.
+// matrices to/from the device, weight-pack caching, exception mapping, the
+// scheduler's reference-facing surface.  All arithmetic runs in libdfk.so's
+// sm_100a kernels; there is no CPU path.
 #include "deepfusion.hpp"
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
-#include <tuple>
+#include <ctime>
+#include <list>
 #include <mutex>
+#include <set>
 #include <sstream>
+#include <tuple>
+
+#include <json.hpp>
 
 #include "dfk.h"
 
@@ -20,6 +28,7 @@ namespace {
   const std::string msg = dfk_last_error();
   if (status == DFK_ERR_SHAPE) throw ShapeError(msg);
   if (status == DFK_ERR_INVALID) throw std::invalid_argument(msg);
+  if (status == DFK_ERR_CACHE) throw CacheError(msg);
   throw GpuError(status, msg);
 }
 
@@ -27,26 +36,42 @@ void check(int status) {
   if (status != DFK_OK) raise(status);
 }
 
-// One process-wide context per device (created on first use).
+// Device scratch of one context, grown on demand (never per call).
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(dfk_context c, size_t need) {
+    if (need > bytes) {
+      if (p) dfk_free(c, p);
+      p = nullptr;
+      bytes = 0;
+      check(dfk_malloc(c, need, &p));
+      bytes = need;
+    }
+    return p;
+  }
+};
+
+// One process-wide context per device (created on first use), its scratch,
+// and an LRU cache of prepacked weight sets keyed by the matrices' exact
+// contents (Matrix id + version, see deepfusion.hpp).
 struct Runtime {
   std::mutex mu;
   std::map<int, dfk_context> ctx;
-  struct WeightsKey {
-    const void* g;
-    const void* u;
-    const void* d;
+  std::map<int, Scratch> x_buf, a2_buf, y_buf;
+
+  struct Key {
+    std::uint64_t g_id, g_ver, u_id, u_ver, d_id, d_ver;
     Index dm, df, f0, f1;
     int device;
-    bool operator<(const WeightsKey& o) const {
-      return std::tie(g, u, d, dm, df, f0, f1, device) <
-             std::tie(o.g, o.u, o.d, o.dm, o.df, o.f0, o.f1, o.device);
+    bool operator<(const Key& o) const {
+      return std::tie(g_id, g_ver, u_id, u_ver, d_id, d_ver, dm, df, f0, f1, device) <
+             std::tie(o.g_id, o.g_ver, o.u_id, o.u_ver, o.d_id, o.d_ver, o.dm, o.df, o.f0,
+                      o.f1, o.device);
     }
   };
-  struct Cached {
-    dfk_weights h = nullptr;
-    std::uint64_t fingerprint = 0;
-  };
-  std::map<WeightsKey, Cached> weights;
+  // most recently used at the front
+  std::list<std::pair<Key, dfk_weights>> lru;
 
   dfk_context context(int device) {
     auto it = ctx.find(device);
@@ -63,143 +88,113 @@ Runtime& rt() {
   return *r;
 }
 
-std::uint64_t sample_fingerprint(const Matrix& m) {
-  std::uint64_t h = 1469598103934665603ULL ^ static_cast<std::uint64_t>(m.size());
-  const Index n = m.size();
-  const Index step = n > 256 ? n / 256 : 1;
-  for (Index i = 0; i < n; i += step) {
-    std::uint64_t b;
-    std::memcpy(&b, m.data() + i, 8);
-    h = (h ^ b) * 1099511628211ULL;
-  }
-  return h;
-}
+std::uint64_t id_of(const Matrix* m) { return m ? m->id() : 0; }
+std::uint64_t ver_of(const Matrix* m) { return m ? m->version() : 0; }
 
-// Device handle for (w_gate, w_up, w_down) restricted to [f0, f1) of d_ff.
-dfk_weights weights_for(const Matrix& w_gate, const Matrix& w_up,
-                        const Matrix& w_down, Index f0, Index f1,
-                        int device = 0) {
+// Device handle for (w_gate, w_up, w_down) restricted to [f0, f1) of d_ff;
+// w_gate/w_up or w_down may be null (stage-only sets).  Served from the
+// cache while the matrices are unchanged; caller holds rt().mu.
+dfk_weights weights_for_locked(const Matrix* w_gate, const Matrix* w_up,
+                               const Matrix* w_down, Index f0, Index f1, int device = 0) {
   Runtime& r = rt();
-  std::lock_guard<std::mutex> lk(r.mu);
-  const Index dm = w_gate.rows(), df = w_gate.cols();
-  Runtime::WeightsKey key{w_gate.data(), w_up.data(), w_down.data(), dm, df, f0,
-                          f1, device};
-  const std::uint64_t fp = sample_fingerprint(w_gate) ^
-                           (sample_fingerprint(w_up) * 3) ^
-                           (sample_fingerprint(w_down) * 7);
-  auto it = r.weights.find(key);
-  if (it != r.weights.end()) {
-    if (it->second.fingerprint == fp) return it->second.h;
-    dfk_weights_destroy(it->second.h);
-    r.weights.erase(it);
+  const Index dm = w_gate ? w_gate->rows() : w_down->cols();
+  const Index df = w_gate ? w_gate->cols() : w_down->rows();
+  const Runtime::Key key{id_of(w_gate), ver_of(w_gate), id_of(w_up), ver_of(w_up),
+                         id_of(w_down), ver_of(w_down), dm, df, f0, f1, device};
+  for (auto it = r.lru.begin(); it != r.lru.end(); ++it) {
+    if (!(it->first < key) && !(key < it->first)) {
+      r.lru.splice(r.lru.begin(), r.lru, it);
+      return it->second;
+    }
   }
   dfk_weights h = nullptr;
-  check(dfk_weights_create(r.context(device), w_gate.data(), w_up.data(),
-                           w_down.data(), dm, df, DFK_F64, DFK_HOST, f0, f1, &h));
-  r.weights[key] = {h, fp};
+  check(dfk_weights_create(r.context(device), w_gate ? w_gate->data() : nullptr,
+                           w_up ? w_up->data() : nullptr, w_down ? w_down->data() : nullptr,
+                           dm, df, DFK_F64, DFK_HOST, f0, f1, &h));
+  r.lru.emplace_front(key, h);
+  while (static_cast<int>(r.lru.size()) > kGpuCachedWeightSets) {
+    dfk_weights_destroy(r.lru.back().second);
+    r.lru.pop_back();
+  }
   return h;
 }
 
-// Uncached registration for calls whose weights are temporaries (stage 1
-// alone, down alone): destroyed with the guard.
-struct TempWeights {
-  dfk_weights h = nullptr;
-  TempWeights(const Matrix& g, const Matrix& u, const Matrix& d, Index f0, Index f1) {
-    check(dfk_weights_create(rt().context(0), g.data(), u.data(), d.data(), g.rows(),
-                             g.cols(), DFK_F64, DFK_HOST, f0, f1, &h));
-  }
-  ~TempWeights() { dfk_weights_destroy(h); }
-  TempWeights(const TempWeights&) = delete;
-  TempWeights& operator=(const TempWeights&) = delete;
-};
-
-std::vector<std::uint16_t> to_bf16(const Matrix& m) {
-  std::vector<std::uint16_t> out(static_cast<size_t>(m.size()));
-  for (Index i = 0; i < m.size(); ++i) {
-    float f = static_cast<float>(m.data()[i]);
+void to_bf16(const double* src, Index n, std::uint16_t* out) {
+  for (Index i = 0; i < n; ++i) {
+    float f = static_cast<float>(src[i]);
     std::uint32_t u;
     std::memcpy(&u, &f, 4);
     if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) {
-      out[static_cast<size_t>(i)] = static_cast<std::uint16_t>((u >> 16) | 0x40u);
+      out[i] = static_cast<std::uint16_t>((u >> 16) | 0x40u);
     } else {
       u += 0x7FFFu + ((u >> 16) & 1u);
-      out[static_cast<size_t>(i)] = static_cast<std::uint16_t>(u >> 16);
+      out[i] = static_cast<std::uint16_t>(u >> 16);
     }
   }
-  return out;
 }
 
-Matrix from_bf16(const std::vector<std::uint16_t>& v, Index rows, Index cols) {
-  Matrix m(rows, cols);
+void from_bf16(const std::uint16_t* v, Matrix& m) {
+  double* d = m.data();
   for (Index i = 0; i < m.size(); ++i) {
-    const std::uint32_t u = static_cast<std::uint32_t>(v[static_cast<size_t>(i)]) << 16;
+    const std::uint32_t u = static_cast<std::uint32_t>(v[i]) << 16;
     float f;
     std::memcpy(&f, &u, 4);
-    m.data()[i] = f;
+    d[i] = f;
   }
-  return m;
-}
-
-struct DevBuf {
-  dfk_context c;
-  void* p = nullptr;
-  DevBuf(dfk_context ctx, size_t bytes) : c(ctx) { check(dfk_malloc(c, bytes, &p)); }
-  ~DevBuf() { dfk_free(c, p); }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-};
-
-dfk_config variant_config(VariantTag v) {
-  dfk_config c;
-  std::memset(&c, 0, sizeof(c));
-  if (v == VariantTag::Fused) {
-    // Default fused launch (the scheduler's choice once tuned): ask for the
-    // library default by passing NULL; this copy is only used for the
-    // unfused variants.
-    c.variant = DFK_VARIANT_FUSED;
-  } else {
-    c.variant = v == VariantTag::TwoKernel ? DFK_VARIANT_TWO_KERNEL
-                                           : DFK_VARIANT_FOUR_KERNEL;
-  }
-  return c;
 }
 
 const dfk_config* cfg_ptr(VariantTag v, dfk_config* storage) {
-  if (v == VariantTag::Fused) return nullptr;
-  *storage = variant_config(v);
+  if (v == VariantTag::Fused) return nullptr;  // the scheduler's / library's pick
+  std::memset(storage, 0, sizeof(*storage));
+  storage->variant =
+      v == VariantTag::TwoKernel ? DFK_VARIANT_TWO_KERNEL : DFK_VARIANT_FOUR_KERNEL;
   return storage;
 }
 
-// Stage 1 through the ABI: A2 = (X W_up) * silu(X W_gate).
-void gpu_stage1(VariantTag v, const Matrix& x, const Matrix& w_up,
-                const Matrix& w_gate, const Matrix* w_down, Matrix& a2) {
-  const Index B = x.rows(), dm = x.cols(), df = w_up.cols();
-  std::unique_ptr<TempWeights> temp;
-  dfk_weights h = nullptr;
-  if (w_down) {
-    h = weights_for(w_gate, w_up, *w_down, 0, df);
-  } else {
-    temp = std::make_unique<TempWeights>(w_gate, w_up, Matrix(df, dm), 0, df);
-    h = temp->h;
-  }
+// The GPU launch configuration a KernelConfig names: one of
+// dfk_candidates_shape's labels (gpu_candidates), else the variant's default.
+bool gpu_config_for(const KernelConfig& k, Index B, Index dm, Index df, dfk_config* out) {
+  if (k.label.empty()) return false;
   dfk_context c = rt().context(0);
-  DevBuf xd(c, static_cast<size_t>(B * dm) * 2), ad(c, static_cast<size_t>(B * df) * 2);
-  const auto xb = to_bf16(x);
-  check(dfk_memcpy_h2d(c, xd.p, xb.data(), xb.size() * 2));
-  dfk_config storage;
-  check(dfk_stage1(c, h, xd.p, B, ad.p, cfg_ptr(v, &storage)));
-  std::vector<std::uint16_t> out(static_cast<size_t>(B * df));
-  check(dfk_memcpy_d2h(c, out.data(), ad.p, out.size() * 2));
-  check(dfk_context_sync(c));
-  a2 = from_bf16(out, B, df);
+  std::vector<dfk_config> all(256);
+  int32_t n = 0;
+  check(dfk_candidates_shape(c, B, dm, df, all.data(), static_cast<int32_t>(all.size()), &n));
+  for (int32_t i = 0; i < std::min<int32_t>(n, static_cast<int32_t>(all.size())); ++i) {
+    if (k.label == all[static_cast<size_t>(i)].label) {
+      *out = all[static_cast<size_t>(i)];
+      return true;
+    }
+  }
+  return false;
 }
 
-Matrix gpu_forward(VariantTag v, const Matrix& x, const MlpWeights& w) {
-  dfk_weights h = weights_for(w.w_gate, w.w_up, w.w_down, 0, w.shape.d_ff);
+// Stage 1 through the ABI: A2 = (X W_up) * silu(X W_gate).  `w_down` given:
+// the full set is cached (and shared with full-block calls).
+void gpu_stage1(const dfk_config* cfg, const Matrix& x, const Matrix& w_up,
+                const Matrix& w_gate, const Matrix* w_down, Matrix& a2) {
+  const Index B = x.rows(), dm = x.cols(), df = w_up.cols();
+  Runtime& r = rt();
+  std::lock_guard<std::mutex> lk(r.mu);
+  dfk_weights h = weights_for_locked(&w_gate, &w_up, w_down, 0, df);
+  dfk_context c = r.context(0);
+  void* xd = r.x_buf[0].get(c, static_cast<size_t>(B * dm) * 2);
+  void* ad = r.a2_buf[0].get(c, static_cast<size_t>(B * df) * 2);
+  std::vector<std::uint16_t> xb(static_cast<size_t>(B * dm)), out(static_cast<size_t>(B * df));
+  to_bf16(x.data(), B * dm, xb.data());
+  check(dfk_memcpy_h2d(c, xd, xb.data(), xb.size() * 2));
+  check(dfk_stage1(c, h, xd, B, ad, cfg));
+  check(dfk_memcpy_d2h(c, out.data(), ad, out.size() * 2));
+  check(dfk_context_sync(c));
+  from_bf16(out.data(), a2);
+}
+
+Matrix gpu_forward(const dfk_config* cfg, const Matrix& x, const MlpWeights& w) {
+  Runtime& r = rt();
+  std::lock_guard<std::mutex> lk(r.mu);
+  dfk_weights h = weights_for_locked(&w.w_gate, &w.w_up, &w.w_down, 0, w.shape.d_ff);
   Matrix y(x.rows(), w.shape.d_model);
-  dfk_config storage;
-  check(dfk_forward_host(rt().context(0), h, x.data(), DFK_F64, x.rows(), y.data(),
-                         DFK_F64, cfg_ptr(v, &storage)));
+  check(dfk_forward_host(r.context(0), h, x.data(), DFK_F64, x.rows(), y.data(), DFK_F64,
+                         cfg));
   return y;
 }
 
@@ -222,10 +217,28 @@ void check_stage1_output(const Matrix& x, const MlpWeights& w, const Matrix& a2)
   }
 }
 
+void check_fused_stage1_args(const Matrix& x, const Matrix& w_up, const Matrix& w_gate,
+                             const Matrix& a2) {
+  if (w_up.rows() != x.cols() || w_gate.rows() != x.cols() ||
+      w_up.cols() != w_gate.cols()) {
+    std::ostringstream msg;
+    msg << "run_fused_stage1: inconsistent dims, x is " << x.rows() << "x" << x.cols()
+        << ", w_up is " << w_up.rows() << "x" << w_up.cols() << ", w_gate is "
+        << w_gate.rows() << "x" << w_gate.cols();
+    throw ShapeError(msg.str());
+  }
+  if (a2.rows() != x.rows() || a2.cols() != w_up.cols()) {
+    std::ostringstream msg;
+    msg << "run_fused_stage1: a2 is " << a2.rows() << "x" << a2.cols() << ", expected "
+        << x.rows() << "x" << w_up.cols();
+    throw ShapeError(msg.str());
+  }
+}
+
 }  // namespace
 
 // --- Matrix / shapes / generator ------------------------------------------------
-Matrix::Matrix(Index rows, Index cols) : rows_(rows), cols_(cols) {
+Matrix::Matrix(Index rows, Index cols) : rows_(rows), cols_(cols), id_(next_id()) {
   if (rows < 1 || cols < 1) {
     std::ostringstream msg;
     msg << "Matrix: dimensions must be >= 1, got " << rows << "x" << cols;
@@ -240,7 +253,10 @@ Matrix Matrix::identity(Index n) {
   return m;
 }
 
-void Matrix::set_zero() { std::fill(data_.begin(), data_.end(), 0.0); }
+void Matrix::set_zero() {
+  ++version_;
+  std::fill(data_.begin(), data_.end(), 0.0);
+}
 
 void MlpShape::validate() const {
   if (batch < 1 || d_model < 1 || d_ff < 1)
@@ -338,26 +354,31 @@ void run_four_kernel_stage1(const Matrix& x, const MlpWeights& w, Matrix& a2,
                             Accounting) {
   check_input(x, w);
   check_stage1_output(x, w, a2);
-  gpu_stage1(VariantTag::FourKernel, x, w.w_up, w.w_gate, &w.w_down, a2);
+  dfk_config storage;
+  gpu_stage1(cfg_ptr(VariantTag::FourKernel, &storage), x, w.w_up, w.w_gate, &w.w_down, a2);
 }
 
 Matrix run_four_kernel(const Matrix& x, const MlpWeights& w, Accounting) {
   check_input(x, w);
-  return gpu_forward(VariantTag::FourKernel, x, w);
+  dfk_config storage;
+  return gpu_forward(cfg_ptr(VariantTag::FourKernel, &storage), x, w);
 }
 
 void run_two_kernel_stage1(const Matrix& x, const MlpWeights& w, Matrix& a2,
                            Accounting) {
   check_input(x, w);
   check_stage1_output(x, w, a2);
-  gpu_stage1(VariantTag::TwoKernel, x, w.w_up, w.w_gate, &w.w_down, a2);
+  dfk_config storage;
+  gpu_stage1(cfg_ptr(VariantTag::TwoKernel, &storage), x, w.w_up, w.w_gate, &w.w_down, a2);
 }
 
 Matrix run_two_kernel(const Matrix& x, const MlpWeights& w, Accounting) {
   check_input(x, w);
-  return gpu_forward(VariantTag::TwoKernel, x, w);
+  dfk_config storage;
+  return gpu_forward(cfg_ptr(VariantTag::TwoKernel, &storage), x, w);
 }
 
+// Y = A2 W_down with a down-only weight set (cached like every other set).
 Matrix down_projection(const Matrix& a2, const Matrix& w_down, Accounting) {
   if (a2.cols() != w_down.rows()) {
     std::ostringstream msg;
@@ -366,46 +387,37 @@ Matrix down_projection(const Matrix& a2, const Matrix& w_down, Accounting) {
     throw ShapeError(msg.str());
   }
   const Index B = a2.rows(), df = a2.cols(), dm = w_down.cols();
-  const Matrix zeros(dm, df);
-  TempWeights temp(zeros, zeros, w_down, 0, df);
-  dfk_weights h = temp.h;
-  dfk_context c = rt().context(0);
-  DevBuf ad(c, static_cast<size_t>(B * df) * 2), yd(c, static_cast<size_t>(B * dm) * 4);
-  const auto ab = to_bf16(a2);
-  check(dfk_memcpy_h2d(c, ad.p, ab.data(), ab.size() * 2));
-  check(dfk_down(c, h, ad.p, B, yd.p, DFK_F32, nullptr));
+  Runtime& r = rt();
+  std::lock_guard<std::mutex> lk(r.mu);
+  dfk_weights h = weights_for_locked(nullptr, nullptr, &w_down, 0, df);
+  dfk_context c = r.context(0);
+  void* ad = r.a2_buf[0].get(c, static_cast<size_t>(B * df) * 2);
+  void* yd = r.y_buf[0].get(c, static_cast<size_t>(B * dm) * 4);
+  std::vector<std::uint16_t> ab(static_cast<size_t>(B * df));
+  to_bf16(a2.data(), B * df, ab.data());
+  check(dfk_memcpy_h2d(c, ad, ab.data(), ab.size() * 2));
+  check(dfk_down(c, h, ad, B, yd, DFK_F32, nullptr));
   std::vector<float> out(static_cast<size_t>(B * dm));
-  check(dfk_memcpy_d2h(c, out.data(), yd.p, out.size() * 4));
+  check(dfk_memcpy_d2h(c, out.data(), yd, out.size() * 4));
   check(dfk_context_sync(c));
   Matrix y(B, dm);
-  for (Index i = 0; i < y.size(); ++i) y.data()[i] = out[static_cast<size_t>(i)];
+  double* yv = y.data();
+  for (Index i = 0; i < y.size(); ++i) yv[i] = out[static_cast<size_t>(i)];
   return y;
 }
 
+// Stage 1 with a stage-1-only weight set (W_up, W_gate; cached).
 void run_fused_stage1(const Matrix& x, const Matrix& w_up, const Matrix& w_gate,
                       const TileConfig& tile, Matrix& a2, int) {
   tile.validate();
-  if (w_up.rows() != x.cols() || w_gate.rows() != x.cols() ||
-      w_up.cols() != w_gate.cols()) {
-    std::ostringstream msg;
-    msg << "run_fused_stage1: inconsistent dims, x is " << x.rows() << "x" << x.cols()
-        << ", w_up is " << w_up.rows() << "x" << w_up.cols() << ", w_gate is "
-        << w_gate.rows() << "x" << w_gate.cols();
-    throw ShapeError(msg.str());
-  }
-  if (a2.rows() != x.rows() || a2.cols() != w_up.cols()) {
-    std::ostringstream msg;
-    msg << "run_fused_stage1: a2 is " << a2.rows() << "x" << a2.cols()
-        << ", expected " << x.rows() << "x" << w_up.cols();
-    throw ShapeError(msg.str());
-  }
-  gpu_stage1(VariantTag::Fused, x, w_up, w_gate, nullptr, a2);
+  check_fused_stage1_args(x, w_up, w_gate, a2);
+  gpu_stage1(nullptr, x, w_up, w_gate, nullptr, a2);
 }
 
 Matrix run_fused(const Matrix& x, const MlpWeights& w, const TileConfig& tile, int) {
   check_input(x, w);
   tile.validate();
-  return gpu_forward(VariantTag::Fused, x, w);
+  return gpu_forward(nullptr, x, w);
 }
 
 void run_stage1(VariantTag variant, const Matrix& x, const MlpWeights& w, Matrix& a2,
@@ -425,6 +437,8 @@ void run_stage1(VariantTag variant, const Matrix& x, const MlpWeights& w, Matrix
   throw std::invalid_argument("run_stage1: unknown variant");
 }
 
+// A KernelConfig whose label is one of gpu_candidates() runs that launch
+// configuration; any other label runs the variant's default.
 Matrix run_variant(const KernelConfig& config, const Matrix& x, const MlpWeights& w,
                    Accounting) {
   check_input(x, w);
@@ -432,7 +446,32 @@ Matrix run_variant(const KernelConfig& config, const Matrix& x, const MlpWeights
   if (config.variant != VariantTag::Fused && config.variant != VariantTag::TwoKernel &&
       config.variant != VariantTag::FourKernel)
     throw std::invalid_argument("run_stage1: unknown variant");
-  return gpu_forward(config.variant, x, w);
+  dfk_config storage;
+  if (gpu_config_for(config, x.rows(), w.shape.d_model, w.shape.d_ff, &storage))
+    return gpu_forward(&storage, x, w);
+  return gpu_forward(cfg_ptr(config.variant, &storage), x, w);
+}
+
+ReuseCounts predicted_reuse_counts(const MlpShape& shape, const TileConfig& tile) {
+  shape.validate();
+  tile.validate();
+  const TileConfig t = tile.clamped(shape);
+  const auto B = static_cast<std::uint64_t>(shape.batch);
+  const auto dm = static_cast<std::uint64_t>(shape.d_model);
+  const auto df = static_cast<std::uint64_t>(shape.d_ff);
+  const auto blocks = [](std::uint64_t n, std::uint64_t b) { return (n + b - 1) / b; };
+  ReuseCounts r;
+  r.a2_writes = B * df;
+  if (t.loop_order == LoopOrder::ColumnMajorTiling) {
+    // weight strips resident, X re-staged once per column block
+    r.x_reads = B * dm * blocks(df, static_cast<std::uint64_t>(t.tile_n));
+    r.weight_reads = 2 * dm * df;
+  } else {
+    // X strips resident, weight strips re-staged once per row block
+    r.x_reads = B * dm;
+    r.weight_reads = 2 * dm * df * blocks(B, static_cast<std::uint64_t>(t.tile_m));
+  }
+  return r;
 }
 
 // --- tensor parallelism ------------------------------------------------------------
@@ -499,8 +538,13 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
   TpResult result;
   int ndev = 0;
   dfk_device_count(&ndev);
-  const auto xb = to_bf16(x);
-  if (plan.num_devices > 1 && plan.num_devices <= 8 && dm % 4 == 0 && B <= 256) {
+  std::vector<std::uint16_t> xb(static_cast<size_t>(x.size()));
+  to_bf16(x.data(), x.size(), xb.data());
+  // The fused all-reduce needs every rank on its balanced_ranges shard (the
+  // tile-completion count is derived from it); other plans run the shards
+  // in sequence below.
+  const bool balanced = plan.ff_ranges == balanced_ranges(w.shape.d_ff, plan.num_devices);
+  if (balanced && plan.num_devices > 1 && plan.num_devices <= 8 && dm % 4 == 0 && B <= 256) {
     // One context per rank -- on its own device when there are enough, else
     // all on device 0 (each rank's block on its own stream) -- with the
     // fused all-reduce: partial Y reduced over peer memory INSIDE the block
@@ -541,7 +585,7 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
     for (Index p = 0; p < plan.num_devices; ++p)
       check(dfk_tp_forward_fused(ctxs[static_cast<size_t>(p)], hs[static_cast<size_t>(p)],
                                  xs[static_cast<size_t>(p)], B,
-                                 static_cast<float*>(ys[static_cast<size_t>(p)]), cfg));
+                                 ys[static_cast<size_t>(p)], DFK_F32, cfg));
     std::vector<float> out(static_cast<size_t>(B * dm));
     for (Index p = 0; p < plan.num_devices; ++p) check(dfk_context_sync(ctxs[static_cast<size_t>(p)]));
     for (Index p = 0; p < plan.num_devices; ++p) {
@@ -551,11 +595,13 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
       check(dfk_memcpy_d2h(c, a.data(), as[static_cast<size_t>(p)], a.size() * 2));
       if (p == 0) check(dfk_memcpy_d2h(c, out.data(), ys[0], out.size() * 4));
       check(dfk_context_sync(c));
-      result.stage1_shards.push_back(from_bf16(a, B, r.size()));
+      Matrix shard(B, r.size());
+      from_bf16(a.data(), shard);
+      result.stage1_shards.push_back(std::move(shard));
     }
     result.output = Matrix(B, dm);
-    for (Index i = 0; i < result.output.size(); ++i)
-      result.output.data()[i] = out[static_cast<size_t>(i)];
+    double* ov = result.output.data();
+    for (Index i = 0; i < result.output.size(); ++i) ov[i] = out[static_cast<size_t>(i)];
     for (Index p = 0; p < plan.num_devices; ++p) {
       dfk_context c = ctxs[static_cast<size_t>(p)];
       dfk_free(c, xs[static_cast<size_t>(p)]);
@@ -568,23 +614,28 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
     // Shapes the fused all-reduce does not take (d_model % 4, B > 256, more
     // than 8 ranks): shards in sequence on one GPU, fp32 partials summed in
     // device order.
-    dfk_context c = rt().context(0);
-    DevBuf xd(c, xb.size() * 2), yd(c, static_cast<size_t>(B * dm) * 4);
-    check(dfk_memcpy_h2d(c, xd.p, xb.data(), xb.size() * 2));
+    Runtime& rr = rt();
+    std::lock_guard<std::mutex> lk(rr.mu);
+    dfk_context c = rr.context(0);
+    void* xd = rr.x_buf[0].get(c, xb.size() * 2);
+    void* yd = rr.y_buf[0].get(c, static_cast<size_t>(B * dm) * 4);
+    check(dfk_memcpy_h2d(c, xd, xb.data(), xb.size() * 2));
     result.output = Matrix(B, dm);
+    double* ov = result.output.data();
     std::vector<float> part(static_cast<size_t>(B * dm));
     for (const ColRange& r : plan.ff_ranges) {
-      dfk_weights h = weights_for(w.w_gate, w.w_up, w.w_down, r.begin, r.end);
-      DevBuf ad(c, static_cast<size_t>(B * r.size()) * 2);
-      check(dfk_stage1(c, h, xd.p, B, ad.p, cfg));
-      check(dfk_down(c, h, ad.p, B, yd.p, DFK_F32, cfg));
+      dfk_weights h = weights_for_locked(&w.w_gate, &w.w_up, &w.w_down, r.begin, r.end);
+      void* ad = rr.a2_buf[0].get(c, static_cast<size_t>(B * r.size()) * 2);
+      check(dfk_stage1(c, h, xd, B, ad, cfg));
+      check(dfk_down(c, h, ad, B, yd, DFK_F32, cfg));
       std::vector<std::uint16_t> a(static_cast<size_t>(B * r.size()));
-      check(dfk_memcpy_d2h(c, a.data(), ad.p, a.size() * 2));
-      check(dfk_memcpy_d2h(c, part.data(), yd.p, part.size() * 4));
+      check(dfk_memcpy_d2h(c, a.data(), ad, a.size() * 2));
+      check(dfk_memcpy_d2h(c, part.data(), yd, part.size() * 4));
       check(dfk_context_sync(c));
-      result.stage1_shards.push_back(from_bf16(a, B, r.size()));
-      for (Index i = 0; i < result.output.size(); ++i)
-        result.output.data()[i] += part[static_cast<size_t>(i)];
+      Matrix shard(B, r.size());
+      from_bf16(a.data(), shard);
+      result.stage1_shards.push_back(std::move(shard));
+      for (Index i = 0; i < result.output.size(); ++i) ov[i] += part[static_cast<size_t>(i)];
     }
   }
   result.log.events.push_back(
@@ -612,33 +663,370 @@ double comm_volume_bytes(const CollectiveLog& log, Index num_devices, CommModel 
 }
 
 // --- scheduler -------------------------------------------------------------------
+namespace {
+
+using nlohmann::json;
+
+int variant_rank(VariantTag v) {  // deeper fusion first on ties (tuner.cpp:23-30)
+  return v == VariantTag::Fused ? 0 : v == VariantTag::TwoKernel ? 1 : 2;
+}
+
+std::string utc_now() {
+  const std::time_t t = std::chrono::system_clock::to_time_t(std::chrono::system_clock::now());
+  std::tm u{};
+  gmtime_r(&t, &u);
+  char b[32];
+  std::strftime(b, sizeof(b), "%Y-%m-%dT%H:%M:%SZ", &u);
+  return b;
+}
+
+// max|a - ref| / max|ref| (max|a - ref| when ref is all zero).
+double rel_inf(const Matrix& a, const Matrix& ref) {
+  double num = 0.0, den = 0.0;
+  for (Index i = 0; i < a.size(); ++i) {
+    const double d = std::fabs(a.data()[i] - ref.data()[i]);
+    num = std::isnan(d) ? INFINITY : std::max(num, d);
+    den = std::max(den, std::fabs(ref.data()[i]));
+  }
+  return den > 0 ? num / den : num;
+}
+
+// ScheduleEntry <-> the cache schema (tuner.cpp:198-266 field names).
+json entry_to_json(const ScheduleEntry& e) {
+  json results = json::array();
+  for (const BenchmarkResult& r : e.all_results) {
+    json j = {{"label", r.config_label},
+              {"variant", std::string(to_string(r.variant))},
+              {"samples_ns", r.samples_ns},
+              {"median_ns", r.median_ns},
+              {"warmup_runs", r.warmup_runs},
+              {"measured_runs", r.measured_runs}};
+    if (r.disqualified) j["disqualified"] = *r.disqualified;
+    results.push_back(std::move(j));
+  }
+  return {{"shape", {{"batch", e.shape.batch}, {"d_model", e.shape.d_model},
+                     {"d_ff", e.shape.d_ff}}},
+          {"fingerprint", e.fingerprint},
+          {"chosen", e.chosen},
+          {"created_at", e.created_at},
+          {"results", std::move(results)}};
+}
+
+ScheduleEntry entry_from_json(const json& j, const std::string& where) {
+  const auto need = [&](const json& o, const char* k) -> const json& {
+    auto it = o.find(k);
+    if (it == o.end()) throw CacheError(where + ": entry has no '" + k + "'");
+    return *it;
+  };
+  try {
+    ScheduleEntry e;
+    const json& sh = need(j, "shape");
+    e.shape = {need(sh, "batch").get<Index>(), need(sh, "d_model").get<Index>(),
+               need(sh, "d_ff").get<Index>()};
+    e.fingerprint = need(j, "fingerprint").get<std::string>();
+    e.chosen = need(j, "chosen").get<std::string>();
+    e.created_at = need(j, "created_at").get<std::string>();
+    for (const json& r : need(j, "results")) {
+      BenchmarkResult b;
+      b.config_label = need(r, "label").get<std::string>();
+      const auto v = variant_from_string(need(r, "variant").get<std::string>());
+      if (!v) throw CacheError(where + ": unknown variant name in a result");
+      b.variant = *v;
+      b.samples_ns = need(r, "samples_ns").get<std::vector<std::int64_t>>();
+      b.median_ns = need(r, "median_ns").get<std::int64_t>();
+      b.warmup_runs = need(r, "warmup_runs").get<int>();
+      b.measured_runs = need(r, "measured_runs").get<int>();
+      if (auto d = r.find("disqualified"); d != r.end()) b.disqualified = d->get<std::string>();
+      e.all_results.push_back(std::move(b));
+    }
+    return e;
+  } catch (const json::exception& ex) {
+    throw CacheError(where + ": malformed entry (" + ex.what() + ")");
+  }
+}
+
+}  // namespace
+
+std::vector<KernelConfig> default_candidates(const MlpShape& shape) {
+  shape.validate();
+  std::vector<KernelConfig> out = {{VariantTag::FourKernel, {}, "four_kernel"},
+                                   {VariantTag::TwoKernel, {}, "two_kernel"}};
+  std::set<std::tuple<Index, Index, Index, LoopOrder>> seen;
+  for (Index tm : {Index{1}, shape.batch})
+    for (Index tn : {Index{32}, Index{128}, shape.d_ff})
+      for (Index tk : {Index{32}, shape.d_model})
+        for (LoopOrder o : {LoopOrder::RowMajorTiling, LoopOrder::ColumnMajorTiling}) {
+          const TileConfig t = TileConfig{tm, tn, tk, o}.clamped(shape);
+          if (seen.emplace(t.tile_m, t.tile_n, t.tile_k, o).second)
+            out.push_back({VariantTag::Fused, t, "fused_" + t.describe()});
+        }
+  return out;
+}
+
+std::vector<KernelConfig> gpu_candidates(const MlpShape& shape) {
+  shape.validate();
+  std::vector<dfk_config> all(256);
+  int32_t n = 0;
+  {
+    std::lock_guard<std::mutex> lk(rt().mu);
+    check(dfk_candidates_shape(rt().context(0), shape.batch, shape.d_model, shape.d_ff,
+                               all.data(), static_cast<int32_t>(all.size()), &n));
+  }
+  std::vector<KernelConfig> out;
+  for (int32_t i = 0; i < std::min<int32_t>(n, static_cast<int32_t>(all.size())); ++i) {
+    const dfk_config& c = all[static_cast<size_t>(i)];
+    const VariantTag v = c.variant == DFK_VARIANT_TWO_KERNEL    ? VariantTag::TwoKernel
+                         : c.variant == DFK_VARIANT_FOUR_KERNEL ? VariantTag::FourKernel
+                                                                : VariantTag::Fused;
+    out.push_back({v, TileConfig{shape.batch, shape.d_ff, shape.d_model}, c.label});
+  }
+  return out;
+}
+
+CandidateRunner make_runner(const KernelConfig& config) {
+  return {config, [config](const Matrix& x, const MlpWeights& w, Matrix& a2) {
+            check_input(x, w);
+            check_stage1_output(x, w, a2);
+            dfk_config c;
+            if (gpu_config_for(config, x.rows(), w.shape.d_model, w.shape.d_ff, &c)) {
+              gpu_stage1(&c, x, w.w_up, w.w_gate, &w.w_down, a2);
+            } else {
+              run_stage1(config.variant, x, w, a2, config.tile);
+            }
+          }};
+}
+
+std::vector<CandidateRunner> make_runners(const std::vector<KernelConfig>& configs) {
+  std::vector<CandidateRunner> out;
+  out.reserve(configs.size());
+  for (const KernelConfig& c : configs) out.push_back(make_runner(c));
+  return out;
+}
+
+std::vector<BenchmarkResult> profile(const std::vector<CandidateRunner>& cands,
+                                     const MlpShape& shape, const ProfileOptions& opts) {
+  if (opts.warmup < 1) throw std::invalid_argument("profile: warmup must be >= 1");
+  if (opts.runs < 3) throw std::invalid_argument("profile: runs must be >= 3");
+  shape.validate();
+  // Seeded data, identical across candidates: X first, then the weights
+  // (tuner.cpp:117-120 fill order).
+  std::mt19937_64 rng(opts.seed);
+  Matrix x(shape.batch, shape.d_model);
+  fill_uniform(x, rng);
+  const MlpWeights w = make_random_weights(shape, rng);
+  Matrix ref(shape.batch, shape.d_ff);
+  run_four_kernel_stage1(x, w, ref);  // the gate's reference (tuner.cpp:122-123)
+
+  std::vector<BenchmarkResult> results;
+  results.reserve(cands.size());
+  for (const CandidateRunner& cand : cands) {
+    BenchmarkResult res;
+    res.config_label = cand.config.label;
+    res.variant = cand.config.variant;
+    res.warmup_runs = opts.warmup;
+    Matrix a2(shape.batch, shape.d_ff);
+    cand.stage1(x, w, a2);  // gate, unmeasured
+    const double dev = rel_inf(a2, ref);
+    if (!(dev <= kCorrectnessGateTolerance)) {
+      std::ostringstream why;
+      why << "output deviates from the four-kernel reference by " << dev
+          << " relative (gate " << kCorrectnessGateTolerance << ")";
+      res.disqualified = why.str();
+      results.push_back(std::move(res));
+      continue;
+    }
+    for (int i = 0; i < opts.warmup; ++i) cand.stage1(x, w, a2);
+    for (int i = 0; i < opts.runs; ++i) {
+      const auto t0 = std::chrono::steady_clock::now();
+      cand.stage1(x, w, a2);
+      const auto t1 = std::chrono::steady_clock::now();
+      res.samples_ns.push_back(
+          std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+    }
+    res.measured_runs = opts.runs;
+    std::vector<std::int64_t> s = res.samples_ns;
+    std::sort(s.begin(), s.end());
+    res.median_ns = s[(s.size() - 1) / 2];  // lower median (tuner.cpp:32-35)
+    results.push_back(std::move(res));
+  }
+  return results;
+}
+
+std::vector<BenchmarkResult> profile(const std::vector<KernelConfig>& configs,
+                                     const MlpShape& shape, const ProfileOptions& opts) {
+  return profile(make_runners(configs), shape, opts);
+}
+
+ScheduleEntry select(const MlpShape& shape, const std::string& fingerprint,
+                     const std::vector<BenchmarkResult>& results) {
+  const BenchmarkResult* best = nullptr;
+  const auto rank = [](const BenchmarkResult& r) {
+    return std::make_tuple(r.median_ns, variant_rank(r.variant), std::cref(r.config_label));
+  };
+  for (const BenchmarkResult& r : results)
+    if (!r.disqualified && (!best || rank(r) < rank(*best))) best = &r;
+  if (!best)
+    throw std::runtime_error("select: no candidate passed the correctness gate");
+  return {shape, fingerprint, best->config_label, results, utc_now()};
+}
+
+void cache_store(const ScheduleEntry& entry, const std::filesystem::path& path) {
+  const std::string text = entry_to_json(entry).dump();
+  check(dfk_cache_store(path.c_str(), text.c_str()));
+}
+
+std::optional<ScheduleEntry> cache_lookup(const MlpShape& shape,
+                                          const std::string& fingerprint,
+                                          const std::filesystem::path& path) {
+  size_t need = 0;
+  int32_t found = 0;
+  check(dfk_cache_lookup(path.c_str(), shape.batch, shape.d_model, shape.d_ff,
+                         fingerprint.c_str(), nullptr, 0, &need, &found));
+  if (!found) return std::nullopt;
+  std::string buf(need, '\0');
+  check(dfk_cache_lookup(path.c_str(), shape.batch, shape.d_model, shape.d_ff,
+                         fingerprint.c_str(), buf.data(), buf.size(), &need, &found));
+  if (!found) return std::nullopt;  // replaced between the two reads: a miss
+  buf.resize(std::strlen(buf.c_str()));
+  const json j = json::parse(buf, nullptr, false);
+  if (j.is_discarded()) throw CacheError("tuning cache " + path.string() + ": bad entry");
+  return entry_from_json(j, "tuning cache " + path.string());
+}
+
 std::string default_fingerprint() {
   char buf[256];
+  std::lock_guard<std::mutex> lk(rt().mu);
   check(dfk_fingerprint(rt().context(0), buf, sizeof(buf)));
   return buf;
 }
 
-ScheduleEntry Tuner::get_or_tune(const MlpShape& shape, const MlpWeights& w) {
+ScheduleEntry Tuner::get_or_tune(const MlpShape& shape,
+                                 const std::vector<KernelConfig>& candidates) {
+  if (!opts_.cache_path.empty()) {
+    if (auto hit = cache_lookup(shape, opts_.fingerprint, opts_.cache_path)) {
+      last_was_cache_hit_ = true;
+      return *hit;
+    }
+  }
+  last_was_cache_hit_ = false;
+  ++profile_invocations_;
+  ScheduleEntry e = select(shape, opts_.fingerprint, profile(candidates, shape, opts_.profile));
+  if (!opts_.cache_path.empty()) cache_store(e, opts_.cache_path);
+  return e;
+}
+
+ScheduleEntry tune_on_device(const MlpShape& shape, const MlpWeights& w,
+                             const std::filesystem::path& cache_path, int warmup, int runs) {
   w.validate();
-  if (opts_.warmup < 1) throw std::invalid_argument("profile: warmup must be >= 1");
-  if (opts_.runs < 3) throw std::invalid_argument("profile: runs must be >= 3");
-  dfk_weights h = weights_for(w.w_gate, w.w_up, w.w_down, 0, w.shape.d_ff);
+  if (shape.d_model != w.shape.d_model || shape.d_ff != w.shape.d_ff)
+    throw ShapeError("tune_on_device: shape and weights disagree");
+  if (warmup < 1) throw std::invalid_argument("profile: warmup must be >= 1");
+  if (runs < 3) throw std::invalid_argument("profile: runs must be >= 3");
+  Runtime& r = rt();
+  std::lock_guard<std::mutex> lk(r.mu);
+  dfk_weights h = weights_for_locked(&w.w_gate, &w.w_up, &w.w_down, 0, w.shape.d_ff);
   dfk_config chosen;
   int32_t hit = 0;
-  std::vector<char> json(1 << 16);
-  check(dfk_tune(rt().context(0), h, shape.batch,
-                 opts_.cache_path.empty() ? nullptr : opts_.cache_path.c_str(),
-                 opts_.warmup, opts_.runs, &chosen, &hit, json.data(), json.size()));
-  last_was_cache_hit_ = hit != 0;
-  if (!hit) ++profile_invocations_;
-  return {shape, default_fingerprint(), chosen.label, json.data(), hit != 0};
+  std::string out(1 << 20, '\0');
+  check(dfk_tune(r.context(0), h, shape.batch,
+                 cache_path.empty() ? nullptr : cache_path.c_str(), warmup, runs, &chosen,
+                 &hit, out.data(), out.size()));
+  out.resize(std::strlen(out.c_str()));
+  const json j = json::parse(out, nullptr, false);
+  ScheduleEntry e;
+  e.shape = shape;
+  e.chosen = chosen.label;
+  if (!j.is_discarded()) {
+    e.fingerprint = j.value("fingerprint", std::string());
+    e.created_at = j.value("created_at", std::string());
+    for (const json& rj : j.value("results", json::array())) {
+      BenchmarkResult b;
+      b.config_label = rj.value("label", std::string());
+      b.variant = variant_from_string(rj.value("variant", std::string("fused")))
+                      .value_or(VariantTag::Fused);
+      b.samples_ns = rj.value("samples_ns", std::vector<std::int64_t>{});
+      b.median_ns = rj.value("median_ns", std::int64_t{0});
+      b.warmup_runs = rj.value("warmup_runs", 0);
+      b.measured_runs = rj.value("measured_runs", 0);
+      if (rj.contains("disqualified")) b.disqualified = rj["disqualified"].get<std::string>();
+      e.all_results.push_back(std::move(b));
+    }
+  }
+  return e;
 }
 
 void release_gpu_cache() {
   Runtime& r = rt();
   std::lock_guard<std::mutex> lk(r.mu);
-  for (auto& [k, v] : r.weights) dfk_weights_destroy(v.h);
-  r.weights.clear();
+  for (auto& kv : r.lru) dfk_weights_destroy(kv.second);
+  r.lru.clear();
 }
+
+// --- verification seam (verification.hpp:27-53) -----------------------------------
+namespace verification {
+
+std::optional<Mutant> mutant_from_string(std::string_view s) {
+  if (s == "none") return Mutant::None;
+  if (s == "silu-per-k-chunk") return Mutant::SiluPerKChunk;
+  if (s == "materialize-intermediate") return Mutant::MaterializeIntermediate;
+  return std::nullopt;
+}
+
+FusedStage1Fn fused_stage1_for(Mutant mutant) {
+  switch (mutant) {
+    case Mutant::None:
+      return [](const Matrix& x, const Matrix& w_up, const Matrix& w_gate,
+                const TileConfig& tile, Matrix& a2) {
+        run_fused_stage1(x, w_up, w_gate, tile, a2);
+      };
+    case Mutant::SiluPerKChunk:
+      return &fused_stage1_silu_per_k_chunk;
+    case Mutant::MaterializeIntermediate:
+      return &fused_stage1_materializing;
+  }
+  throw std::invalid_argument("unknown mutant");
+}
+
+void fused_stage1_silu_per_k_chunk(const Matrix& x, const Matrix& w_up,
+                                   const Matrix& w_gate, const TileConfig& tile,
+                                   Matrix& a2) {
+  tile.validate();
+  check_fused_stage1_args(x, w_up, w_gate, a2);
+  const TileConfig t = tile.clamped({x.rows(), x.cols(), w_up.cols()});
+  dfk_config c;
+  std::memset(&c, 0, sizeof(c));
+  c.variant = DFK_VARIANT_FUSED;
+  c.s1_family = DFK_FAMILY_TC;
+  c.down_family = DFK_FAMILY_TC;
+  c.s1_split_k = 1;
+  c.dynamic_sched = 1;
+  c.s1_chunk_kb = static_cast<int32_t>(std::max<Index>(1, (t.tile_k + 63) / 64));
+  c.mutant = 1;
+  gpu_stage1(&c, x, w_up, w_gate, nullptr, a2);
+}
+
+void fused_stage1_materializing(const Matrix& x, const Matrix& w_up, const Matrix& w_gate,
+                                const TileConfig& tile, Matrix& a2) {
+  tile.validate();
+  check_fused_stage1_args(x, w_up, w_gate, a2);
+  dfk_config c;
+  std::memset(&c, 0, sizeof(c));
+  c.variant = DFK_VARIANT_FUSED;
+  c.s1_family = DFK_FAMILY_TC;
+  c.down_family = DFK_FAMILY_TC;
+  c.s1_split_k = 1;
+  c.mutant = 2;
+  gpu_stage1(&c, x, w_up, w_gate, nullptr, a2);
+}
+
+double max_abs_diff(const Matrix& a, const Matrix& b) {
+  if (a.rows() != b.rows() || a.cols() != b.cols())
+    throw ShapeError("max_abs_diff: shapes differ");
+  double m = 0.0;
+  for (Index i = 0; i < a.size(); ++i) m = std::max(m, std::fabs(a.data()[i] - b.data()[i]));
+  return m;
+}
+
+}  // namespace verification
 
 }  // namespace deepfusion

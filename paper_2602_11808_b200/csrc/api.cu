@@ -45,14 +45,14 @@ int fail(int status, const std::string& msg) {
 }
 
 void free_weights(dfk_weights_s* w) {
-  cudaFree(w->s1_pack);
-  cudaFree(w->dn_pack);
+  if (w->s1_pack) cudaFree(w->s1_pack);
+  if (w->dn_pack) cudaFree(w->dn_pack);
   if (w->cat_t) cudaFree(w->cat_t);
   if (w->down_t) cudaFree(w->down_t);
   delete w;
 }
 
-int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s) {
+int ensure_buf(dfk_context_s* ctx, DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return DFK_OK;
   if (b.p) {
@@ -61,6 +61,9 @@ int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s) {
     b.p = nullptr;
     b.bytes = 0;
   }
+  // Captured decode graphs bake buffer addresses in: any (re)allocation
+  // invalidates them (decode.cpp checks the generation before a replay).
+  ++ctx->generation;
   cudaError_t e = cudaMalloc(&b.p, bytes);
   if (e != cudaSuccess) {
     return fail(DFK_ERR_NOMEM, std::string("cudaMalloc(") +
@@ -211,7 +214,7 @@ int tma_operand(dfk_context_s* ctx, const void* p, int64_t rows, int64_t cols,
     return DFK_OK;
   }
   const int64_t ld2 = round_up(cols, 8);
-  DFK_TRY(ensure_buf(pad, static_cast<size_t>(rows * ld2 * 2), false,
+  DFK_TRY(ensure_buf(ctx, pad, static_cast<size_t>(rows * ld2 * 2), false,
                      ctx->stream));
   DFK_CUDA(launch_pad_rows(static_cast<const __nv_bfloat16*>(p), rows, cols,
                            ld, static_cast<__nv_bfloat16*>(pad.p), ld2,
@@ -269,7 +272,7 @@ const Knobs& knobs() {
 int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
                  int grid, StreamArgs* a, bool down_only = false) {
   if (!cfg.dynamic_sched) return DFK_OK;
-  DFK_TRY(ensure_buf(ctx->sched, 64, true, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->sched, 64, true, ctx->stream));
   a->dynamic = 1;
   a->sched = static_cast<int*>(ctx->sched.p);
   // 32-K-block (512 KiB) down chunks measured best on full-size weights; a
@@ -326,10 +329,10 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   }
   a->s1_chunk = s1c;
   if (s1c < w->s1_kblocks) {
-    DFK_TRY(ensure_buf(ctx->s1acc,
+    DFK_TRY(ensure_buf(ctx, ctx->s1acc,
                        static_cast<size_t>(w->s1_tiles) * a->n_pad * kBlockRows * 4,
                        true, ctx->stream));
-    DFK_TRY(ensure_buf(ctx->s1cnt, static_cast<size_t>(w->s1_tiles) * 4, true,
+    DFK_TRY(ensure_buf(ctx, ctx->s1cnt, static_cast<size_t>(w->s1_tiles) * 4, true,
                        ctx->stream));
     a->s1acc = static_cast<float*>(ctx->s1acc.p);
     a->s1cnt = static_cast<int*>(ctx->s1cnt.p);
@@ -383,6 +386,7 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk, a->a2_tma);
   a->trace = ctx->trace;
   if (a->trace) a->trace_s0 = knobs().trace_s0;
+  a->tp_error = ctx->err_dev;
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
   if (tc && sk == 1) {
@@ -397,11 +401,11 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
 }
 
 int ensure_down_workspace(dfk_context_s* ctx, dfk_weights_s* w, int64_t rows) {
-  DFK_TRY(ensure_buf(ctx->yacc,
+  DFK_TRY(ensure_buf(ctx, ctx->yacc,
                      static_cast<size_t>(rows) * w->dn_tiles * kDownCols *
                          sizeof(float),
                      true, ctx->stream));
-  return ensure_buf(ctx->counters, static_cast<size_t>(w->dn_tiles) * 4, true,
+  return ensure_buf(ctx, ctx->counters, static_cast<size_t>(w->dn_tiles) * 4, true,
                     ctx->stream);
 }
 
@@ -441,6 +445,11 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
     a.mutant = cfg.mutant;
+    if (cfg.mutant == 2) {
+      DFK_TRY(ensure_buf(ctx, ctx->mat_scratch, static_cast<size_t>(nb * w->d_ff) * 4, false,
+                         ctx->stream));
+      a.mat_scratch = static_cast<float*>(ctx->mat_scratch.p);
+    }
     const int sk = a.split_k;
     // Clusters of sk CTAs; as many clusters as keep every cluster at the
     // same tile count, never more than can be co-resident.
@@ -562,7 +571,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
   int64_t x_ld;
   DFK_TRY(tma_operand(ctx, x, B, w->d_model, w->d_model, ctx->xpad, &xp, &x_ld));
   DFK_TRY(ensure_down_workspace(ctx, w, std::min(L.chunk, B)));
-  DFK_TRY(ensure_buf(ctx->flags, static_cast<size_t>(w->s1_tiles) * 4, true,
+  DFK_TRY(ensure_buf(ctx, ctx->flags, static_cast<size_t>(w->s1_tiles) * 4, true,
                      ctx->stream));
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
@@ -582,12 +591,12 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
       a.tp_rank = tp->tp_rank;
       a.tp_size = tp->tp_size;
       a.tp_total_kb = tp->tp_total_kb;
-      a.tp_error = tp->tp_error;
       for (int r = 0; r < kMaxTp; ++r) {
         a.tp_yacc[r] = tp->tp_yacc[r];
         a.tp_cnt[r] = tp->tp_cnt[r];
         a.tp_done[r] = tp->tp_done[r];
-        a.tp_y[r] = tp->tp_y[r];
+        // the chunk's rows of every rank's Y (GEMV family: 8-row chunks)
+        a.tp_y[r] = tp->tp_y[r] ? tp->tp_y[r] + b0 * y_ld : nullptr;
       }
       a.yacc_ld = tp->yacc_ld;
     }
@@ -601,6 +610,11 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     if (++ctx->epoch == 0) ++ctx->epoch;
     a.epoch = ctx->epoch;
     a.mutant = cfg.mutant;
+    if (cfg.mutant == 2) {
+      DFK_TRY(ensure_buf(ctx, ctx->mat_scratch, static_cast<size_t>(nb * w->d_ff) * 4, false,
+                         ctx->stream));
+      a.mat_scratch = static_cast<float*>(ctx->mat_scratch.p);
+    }
     // Dynamic: 7/8 of the SMs at N <= 16 (the idle eighth starts the next
     // PDL launch's weight stream early; measured optimum, profiles/), every
     // SM at N >= 32 on shards with a full stage-1 wave (-2 to -3 % at
@@ -635,16 +649,29 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
 // ---------------------------------------------------------------------------
 // Unfused comparators on cuBLASLt (bf16 in, fp32 accumulate).
 // ---------------------------------------------------------------------------
-int ensure_unfused_weights(dfk_context_s* ctx, dfk_weights_s* w) {
-  if (w->cat_t && w->down_t) return DFK_OK;
+// K-major copies for cuBLASLt, built lazily from the packs (only the parts
+// the registered set has: stage-only sets, dfk_weights_create).
+int ensure_unfused_s1(dfk_context_s* ctx, dfk_weights_s* w) {
+  if (w->cat_t) return DFK_OK;
+  if (!w->s1_pack) return fail(DFK_ERR_INVALID, "weights registered without W_gate / W_up");
   const size_t cat_bytes = static_cast<size_t>(2 * w->d_ff * w->d_model) * 2;
-  const size_t down_bytes = static_cast<size_t>(w->d_ff * w->d_model) * 2;
-  if (cudaMalloc(&w->cat_t, cat_bytes) != cudaSuccess ||
-      cudaMalloc(&w->down_t, down_bytes) != cudaSuccess) {
+  if (cudaMalloc(&w->cat_t, cat_bytes) != cudaSuccess) {
+    w->cat_t = nullptr;
     return fail(DFK_ERR_NOMEM, "unfused comparator weights");
   }
   DFK_CUDA(launch_unpack_stage1(w->s1_pack, w->d_model, w->d_ff, w->s1_tiles,
                                 w->s1_kblocks, w->cat_t, ctx->stream));
+  return DFK_OK;
+}
+
+int ensure_unfused_dn(dfk_context_s* ctx, dfk_weights_s* w) {
+  if (w->down_t) return DFK_OK;
+  if (!w->dn_pack) return fail(DFK_ERR_INVALID, "weights registered without W_down");
+  const size_t down_bytes = static_cast<size_t>(w->d_ff * w->d_model) * 2;
+  if (cudaMalloc(&w->down_t, down_bytes) != cudaSuccess) {
+    w->down_t = nullptr;
+    return fail(DFK_ERR_NOMEM, "unfused comparator weights");
+  }
   DFK_CUDA(launch_unpack_down(w->dn_pack, w->d_model, w->d_ff, w->dn_tiles,
                               w->dn_kblocks, w->down_t, ctx->stream));
   return DFK_OK;
@@ -661,7 +688,7 @@ int lt_gemm(dfk_context_s* ctx, const __nv_bfloat16* A, int64_t lda,
       return fail(DFK_ERR_CUDA, "cublasLtCreate");
   }
   const size_t ws_bytes = 32u << 20;
-  DFK_TRY(ensure_buf(ctx->lt_ws, ws_bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->lt_ws, ws_bytes, false, ctx->stream));
   cublasLtMatmulDesc_t op = nullptr;
   cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
   const cudaDataType_t ct = c_bf16 ? CUDA_R_16BF : CUDA_R_32F;
@@ -716,12 +743,12 @@ int lt_gemm(dfk_context_s* ctx, const __nv_bfloat16* A, int64_t lda,
 // Stage 1 of the unfused layouts into a2 (ld = d_ff).
 int stage1_unfused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
                    int64_t B, __nv_bfloat16* a2, int64_t a2_ld, int variant) {
-  DFK_TRY(ensure_unfused_weights(ctx, w));
+  DFK_TRY(ensure_unfused_s1(ctx, w));
   const int64_t df = w->d_ff, dm = w->d_model;
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   if (variant == DFK_VARIANT_TWO_KERNEL) {
     // Grouped GEMM into [A_gate | A_1] (gate columns first), then silu-mul.
-    DFK_TRY(ensure_buf(ctx->concat, static_cast<size_t>(B * 2 * df) * 2, false,
+    DFK_TRY(ensure_buf(ctx, ctx->concat, static_cast<size_t>(B * 2 * df) * 2, false,
                        ctx->stream));
     auto* cc = static_cast<__nv_bfloat16*>(ctx->concat.p);
     DFK_TRY(lt_gemm(ctx, w->cat_t, dm, xb, dm, cc, 2 * df, true, 2 * df, B, dm));
@@ -733,9 +760,9 @@ int stage1_unfused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   }
   // Four-kernel: A_gate, A_1, A_silu materialised.
   const size_t bytes = static_cast<size_t>(B * df) * 2;
-  DFK_TRY(ensure_buf(ctx->concat, bytes, false, ctx->stream));
-  DFK_TRY(ensure_buf(ctx->tmp1, bytes, false, ctx->stream));
-  DFK_TRY(ensure_buf(ctx->tmp2, bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->concat, bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->tmp1, bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->tmp2, bytes, false, ctx->stream));
   auto* agate = static_cast<__nv_bfloat16*>(ctx->concat.p);
   auto* a1 = static_cast<__nv_bfloat16*>(ctx->tmp1.p);
   auto* asilu = static_cast<__nv_bfloat16*>(ctx->tmp2.p);
@@ -749,16 +776,23 @@ int stage1_unfused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
 
 int down_unfused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
                  int64_t B, void* y, bool y_bf16) {
-  DFK_TRY(ensure_unfused_weights(ctx, w));
+  DFK_TRY(ensure_unfused_dn(ctx, w));
   return lt_gemm(ctx, w->down_t, w->d_ff, static_cast<const __nv_bfloat16*>(a2),
                  w->d_ff, y, w->d_model, y_bf16, w->d_model, B, w->d_ff);
 }
 
-int check_handles(dfk_context_s* ctx, dfk_weights_s* w) {
+// need_s1 / need_dn: the call uses the stage-1 / down weights (a set
+// registered for one stage only cannot run the other, dfk_weights_create).
+int check_handles(dfk_context_s* ctx, dfk_weights_s* w, bool need_s1 = true,
+                  bool need_dn = true) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
   if (!w) return fail(DFK_ERR_INVALID, "null weights");
   if (w->ctx != ctx)
     return fail(DFK_ERR_INVALID, "weights belong to another context");
+  if (need_s1 && !w->s1_pack)
+    return fail(DFK_ERR_INVALID, "weights registered without W_gate / W_up (down-only set)");
+  if (need_dn && !w->dn_pack)
+    return fail(DFK_ERR_INVALID, "weights registered without W_down (stage-1-only set)");
   return use_device(ctx);
 }
 
@@ -836,7 +870,7 @@ int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
   dfk_config cfg;
   DFK_TRY(resolve_config(ctx, w, B, cfg_in, &cfg));
   const int64_t a2_ld = round_up(w->d_ff, 8);
-  DFK_TRY(ensure_buf(ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
+  DFK_TRY(ensure_buf(ctx, ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
                      ctx->stream));
   auto* a2 = static_cast<__nv_bfloat16*>(ctx->a2.p);
   if (cfg.variant == DFK_VARIANT_FUSED && cfg.block_kernel) {
@@ -854,12 +888,12 @@ int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
 }
 
 int block_fused_tp(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
-                   void* y, const dfk_config& cfg, const StreamArgs* tp) {
+                   void* y, bool y_bf16, const dfk_config& cfg, const StreamArgs* tp) {
   const int64_t a2_ld = round_up(w->d_ff, 8);
-  DFK_TRY(ensure_buf(ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
+  DFK_TRY(ensure_buf(ctx, ctx->a2, static_cast<size_t>(B * a2_ld) * 2, false,
                      ctx->stream));
   return block_fused(ctx, w, x, B, static_cast<__nv_bfloat16*>(ctx->a2.p), a2_ld, y,
-                     w->d_model, false, cfg, tp);
+                     w->d_model, y_bf16, cfg, tp);
 }
 
 }  // namespace dfk
@@ -916,6 +950,17 @@ int dfk_context_create(int device, void* stream, dfk_context* out) {
   ctx->cc_major = prop.major;
   ctx->cc_minor = prop.minor;
   cudaDriverGetVersion(&ctx->driver_version);
+  // Host-mapped error word the kernels raise when a cross-rank (or host
+  // copy) wait gives up; dfk_context_sync reports and clears it.
+  if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->err_host), sizeof(int),
+                    cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->err_dev), ctx->err_host, 0) !=
+          cudaSuccess) {
+    if (ctx->err_host) cudaFreeHost(ctx->err_host);
+    delete ctx;
+    return fail(DFK_ERR_CUDA, "cannot allocate the mapped error word");
+  }
+  *ctx->err_host = 0;
   if (stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -938,7 +983,7 @@ int dfk_context_destroy(dfk_context ctx) {
                        &ctx->counters, &ctx->concat, &ctx->tmp1, &ctx->tmp2,
                        &ctx->lt_ws, &ctx->flush, &ctx->hx_dev, &ctx->hy_dev,
                        &ctx->dec[0], &ctx->dec[1], &ctx->dec_f32, &ctx->s1acc,
-                       &ctx->s1cnt}) {
+                       &ctx->s1cnt, &ctx->mat_scratch}) {
     if (b->p) cudaFree(b->p);
   }
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -961,6 +1006,7 @@ int dfk_context_destroy(dfk_context ctx) {
   if (ctx->tp_sym.p) cudaFree(ctx->tp_sym.p);
   for (dfk_weights_s* w : ctx->weights) free_weights(w);
   ctx->weights.clear();
+  if (ctx->err_host) cudaFreeHost(ctx->err_host);
   if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
   if (ctx->hy_pinned) cudaFreeHost(ctx->hy_pinned);
   if (ctx->lt) cublasLtDestroy(ctx->lt);
@@ -976,6 +1022,15 @@ int dfk_context_sync(dfk_context ctx) {
   DFK_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->side_stream) DFK_CUDA(cudaStreamSynchronize(ctx->side_stream));
   if (ctx->out_stream) DFK_CUDA(cudaStreamSynchronize(ctx->out_stream));
+  if (ctx->err_host && *reinterpret_cast<volatile int*>(ctx->err_host)) {
+    *ctx->err_host = 0;
+    return fail(DFK_ERR_TIMEOUT,
+                "a kernel gave up waiting (> 4 s) for another rank's fused all-reduce "
+                "contribution or for the host X copy; the results of the calls since the "
+                "last sync are wrong.  Re-create the symmetric workspaces "
+                "(dfk_tp_sym_create + _open / _attach) on every rank before the next "
+                "tensor-parallel call");
+  }
   return DFK_OK;
 }
 
@@ -1021,7 +1076,13 @@ int dfk_weights_create(dfk_context ctx, const void* w_gate, const void* w_up,
                                    ") is empty or outside [0, " +
                                    std::to_string(d_ff) + ")");
   }
-  if (!w_gate || !w_up || !w_down) return fail(DFK_ERR_INVALID, "null weight");
+  // Stage-only sets (run_fused_stage1 takes W_up / W_gate alone,
+  // fused.hpp:61; down_projection W_down alone, swiglu.hpp:90): W_down NULL
+  // or W_gate and W_up both NULL.
+  const bool has_s1 = w_gate || w_up, has_dn = w_down != nullptr;
+  if ((w_gate == nullptr) != (w_up == nullptr))
+    return fail(DFK_ERR_INVALID, "W_gate and W_up must both be given or both be NULL");
+  if (!has_s1 && !has_dn) return fail(DFK_ERR_INVALID, "no weight matrix given");
   if (dtype != DFK_F64 && dtype != DFK_F32 && dtype != DFK_BF16)
     return fail(DFK_ERR_INVALID, "unknown dtype");
   DFK_CUDA(cudaSetDevice(ctx->device));
@@ -1039,53 +1100,52 @@ int dfk_weights_create(dfk_context ctx, const void* w_gate, const void* w_up,
       static_cast<size_t>(w->s1_tiles) * w->s1_kblocks * kBlockBytes;
   const size_t dn_bytes =
       static_cast<size_t>(w->dn_tiles) * w->dn_kblocks * kBlockBytes;
-  if (cudaMalloc(&w->s1_pack, s1_bytes) != cudaSuccess ||
-      cudaMalloc(&w->dn_pack, dn_bytes) != cudaSuccess) {
-    cudaFree(w->s1_pack);
+  auto drop = [&](int status, const std::string& msg) {
+    if (w->s1_pack) cudaFree(w->s1_pack);
+    if (w->dn_pack) cudaFree(w->dn_pack);
     delete w;
-    return fail(DFK_ERR_NOMEM, "weight pack allocation");
+    return fail(status, msg);
+  };
+  if ((has_s1 && cudaMalloc(&w->s1_pack, s1_bytes) != cudaSuccess) ||
+      (has_dn && cudaMalloc(&w->dn_pack, dn_bytes) != cudaSuccess)) {
+    cudaGetLastError();
+    return drop(DFK_ERR_NOMEM, "weight pack allocation");
   }
-  const void* g = w_gate;
-  const void* u = w_up;
-  const void* d = w_down;
+  const void* srcs[3] = {w_gate, w_up, w_down};
   void* staging[3] = {nullptr, nullptr, nullptr};
   const size_t esz = dtype_size(dtype);
   if (memory == DFK_HOST) {
     const size_t n1 = static_cast<size_t>(d_model * d_ff) * esz;
-    const void* srcs[3] = {w_gate, w_up, w_down};
     for (int i = 0; i < 3; ++i) {
+      if (!srcs[i]) continue;
       if (cudaMalloc(&staging[i], n1) != cudaSuccess) {
+        cudaGetLastError();
         for (void* p : staging) cudaFree(p);
-        cudaFree(w->s1_pack);
-        cudaFree(w->dn_pack);
-        delete w;
-        return fail(DFK_ERR_NOMEM, "weight staging allocation");
+        return drop(DFK_ERR_NOMEM, "weight staging allocation");
       }
       DFK_CUDA(cudaMemcpyAsync(staging[i], srcs[i], n1, cudaMemcpyHostToDevice,
                                ctx->stream));
+      srcs[i] = staging[i];
     }
-    g = staging[0];
-    u = staging[1];
-    d = staging[2];
   }
-  cudaError_t e1 = launch_pack_stage1(g, u, dtype, d_model, d_ff, ff_begin,
-                                      w->d_ff, w->s1_tiles, w->s1_kblocks,
-                                      w->s1_pack, ctx->stream);
-  cudaError_t e2 = launch_pack_down(d, dtype, d_model, ff_begin, w->d_ff,
-                                    w->dn_tiles, w->dn_kblocks, w->dn_pack,
-                                    ctx->stream);
+  cudaError_t e1 = cudaSuccess, e2 = cudaSuccess;
+  if (has_s1)
+    e1 = launch_pack_stage1(srcs[0], srcs[1], dtype, d_model, d_ff, ff_begin, w->d_ff,
+                            w->s1_tiles, w->s1_kblocks, w->s1_pack, ctx->stream);
+  if (has_dn)
+    e2 = launch_pack_down(srcs[2], dtype, d_model, ff_begin, w->d_ff, w->dn_tiles,
+                          w->dn_kblocks, w->dn_pack, ctx->stream);
   cudaError_t e3 = cudaStreamSynchronize(ctx->stream);
   for (void* p : staging)
     if (p) cudaFree(p);
-  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
-    cudaFree(w->s1_pack);
-    cudaFree(w->dn_pack);
-    delete w;
-    return fail(DFK_ERR_CUDA,
-                std::string("weight prepack: ") +
-                    cudaGetErrorString(e1 != cudaSuccess   ? e1
-                                       : e2 != cudaSuccess ? e2
-                                                           : e3));
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+    return drop(DFK_ERR_CUDA, std::string("weight prepack: ") +
+                                  cudaGetErrorString(e1 != cudaSuccess   ? e1
+                                                     : e2 != cudaSuccess ? e2
+                                                                         : e3));
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->weights.insert(w);  // freed with the context if never destroyed
   }
   *out = w;
   return DFK_OK;
@@ -1099,6 +1159,8 @@ int dfk_weights_destroy(dfk_weights w) {
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (!ctx->weights.erase(w)) return fail(DFK_ERR_INVALID, "unknown weights handle");
+    // A new handle may reuse this address: graphs keyed by it are stale.
+    ++ctx->generation;
   }
   free_weights(w);
   return DFK_OK;
@@ -1115,15 +1177,15 @@ int dfk_weights_shape(dfk_weights w, int64_t* d_model, int64_t* d_ff_shard,
 
 int dfk_weights_bytes(dfk_weights w, int64_t* bytes) {
   if (!w || !bytes) return fail(DFK_ERR_INVALID, "null argument");
-  *bytes = (static_cast<int64_t>(w->s1_tiles) * w->s1_kblocks +
-            static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks) *
+  *bytes = ((w->s1_pack ? static_cast<int64_t>(w->s1_tiles) * w->s1_kblocks : 0) +
+            (w->dn_pack ? static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks : 0)) *
            kBlockBytes;
   return DFK_OK;
 }
 
 int dfk_stage1(dfk_context ctx, dfk_weights w, const void* x, int64_t batch,
                void* a2, const dfk_config* cfg_in) {
-  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_handles(ctx, w, true, false));
   DFK_TRY(check_batch(batch));
   if (!x || !a2) return fail(DFK_ERR_INVALID, "null activation pointer");
   dfk_config cfg;
@@ -1136,7 +1198,7 @@ int dfk_stage1(dfk_context ctx, dfk_weights w, const void* x, int64_t batch,
 
 int dfk_down(dfk_context ctx, dfk_weights w, const void* a2, int64_t batch,
              void* y, int32_t y_dtype, const dfk_config* cfg_in) {
-  DFK_TRY(check_handles(ctx, w));
+  DFK_TRY(check_handles(ctx, w, false, true));
   DFK_TRY(check_batch(batch));
   if (!a2 || !y) return fail(DFK_ERR_INVALID, "null activation pointer");
   if (y_dtype != DFK_F32 && y_dtype != DFK_BF16)
@@ -1166,7 +1228,8 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
   const size_t xb = xn * 2;
   const size_t yb = xn * 4;
   if (ctx->hx_pinned_bytes < xb) {
-    if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
+    if (ctx->err_host) cudaFreeHost(ctx->err_host);
+  if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
     DFK_CUDA(cudaMallocHost(&ctx->hx_pinned, xb));
     ctx->hx_pinned_bytes = xb;
   }
@@ -1188,8 +1251,8 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
   } else {
     return fail(DFK_ERR_INVALID, "unknown x dtype");
   }
-  DFK_TRY(ensure_buf(ctx->hx_dev, xb, false, ctx->stream));
-  DFK_TRY(ensure_buf(ctx->hy_dev, yb, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->hx_dev, xb, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->hy_dev, yb, false, ctx->stream));
   DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, hx, xb, cudaMemcpyHostToDevice,
                            ctx->stream));
   if (tp_active(ctx)) {
@@ -1229,7 +1292,10 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
   DFK_TRY(resolve_config(ctx, w, batch, cfg, &rc));
   static const WaitValueFn wait_value = driver_fn<WaitValueFn>("cuStreamWaitValue32");
   static const WriteValueFn write_value = driver_fn<WriteValueFn>("cuStreamWriteValue32");
-  if (!tp_active(ctx) && batch <= 256 && rc.variant == DFK_VARIANT_FUSED &&
+  // (one block launch per call: the GEMV family launches 8-row chunks, and
+  // only a single launch carries the X-ready / Y-done flags)
+  const int64_t one_launch = rc.s1_family == DFK_FAMILY_GEMV ? 8 : 256;
+  if (!tp_active(ctx) && batch <= one_launch && rc.variant == DFK_VARIANT_FUSED &&
       rc.block_kernel && rc.dynamic_sched && rc.s1_split_k <= 1 && wait_value &&
       write_value && !knobs().host_stagek) {
     // Copy-engine X and Y: the H2D copy runs on a side stream as soon as its
@@ -1243,7 +1309,7 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
       DFK_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
       DFK_CUDA(cudaStreamCreateWithFlags(&ctx->out_stream, cudaStreamNonBlocking));
     }
-    DFK_TRY(ensure_buf(ctx->host_flags, 3 * kHostSlots * sizeof(unsigned), true, ctx->stream));
+    DFK_TRY(ensure_buf(ctx, ctx->host_flags, 3 * kHostSlots * sizeof(unsigned), true, ctx->stream));
     const int si = ctx->host_next;
     HostSlot& sl = ctx->host_slots[si];
     ctx->host_next = (ctx->host_next + 1) % kHostSlots;
@@ -1254,8 +1320,8 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
       const size_t nx = std::max<size_t>({xb, 2 * sl.x.bytes, 64 * 1024});
       const size_t ny = std::max<size_t>({yb, 2 * sl.y.bytes, 128 * 1024});
       for (HostSlot& o : ctx->host_slots) {
-        DFK_TRY(ensure_buf(o.x, nx, false, ctx->stream));
-        DFK_TRY(ensure_buf(o.y, ny, false, ctx->stream));
+        DFK_TRY(ensure_buf(ctx, o.x, nx, false, ctx->stream));
+        DFK_TRY(ensure_buf(ctx, o.y, ny, false, ctx->stream));
       }
       DFK_CUDA(cudaStreamSynchronize(ctx->stream));
     }
@@ -1313,7 +1379,7 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
       // the device, so it must not recur as batch sizes rotate over slots.
       DFK_CUDA(cudaStreamSynchronize(ctx->stream));
       const size_t nb = std::max<size_t>({xb, 2 * sl.x.bytes, 64 * 1024});
-      for (HostSlot& o : ctx->host_slots) DFK_TRY(ensure_buf(o.x, nb, false, ctx->stream));
+      for (HostSlot& o : ctx->host_slots) DFK_TRY(ensure_buf(ctx, o.x, nb, false, ctx->stream));
     }
     cudaError_t e = launch_stage_rows(ax.devicePointer, sl.x.p, static_cast<int64_t>(xb),
                                       ctx->stream);
@@ -1323,8 +1389,8 @@ int dfk_forward_host_async(dfk_context ctx, dfk_weights w,
   }
   // Stream order makes one staging pair safe: the next call's H2D runs after
   // this call's kernels, its kernels after this call's D2H.
-  DFK_TRY(ensure_buf(ctx->hx_dev, xb, false, ctx->stream));
-  DFK_TRY(ensure_buf(ctx->hy_dev, yb, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->hx_dev, xb, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->hy_dev, yb, false, ctx->stream));
   DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, x_pinned_bf16, xb,
                            cudaMemcpyHostToDevice, ctx->stream));
   if (tp_active(ctx)) {
@@ -1449,7 +1515,7 @@ int dfk_flush_l2(dfk_context ctx) {
   if (!ctx) return fail(DFK_ERR_INVALID, "null context");
   DFK_TRY(use_device(ctx));
   const size_t bytes = static_cast<size_t>(std::max(ctx->l2_bytes, 1 << 20)) * 2;
-  DFK_TRY(ensure_buf(ctx->flush, bytes, false, ctx->stream));
+  DFK_TRY(ensure_buf(ctx, ctx->flush, bytes, false, ctx->stream));
   DFK_CUDA(launch_flush(ctx->flush.p, bytes, ctx->stream));
   return DFK_OK;
 }

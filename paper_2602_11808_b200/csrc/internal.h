@@ -57,6 +57,7 @@ constexpr int kHostSlots = 8;
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int64_t launches = 0;
+  uint64_t generation = 0;  // ctx->generation when captured
 };
 
 }  // namespace dfk
@@ -72,6 +73,9 @@ struct dfk_context_s {
   int cc_major = 0, cc_minor = 0;
   int driver_version = 0;
   int64_t launches = 0;
+  // Bumped by every scratch (re)allocation and weight-set destruction: the
+  // addresses a captured decode graph baked in are valid while it holds.
+  uint64_t generation = 0;
 
   // Scratch (grown on demand, never shrunk).
   dfk::DeviceBuf a2;       // internal A2 of dfk_forward
@@ -83,6 +87,7 @@ struct dfk_context_s {
   dfk::DeviceBuf sched;    // dynamic-scheduler counters (kept zero between launches)
   dfk::DeviceBuf s1acc;    // stage-1 stream-K fp32 partial sums (kept all-zero)
   dfk::DeviceBuf s1cnt;    // stage-1 stream-K per-tile arrival counters (kept zero)
+  dfk::DeviceBuf mat_scratch;  // MaterializeIntermediate control's A_silu (tests)
   unsigned epoch = 0;      // block-kernel launch epoch (flag value)
   unsigned long long* trace = nullptr;  // dfk_set_trace buffer
   int64_t trace_slots = 0;
@@ -126,6 +131,10 @@ struct dfk_context_s {
   dfk::DeviceBuf tp_sym;
   int64_t tp_max_b = 0, tp_dm = 0;
   int tp_sym_rank = 0, tp_sym_size = 0;
+  // Host-mapped error word (cudaHostAllocMapped): kernels set it when a
+  // cross-rank wait times out; dfk_context_sync reports and clears it.
+  int* err_host = nullptr;
+  int* err_dev = nullptr;
   void* tp_peer[8] = {};
   bool tp_peer_ipc[8] = {};
 
@@ -214,13 +223,21 @@ struct StreamArgs;
 // (single rank) the plain block.
 int tp_block(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
              float* y, const dfk_config* cfg);
+// The fused-TP block into Y of either dtype (F32 / BF16).
+int tp_forward_fused_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
+                          int64_t B, void* y, int y_dtype, const dfk_config* cfg);
 bool tp_active(const dfk_context_s* ctx);
 // The block kernel with the fused TP all-reduce (tp.cpp): `tp` carries the
 // tp_* fields of StreamArgs; y is this rank's symmetric output.
 int block_fused_tp(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
-                   void* y, const dfk_config& cfg, const StreamArgs* tp);
-int ensure_buf(DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s);
+                   void* y, bool y_bf16, const dfk_config& cfg, const StreamArgs* tp);
+int ensure_buf(dfk_context_s* ctx, DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s);
 std::string config_label(const dfk_config& c);
+// Tuning cache (tuning_cache.cpp): lookup (false + *err set on a bad file)
+// and insert-or-replace ("" on success, else the error).
+bool cache_find(const std::string& path, int64_t B, int64_t dm, int64_t df,
+                const std::string& fp, std::string* hit, std::string* err);
+std::string cache_put(const std::string& path, const std::string& entry_text);
 
 }  // namespace dfk
 

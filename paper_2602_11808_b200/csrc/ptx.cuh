@@ -390,6 +390,25 @@ __device__ __forceinline__ void red_add_v4_f32_if(float* addr, float a, float b,
       : "memory");
 }
 
+// System-scope forms for partial sums added into another GPU's memory
+// (fused TP all-reduce): every rank's reductions to one address must be
+// atomic with respect to each other, i.e. at .sys scope.
+__device__ __forceinline__ void red_add_sys_f32_if(float* addr, float v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.relaxed.sys.global.add.f32 [%0], %1;\n}"
+      ::"l"(addr), "f"(v), "r"(static_cast<int>(pred))
+      : "memory");
+}
+
+__device__ __forceinline__ void red_add_sys_v4_f32_if(float* addr, float a, float b, float c,
+                                                      float d, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n"
+      " @p red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(addr),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"(static_cast<int>(pred))
+      : "memory");
+}
+
 __device__ __forceinline__ void st_shared_u16(uint32_t addr, unsigned short v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
 }

@@ -10,13 +10,11 @@
 //   lower median                            tuner.cpp:32-35
 //   select: (median, fusion pref, label)    tuner.cpp:170-190, 23-30
 //   all disqualified -> error               tuner.cpp:185-188
-//   cache format_version 1, flock, replace  tuner.cpp:196-390
+//   cache format_version 1, replace-by-key  tuner.cpp:196-390 (tuning_cache.cpp)
 //   get_or_tune (hit skips profiling)       tuner.cpp:408-424
 // One "run" is the mean of kRepsPerRun back-to-back calls (a single µs-scale
 // launch is below event resolution); samples are stored in ns per call.
 #include <cuda_runtime.h>
-#include <sys/file.h>
-#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -24,7 +22,6 @@
 #include <cstdio>
 #include <cstring>
 #include <ctime>
-#include <filesystem>
 #include <set>
 #include <sstream>
 #include <string>
@@ -33,6 +30,7 @@
 #include <json.hpp>
 
 #include "internal.h"
+#include "layout.cuh"
 
 using namespace dfk;
 using nlohmann::json;
@@ -94,8 +92,12 @@ dfk_config make_cfg(int variant, int s1f, int dnf, int kbs, int block,
 // family x down family x down grid), plus one no-PDL control.  Stage sizes
 // and the stage-1 grid use the library's defaults (pick_kbs, balanced_grid),
 // which were themselves chosen from measured sweeps (profiles/).
-std::vector<dfk_config> candidates(const dfk_context_s* ctx,
-                                   const dfk_weights_s* w, int64_t B) {
+struct ShapeTiles {
+  int s1_tiles, s1_kblocks;
+};
+
+std::vector<dfk_config> candidates(const dfk_context_s* ctx, const ShapeTiles* w,
+                                   int64_t B) {
   std::vector<dfk_config> out;
   out.push_back(make_cfg(DFK_VARIANT_FOUR_KERNEL, 0, 0, 0, 0, 0));
   out.push_back(make_cfg(DFK_VARIANT_TWO_KERNEL, 0, 0, 0, 0, 0));
@@ -175,37 +177,29 @@ json cfg_to_json(const dfk_config& c) {
               {"label", std::string(c.label)}};
 }
 
-template <typename T>
-T get_field(const json& j, const char* f) {
-  if (!j.contains(f))
-    throw std::runtime_error(std::string("cache entry missing field '") + f + "'");
-  try {
-    return j.at(f).get<T>();
-  } catch (const json::exception& e) {
-    throw std::runtime_error(std::string("cache field '") + f +
-                             "' has the wrong type: " + e.what());
-  }
-}
-
+// The chosen_config object of a cache entry; throws on a malformed one.
 dfk_config cfg_from_json(const json& j) {
+  if (!j.is_object()) throw std::runtime_error("chosen_config is not an object");
   dfk_config c;
   std::memset(&c, 0, sizeof(c));
-  c.variant = get_field<int>(j, "variant");
-  c.s1_family = get_field<int>(j, "s1_family");
-  c.s1_stages = get_field<int>(j, "s1_stages");
-  c.s1_ctas = get_field<int>(j, "s1_ctas");
-  c.s1_split_k = get_field<int>(j, "s1_split_k");
-  c.down_family = get_field<int>(j, "down_family");
-  c.down_stages = get_field<int>(j, "down_stages");
-  c.down_ctas = get_field<int>(j, "down_ctas");
-  c.pdl = get_field<int>(j, "pdl");
-  c.block_kernel = get_field<int>(j, "block_kernel");
-  c.kbs = get_field<int>(j, "kbs");
-  c.dynamic_sched = get_field<int>(j, "dynamic_sched");
-  c.chunk_kb = get_field<int>(j, "chunk_kb");
-  c.s1_chunk_kb = j.contains("s1_chunk_kb") ? j["s1_chunk_kb"].get<int>() : 0;
-  std::snprintf(c.label, sizeof(c.label), "%s",
-                get_field<std::string>(j, "label").c_str());
+  const std::pair<const char*, int32_t*> ints[] = {
+      {"variant", &c.variant},         {"s1_family", &c.s1_family},
+      {"s1_stages", &c.s1_stages},     {"s1_ctas", &c.s1_ctas},
+      {"s1_split_k", &c.s1_split_k},   {"down_family", &c.down_family},
+      {"down_stages", &c.down_stages}, {"down_ctas", &c.down_ctas},
+      {"pdl", &c.pdl},                 {"block_kernel", &c.block_kernel},
+      {"kbs", &c.kbs},                 {"dynamic_sched", &c.dynamic_sched},
+      {"chunk_kb", &c.chunk_kb},       {"s1_chunk_kb", &c.s1_chunk_kb}};
+  for (const auto& [name, dst] : ints) {
+    auto it = j.find(name);
+    if (it == j.end()) continue;  // fields added later default to 0 (library default)
+    if (!it->is_number_integer())
+      throw std::runtime_error(std::string("chosen_config.") + name + " is not an integer");
+    *dst = it->get<int32_t>();
+  }
+  auto l = j.find("label");
+  if (l == j.end() || !l->is_string()) throw std::runtime_error("chosen_config has no label");
+  std::snprintf(c.label, sizeof(c.label), "%s", l->get<std::string>().c_str());
   return c;
 }
 
@@ -234,104 +228,6 @@ json entry_json(int64_t B, int64_t dm, int64_t df, const std::string& fp,
               {"results", results}};
 }
 
-// Stream + flock released together (tuner.cpp:270-288 semantics).
-class LockedFile {
- public:
-  LockedFile(const std::string& path, const char* mode, int op)
-      : f_(std::fopen(path.c_str(), mode)) {
-    if (f_) flock(fileno(f_), op);
-  }
-  ~LockedFile() {
-    if (f_) std::fclose(f_);
-  }
-  std::FILE* get() const { return f_; }
-  explicit operator bool() const { return f_ != nullptr; }
-
- private:
-  std::FILE* f_;
-};
-
-std::string read_all(std::FILE* f) {
-  std::string text;
-  char buf[4096];
-  size_t got;
-  std::fseek(f, 0, SEEK_SET);
-  while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) text.append(buf, got);
-  return text;
-}
-
-json parse_cache(const std::string& text, const std::string& path) {
-  json doc;
-  try {
-    doc = json::parse(text);
-  } catch (const json::parse_error& e) {
-    throw std::runtime_error("cache file " + path + " is corrupt: " + e.what());
-  }
-  const int v = get_field<int>(doc, "format_version");
-  if (v != kCacheFormatVersion)
-    throw std::runtime_error("cache file " + path + " has format version " +
-                             std::to_string(v) + "; this build reads version " +
-                             std::to_string(kCacheFormatVersion));
-  return doc;
-}
-
-bool key_matches(const json& e, int64_t B, int64_t dm, int64_t df,
-                 const std::string& fp) {
-  const json s = get_field<json>(e, "shape");
-  return get_field<int64_t>(s, "batch") == B &&
-         get_field<int64_t>(s, "d_model") == dm &&
-         get_field<int64_t>(s, "d_ff") == df &&
-         get_field<std::string>(e, "fingerprint") == fp;
-}
-
-bool cache_lookup(const std::string& path, int64_t B, int64_t dm, int64_t df,
-                  const std::string& fp, json* hit) {
-  std::string text;
-  {
-    LockedFile f(path, "r", LOCK_SH);
-    if (!f) return false;
-    text = read_all(f.get());
-  }
-  if (text.empty()) return false;
-  const json doc = parse_cache(text, path);
-  for (const json& e : get_field<json>(doc, "entries")) {
-    if (key_matches(e, B, dm, df, fp)) {
-      *hit = e;
-      return true;
-    }
-  }
-  return false;
-}
-
-void cache_store(const std::string& path, const json& entry, int64_t B,
-                 int64_t dm, int64_t df, const std::string& fp) {
-  std::filesystem::path p(path);
-  if (p.has_parent_path()) std::filesystem::create_directories(p.parent_path());
-  LockedFile f(path, "a+", LOCK_EX);
-  if (!f) throw std::runtime_error("cache file " + path + " is not writable");
-  const std::string text = read_all(f.get());
-  json doc = text.empty() ? json{{"format_version", kCacheFormatVersion},
-                                 {"entries", json::array()}}
-                          : parse_cache(text, path);
-  json& entries = doc["entries"];
-  bool replaced = false;
-  for (json& e : entries) {
-    if (key_matches(e, B, dm, df, fp)) {
-      e = entry;
-      replaced = true;
-      break;
-    }
-  }
-  if (!replaced) entries.push_back(entry);
-  const std::string out = doc.dump(2) + "\n";
-  std::fseek(f.get(), 0, SEEK_SET);
-  if (ftruncate(fileno(f.get()), 0) != 0)
-    throw std::runtime_error("cache file " + path + ": truncate failed");
-  if (std::fwrite(out.data(), 1, out.size(), f.get()) != out.size() ||
-      std::fflush(f.get()) != 0)
-    throw std::runtime_error("cache file " + path + ": write failed");
-}
-
 // max|a-b| / max|b| over n floats.
 double rel_inf_error(const std::vector<float>& a, const std::vector<float>& b) {
   double num = 0.0, den = 0.0;
@@ -356,8 +252,17 @@ extern "C" {
 int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
                    dfk_config* out, int32_t cap, int32_t* n) {
   if (!ctx || !w || !n) return fail(DFK_ERR_INVALID, "null argument");
-  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
-  const auto c = candidates(ctx, w, batch);
+  return dfk_candidates_shape(ctx, batch, w->d_model, w->d_ff, out, cap, n);
+}
+
+int dfk_candidates_shape(dfk_context ctx, int64_t batch, int64_t d_model, int64_t d_ff,
+                         dfk_config* out, int32_t cap, int32_t* n) {
+  if (!ctx || !n) return fail(DFK_ERR_INVALID, "null argument");
+  if (batch < 1 || d_model < 1 || d_ff < 1)
+    return fail(DFK_ERR_SHAPE, "batch, d_model and d_ff must be >= 1");
+  const ShapeTiles st{static_cast<int>(ceil_div64(d_ff, kS1Cols)),
+                      static_cast<int>(ceil_div64(d_model, kBlockK))};
+  const auto c = candidates(ctx, &st, batch);
   *n = static_cast<int32_t>(c.size());
   for (int32_t i = 0; i < std::min<int32_t>(cap, *n); ++i) out[i] = c[i];
   return DFK_OK;
@@ -386,11 +291,20 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   const std::string path = cache_path ? cache_path : "";
   const auto key = std::make_tuple(batch, dm, df);
 
-  try {
-    if (!path.empty()) {
-      json hit;
-      if (cache_lookup(path, batch, dm, df, fp, &hit)) {
-        const dfk_config c = cfg_from_json(get_field<json>(hit, "chosen_config"));
+  if (!path.empty()) {
+    // A hit needs this library's chosen_config; an entry written through the
+    // reference-API shim (same file, same key) without one is a miss.
+    std::string text, err;
+    if (cache_find(path, batch, dm, df, fp, &text, &err)) {
+      const json hit = json::parse(text);
+      auto cc = hit.find("chosen_config");
+      if (cc != hit.end()) {
+        dfk_config c;
+        try {
+          c = cfg_from_json(*cc);
+        } catch (const std::exception& e) {
+          return fail(DFK_ERR_CACHE, "tuning cache " + path + ": " + e.what());
+        }
         {
           std::lock_guard<std::mutex> lk(ctx->mu);
           ctx->chosen[key] = c;
@@ -400,9 +314,9 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
         write_json(hit, results_json, results_len);
         return DFK_OK;
       }
+    } else if (!err.empty()) {
+      return fail(DFK_ERR_CACHE, err);
     }
-  } catch (const std::exception& e) {
-    return fail(DFK_ERR_CACHE, e.what());
   }
 
   // Seeded input, identical across candidates (tuner.cpp:117-120).
@@ -437,7 +351,8 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   std::vector<Result> results;
-  for (const dfk_config& c : candidates(ctx, w, batch)) {
+  const ShapeTiles tiles{w->s1_tiles, w->s1_kblocks};
+  for (const dfk_config& c : candidates(ctx, &tiles, batch)) {
     Result r;
     r.cfg = c;
     r.label = c.label;
@@ -505,11 +420,8 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   if (chosen) *chosen = best->cfg;
   write_json(entry, results_json, results_len);
   if (!path.empty()) {
-    try {
-      cache_store(path, entry, batch, dm, df, fp);
-    } catch (const std::exception& e) {
-      return fail(DFK_ERR_CACHE, e.what());
-    }
+    const std::string err = cache_put(path, entry.dump());
+    if (!err.empty()) return fail(DFK_ERR_CACHE, err);
   }
   return DFK_OK;
 }

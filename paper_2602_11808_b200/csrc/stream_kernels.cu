@@ -364,17 +364,22 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   return v;
 }
 
-// Cross-rank waits give up (error flag + trap: the launch fails instead of
-// hanging the GPU) after 4 s.
-__device__ __forceinline__ void tp_spin_check(const StreamArgs& a,
-                                              unsigned long long t0) {
+// Cross-rank waits give up after 4 s: the error word (host-mapped, read by
+// dfk_context_sync) is set and the wait returns false, so the launch ends
+// -- with a wrong Y -- instead of hanging the GPU or trapping (a trap would
+// leave the context unusable).  Any thread that sees the error set stops
+// waiting at once.
+__device__ __forceinline__ bool tp_wait_timed_out(const StreamArgs& a,
+                                                  unsigned long long t0) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (t - t0 < 1000000ull) return false;  // fast path: no host-memory read
+  if (a.tp_error && *reinterpret_cast<volatile int*>(a.tp_error)) return true;
   if (t - t0 > 4000000000ull) {
-    if (a.tp_error) atomicExch(a.tp_error, 1);
-    __threadfence_system();
-    __trap();
+    if (a.tp_error) atomicExch_system(a.tp_error, 1);
+    return true;
   }
+  return false;
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -396,6 +401,10 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
   }
   named_bar(1, nthr);
   if (*smem_flag) {
+    // The full sums of tile t (owner o's workspace, possibly remote) go to
+    // every rank's Y slot (the all-gather, by push), the workspace is
+    // re-zeroed, and every rank's done word of tile t is raised; each rank
+    // then copies the tile into its caller's Y (tp_collect_y).
     float* acc = a.tp_yacc[o];
     const int col0 = t * kDownCols;
     const int nvec = a.B * (kDownCols / 4);
@@ -419,18 +428,59 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
           const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
           if (j < a.out_cols) {  // out_cols is a multiple of 4 in TP mode
             for (int r = 0; r < a.tp_size; ++r)
-              *reinterpret_cast<float4*>(a.tp_y[r] + n * a.y_ld + j) = v[u];
+              __stcg(reinterpret_cast<float4*>(a.tp_y[r] + n * a.y_ld + j), v[u]);
           }
           __stcg(q[u], make_float4(0.f, 0.f, 0.f, 0.f));
         }
       }
     }
     if (tid == 0) a.tp_cnt[o][t] = 0;
-    __threadfence_system();
     named_bar(1, nthr);
-    if (tid < a.tp_size) atomicAdd_system(a.tp_done[tid], 1);
+    if (tid < a.tp_size) {  // release every rank's tile (cumulative through the barrier)
+      __threadfence_system();
+      atomicAdd_system(a.tp_done[tid] + t, 1);
+    }
   }
   named_bar(1, nthr);
+}
+
+// End of a fused-TP block launch (every CTA, all threads): CTA c copies the
+// tiles t = c, c + G, ... of this rank's full-sum Y slot into the caller's Y
+// (fp32 or bf16) once the finalising CTA (on any rank) has raised the tile's
+// done word, then re-arms it.  The kernel therefore ends with Y complete:
+// one launch per tensor-parallel block, no copy or conversion after it.
+__device__ __forceinline__ void tp_collect_y(const StreamArgs& a, int* smem_flag) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int* done = a.tp_done[a.tp_rank];
+  const float* ys = a.tp_y[a.tp_rank];
+  for (int t = blockIdx.x; t < a.t2; t += gridDim.x) {
+    if (tid == 0) {
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+      while (ld_acquire_sys(done + t) == 0)
+        if (tp_wait_timed_out(a, t0)) break;
+      done[t] = 0;  // consumed: the next finalisation is the next launch's
+    }
+    __syncthreads();  // the acquire is shared through the barrier
+    const int col0 = t * kDownCols;
+    const int nvec = a.B * (kDownCols / 4);
+    for (int idx = tid; idx < nvec; idx += nthr) {
+      const int n = idx / (kDownCols / 4), j = col0 + (idx % (kDownCols / 4)) * 4;
+      if (j >= a.out_cols) continue;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(ys + n * a.y_ld + j));
+      if (a.y_bf16) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.y) + n * a.y_ld + j) = pk;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.y) + n * a.y_ld + j) = v;
+      }
+    }
+  }
+  (void)smem_flag;
 }
 
 // 16 accumulator values of one lane (its output row `lane`, batch rows
@@ -439,6 +489,7 @@ __device__ __forceinline__ void tp_finish_tile(const StreamArgs& a, int t, int n
 // (two shuffle butterflies) so that each lane adds 4 consecutive floats of
 // one batch row with a single red.global.add.v4.f32.  `col0` = the address of
 // the group's first column for batch row 0 (16-byte aligned, ld % 4 == 0).
+template <bool kSys = false>
 __device__ __forceinline__ void red_rows_v4(float (&v)[16], float* col0, int64_t ld,
                                             int c0, int nvalid, int lane) {
   const int li = lane & 3;
@@ -457,7 +508,11 @@ __device__ __forceinline__ void red_rows_v4(float (&v)[16], float* col0, int64_t
       }
     }
     const int n = c0 + 4 * b + li;
-    red_add_v4_f32_if(col0 + static_cast<int64_t>(n) * ld, x[0], x[1], x[2], x[3], n < nvalid);
+    if (kSys)
+      red_add_sys_v4_f32_if(col0 + static_cast<int64_t>(n) * ld, x[0], x[1], x[2], x[3],
+                            n < nvalid);
+    else
+      red_add_v4_f32_if(col0 + static_cast<int64_t>(n) * ld, x[0], x[1], x[2], x[3], n < nvalid);
   }
 }
 
@@ -701,7 +756,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       // gpu scope: the flag and the X bytes are written by this GPU's copy
       // engine / stream front end, visible in its L2
       while (static_cast<int>(ld_acquire(a.x_ready) - a.x_seq) < 0)
-        tp_spin_check(a, t0);
+        if (tp_wait_timed_out(a, t0)) break;
       fence_proxy_async_global();
       x_ok = true;
     }
@@ -937,8 +992,11 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
           if (c == 0 && n < a.B && j < a.out_cols) {
-            atomicAdd(down_acc(a, pc.tile) + static_cast<int64_t>(n) * a.yacc_ld + j,
-                      acc[r][n]);
+            float* dst = down_acc(a, pc.tile) + static_cast<int64_t>(n) * a.yacc_ld + j;
+            if (a.tp_size > 1)
+              atomicAdd_system(dst, acc[r][n]);
+            else
+              atomicAdd(dst, acc[r][n]);
           }
         }
       }
@@ -1278,7 +1336,16 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
           const float up = __shfl_xor_sync(0xffffffffu, v[e], 16);
           const int n = c0 + e;
           if (!is_up && n < a.B && col < a.cols_valid) {
-            a.a2[n * a.a2_ld + col] = __float2bfloat16_rn(silu_f(v[e]) * up);
+            float act = silu_f(v[e]);
+            if (a.mutant == 2) {
+              // MaterializeIntermediate negative control
+              // (verification.cpp:126-169): SiLU(A_gate) round-trips through
+              // a global buffer -- same numbers, extra global traffic.
+              float* slot = a.mat_scratch + static_cast<int64_t>(n) * a.cols_valid + col;
+              asm volatile("st.global.cg.f32 [%0], %1;" ::"l"(slot), "f"(act) : "memory");
+              asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(act) : "l"(slot) : "memory");
+            }
+            a.a2[n * a.a2_ld + col] = __float2bfloat16_rn(act * up);
           }
         }
       }
@@ -1296,19 +1363,31 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       const bool jok = j < a.out_cols;
       float* yp = down_acc(a, pc.tile) + j;
       const int64_t ld = a.yacc_ld;
-      // v4 reductions: local workspace only, whole 4-column groups (the
-      // condition is warp-uniform: the shuffles involve all 32 lanes)
-      const bool vec = a.red_v4 && a.tp_size <= 1 &&
+      // v4 reductions over whole 4-column groups (the condition is
+      // warp-uniform: the shuffles involve all 32 lanes); under the fused TP
+      // all-reduce always, at system scope (the owner's workspace may be on
+      // another GPU: 4x fewer NVLink reductions)
+      const bool tp = a.tp_size > 1;
+      const bool vec = (a.red_v4 || tp) &&
                        __all_sync(0xffffffffu, j - (lane & 3) + 3 < a.out_cols);
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
         tmem_ld16_sum(taddr + c0, nacc, astr, v);
         if (vec) {
-          red_rows_v4(v, yp - (lane & 3), ld, c0, a.B, lane);
+          if (tp)
+            red_rows_v4<true>(v, yp - (lane & 3), ld, c0, a.B, lane);
+          else
+            red_rows_v4(v, yp - (lane & 3), ld, c0, a.B, lane);
         } else {
           float* yc = yp + c0 * ld;
+          if (tp) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) red_add_f32_if(yc + e * ld, v[e], jok && c0 + e < a.B);
+            for (int e = 0; e < 16; ++e)
+              red_add_sys_f32_if(yc + e * ld, v[e], jok && c0 + e < a.B);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) red_add_f32_if(yc + e * ld, v[e], jok && c0 + e < a.B);
+          }
         }
       }
       tc_fence_before();
@@ -1412,21 +1491,17 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   }
 
   __syncthreads();
+  // Fused TP all-reduce: this rank's Y tiles into the caller's buffer.
+  if (kMode == kModeBlock && a.tp_size > 1) {
+    tp_collect_y(a, smem_flag);
+    __syncthreads();
+  }
   if (a.dynamic && threadIdx.x == 0) {
-    // The last CTA out re-arms the work counter for the next launch; under
-    // the fused TP all-reduce it first waits until every down tile of this
-    // rank's Y has been written (by whichever rank finished it).
+    // The last CTA out re-arms the work counter for the next launch.
     if (atom_add_acq_rel_gpu(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
       if (a.x_free) {  // device-scope release: read by stream waits / copy engines
         st_release(a.x_free, a.x_seq);
         if (a.y_done) st_release(a.y_done, a.x_seq);
-      }
-      if (kMode == kModeBlock && a.tp_size > 1) {
-        int* done = a.tp_done[a.tp_rank];
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-        while (ld_acquire_sys(done) < a.t2) tp_spin_check(a, t0);
-        *done = 0;
       }
       a.sched[0] = 0;
       a.sched[1] = 0;

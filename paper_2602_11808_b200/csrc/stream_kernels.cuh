@@ -72,7 +72,11 @@ struct StreamArgs {
   // kModeBlock: per-stage-1-tile completion flags and this launch's epoch.
   unsigned* flags;
   unsigned epoch;
+  // Negative controls (tests only): 1 = SiLU*up per K chunk (stream-K /
+  // split-K pieces), 2 = SiLU(A_gate) materialised in mat_scratch
+  // [B x cols_valid] fp32 and read back before the multiply.
   int mutant;
+  float* mat_scratch;
   // kModeBlock plan (host-computed, block_plan in api.cu).  Stage-1 tiles go
   // round-robin: CTAs c < r own q+1 tiles ("heavy"), the rest own q
   // ("light").  Down units form two groups, each split over all G ranks
@@ -111,20 +115,24 @@ struct StreamArgs {
   // Fused tensor-parallel all-reduce (kModeBlock + dynamic, tp_size > 1):
   // down tile t is OWNED by rank t % tp_size.  Every rank red.adds its
   // partial sums of tile t into the owner's fp32 workspace tp_yacc[owner]
-  // over NVLink peer memory and counts the K blocks it contributed on the
-  // owner's tp_cnt[owner][t]; the CTA (on any rank) that completes the
-  // tile's tp_total_kb K blocks reads the full sums, writes Y into EVERY
-  // rank's tp_y[r] (the all-gather), re-zeroes the owner's workspace and
-  // counter and bumps every rank's tp_done[r].  A rank's launch ends when
-  // its tp_done reaches t2 (spun on by its last CTA out, then reset), so Y
-  // on every rank is the full sum when the kernel completes: the block's one
-  // collective runs inside the kernel, overlapped with the down stream.
+  // over NVLink peer memory (system scope, v4) and counts the K blocks it
+  // contributed on the owner's tp_cnt[owner][t]; the CTA (on any rank) that
+  // completes the tile's tp_total_kb K blocks reads the full sums, stores
+  // them into EVERY rank's full-sum slot tp_y[r] (the all-gather, by push),
+  // re-zeroes the owner's workspace and counter and raises every rank's
+  // tp_done[r][t].  At the end of the launch each rank's CTAs wait for their
+  // tiles' done words (local memory), copy the tiles into the caller's Y
+  // (y, fp32 or bf16) and re-arm the words: the launch completes with the
+  // all-reduced Y in place -- the block's one collective inside its one
+  // kernel, overlapped with the down stream.
   int tp_rank, tp_size, tp_total_kb;
   float* tp_yacc[kMaxTp];
   int* tp_cnt[kMaxTp];
-  int* tp_done[kMaxTp];
+  int* tp_done[kMaxTp];  // per down tile
   float* tp_y[kMaxTp];
-  int* tp_error;  // set before __trap() when a cross-rank wait times out
+  // Error word (host-mapped; dfk_context_sync reports it): set when a wait
+  // on another rank (or on the host path's X copy) gives up after 4 s.
+  int* tp_error;
   // Optional timeline (tools/trace_block.py): per CTA kTraceSlots globaltimer
   // stamps: [0] start, [1] producer done, [2] consumer done, then per piece
   // i < 8: [3+2i] piece fetched (its first weight copy follows), [4+2i]

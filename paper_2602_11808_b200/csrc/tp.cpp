@@ -27,10 +27,10 @@ int nccl_fail(ncclResult_t r, const char* what) {
 
 // One symmetric workspace per rank, identical layout on every rank (so a
 // peer's buffers are at the same offsets from its base): fp32 down
-// accumulator [max_b x t2*128], per-tile K-block counters, the done counter,
-// an error flag, and the full-sum Y [max_b x d_model] fp32.
+// accumulator [max_b x t2*128], per-tile K-block counters, per-tile done
+// words, and the full-sum Y slot [max_b x d_model] fp32.
 struct SymLayout {
-  size_t yacc, cnt, done, err, y, total;
+  size_t yacc, cnt, done, y, total;
   int t2;
 };
 
@@ -45,9 +45,7 @@ SymLayout sym_layout(int64_t max_b, int64_t dm) {
   L.cnt = off;
   off = align256(off + static_cast<size_t>(L.t2) * 4);
   L.done = off;
-  off = align256(off + 4);
-  L.err = off;
-  off = align256(off + 4);
+  off = align256(off + static_cast<size_t>(L.t2) * 4);
   L.y = off;
   off = align256(off + static_cast<size_t>(max_b * dm) * 4);
   L.total = off;
@@ -72,8 +70,70 @@ bool tp_active(const dfk_context_s* ctx) {
 
 int tp_block(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
              float* y, const dfk_config* cfg) {
-  if (ctx->tp_sym_size > 1) return dfk_tp_forward_fused(ctx, w, x, B, y, cfg);
+  if (ctx->tp_sym_size > 1) return tp_forward_fused_impl(ctx, w, x, B, y, DFK_F32, cfg);
   return dfk_tp_forward(ctx, w, x, B, y, cfg);
+}
+
+int tp_forward_fused_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
+                          int64_t batch, void* y, int y_dtype, const dfk_config* cfg) {
+  if (!ctx || !w) return fail(DFK_ERR_INVALID, "null handle");
+  if (w->ctx != ctx) return fail(DFK_ERR_INVALID, "weights belong to another context");
+  if (!w->s1_pack || !w->dn_pack)
+    return fail(DFK_ERR_INVALID, "the TP block needs all three weight matrices");
+  if (!x || !y) return fail(DFK_ERR_INVALID, "null activation pointer");
+  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
+  if (y_dtype != DFK_F32 && y_dtype != DFK_BF16)
+    return fail(DFK_ERR_INVALID, "y_dtype must be F32 or BF16");
+  if (ctx->tp_sym_size < 1 || !ctx->tp_sym.p)
+    return fail(DFK_ERR_INVALID, "dfk_tp_sym_create / _open / _attach first");
+  const int P = ctx->tp_sym_size;
+  if (P == 1) return forward_impl(ctx, w, x, batch, y, y_dtype, cfg);
+  if (batch > ctx->tp_max_b)
+    return fail(DFK_ERR_SHAPE, "batch exceeds the symmetric workspace's max_batch");
+  if (w->d_model != ctx->tp_dm)
+    return fail(DFK_ERR_SHAPE, "weights' d_model differs from the symmetric workspace");
+  // A tile is complete when the K blocks of ALL ranks' shards have arrived;
+  // every rank derives that total from balanced_ranges, so each rank must
+  // hold exactly its balanced shard (tp.cpp:8-29, make_plan :55-61).
+  int64_t mb = 0, me = 0;
+  DFK_TRY(dfk_balanced_range(w->d_ff_total, P, ctx->tp_sym_rank, &mb, &me));
+  if (w->ff_begin != mb || w->ff_begin + w->d_ff != me)
+    return fail(DFK_ERR_INVALID,
+                "fused TP: rank " + std::to_string(ctx->tp_sym_rank) + " holds d_ff [" +
+                    std::to_string(w->ff_begin) + ", " + std::to_string(w->ff_begin + w->d_ff) +
+                    ") but the all-reduce expects its balanced_ranges shard [" +
+                    std::to_string(mb) + ", " + std::to_string(me) +
+                    ") (use dfk_tp_forward for other plans)");
+  dfk_config c;
+  DFK_TRY(resolve_config(ctx, w, batch, cfg, &c));
+  c.variant = DFK_VARIANT_FUSED;  // the all-reduce lives in the block kernel
+  c.block_kernel = 1;
+  c.dynamic_sched = 1;
+  c.s1_split_k = 1;
+  // Down K blocks contributed to every tile by all ranks (shards may differ
+  // by one column, balanced_ranges tp.cpp:8-29).
+  int total_kb = 0;
+  for (int r = 0; r < P; ++r) {
+    int64_t b = 0, e = 0;
+    DFK_TRY(dfk_balanced_range(w->d_ff_total, P, r, &b, &e));
+    total_kb += static_cast<int>((e - b + kBlockK - 1) / kBlockK);
+  }
+  const SymLayout L = sym_layout(ctx->tp_max_b, ctx->tp_dm);
+  StreamArgs t = {};
+  t.tp_rank = ctx->tp_sym_rank;
+  t.tp_size = P;
+  t.tp_total_kb = total_kb;
+  t.yacc_ld = L.t2 * kDownCols;
+  for (int r = 0; r < P; ++r) {
+    auto* base = static_cast<uint8_t*>(ctx->tp_peer[r]);
+    if (!base) return fail(DFK_ERR_INVALID, "peer workspace missing");
+    t.tp_yacc[r] = reinterpret_cast<float*>(base + L.yacc);
+    t.tp_cnt[r] = reinterpret_cast<int*>(base + L.cnt);
+    t.tp_done[r] = reinterpret_cast<int*>(base + L.done);
+    t.tp_y[r] = reinterpret_cast<float*>(base + L.y);
+  }
+  DFK_CUDA(cudaSetDevice(ctx->device));
+  return block_fused_tp(ctx, w, x, batch, y, y_dtype == DFK_BF16, c, &t);
 }
 
 }  // namespace dfk
@@ -250,54 +310,8 @@ int dfk_tp_sym_attach(dfk_context* ctxs, int n) {
 }
 
 int dfk_tp_forward_fused(dfk_context ctx, dfk_weights w, const void* x,
-                         int64_t batch, float* y, const dfk_config* cfg) {
-  if (!ctx || !w) return fail(DFK_ERR_INVALID, "null handle");
-  if (w->ctx != ctx) return fail(DFK_ERR_INVALID, "weights belong to another context");
-  if (!x || !y) return fail(DFK_ERR_INVALID, "null activation pointer");
-  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
-  if (ctx->tp_sym_size < 1 || !ctx->tp_sym.p)
-    return fail(DFK_ERR_INVALID, "dfk_tp_sym_create / _open / _attach first");
-  const int P = ctx->tp_sym_size;
-  if (P == 1) return forward_impl(ctx, w, x, batch, y, DFK_F32, cfg);
-  if (batch > ctx->tp_max_b)
-    return fail(DFK_ERR_SHAPE, "batch exceeds the symmetric workspace's max_batch");
-  if (w->d_model != ctx->tp_dm)
-    return fail(DFK_ERR_SHAPE, "weights' d_model differs from the symmetric workspace");
-  dfk_config c;
-  DFK_TRY(resolve_config(ctx, w, batch, cfg, &c));
-  c.variant = DFK_VARIANT_FUSED;  // the all-reduce lives in the block kernel
-  c.block_kernel = 1;
-  c.dynamic_sched = 1;
-  c.s1_split_k = 1;
-  // Down K blocks contributed to every tile by all ranks (shards may differ
-  // by one column, balanced_ranges tp.cpp:8-29).
-  int total_kb = 0;
-  for (int r = 0; r < P; ++r) {
-    int64_t b = 0, e = 0;
-    DFK_TRY(dfk_balanced_range(w->d_ff_total, P, r, &b, &e));
-    total_kb += static_cast<int>((e - b + kBlockK - 1) / kBlockK);
-  }
-  const SymLayout L = sym_layout(ctx->tp_max_b, ctx->tp_dm);
-  StreamArgs t = {};
-  t.tp_rank = ctx->tp_sym_rank;
-  t.tp_size = P;
-  t.tp_total_kb = total_kb;
-  t.yacc_ld = L.t2 * kDownCols;
-  for (int r = 0; r < P; ++r) {
-    auto* base = static_cast<uint8_t*>(ctx->tp_peer[r]);
-    if (!base) return fail(DFK_ERR_INVALID, "peer workspace missing");
-    t.tp_yacc[r] = reinterpret_cast<float*>(base + L.yacc);
-    t.tp_cnt[r] = reinterpret_cast<int*>(base + L.cnt);
-    t.tp_done[r] = reinterpret_cast<int*>(base + L.done);
-    t.tp_y[r] = reinterpret_cast<float*>(base + L.y);
-  }
-  auto* own = static_cast<uint8_t*>(ctx->tp_sym.p);
-  t.tp_error = reinterpret_cast<int*>(own + L.err);
-  DFK_CUDA(cudaSetDevice(ctx->device));
-  DFK_TRY(block_fused_tp(ctx, w, x, batch, own + L.y, c, &t));
-  DFK_CUDA(cudaMemcpyAsync(y, own + L.y, static_cast<size_t>(batch * w->d_model) * 4,
-                           cudaMemcpyDeviceToDevice, ctx->stream));
-  return DFK_OK;
+                         int64_t batch, void* y, int32_t y_dtype, const dfk_config* cfg) {
+  return tp_forward_fused_impl(ctx, w, x, batch, y, y_dtype, cfg);
 }
 
 }  // extern "C"

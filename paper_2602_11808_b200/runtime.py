@@ -17,7 +17,7 @@ from . import build as _build
 
 # --- status codes (dfk_status) ---------------------------------------------
 OK, ERR_SHAPE, ERR_INVALID, ERR_CUDA, ERR_NCCL, ERR_NOMEM, ERR_UNSUPPORTED, \
-    ERR_GATE, ERR_CACHE = range(9)
+    ERR_GATE, ERR_CACHE, ERR_TIMEOUT = range(10)
 F64, F32, BF16 = 0, 1, 2
 HOST, DEVICE = 0, 1
 VARIANT_FUSED, VARIANT_TWO_KERNEL, VARIANT_FOUR_KERNEL = 0, 1, 2
@@ -48,6 +48,10 @@ class GateError(DfkError):
 
 class CacheError(DfkError):
     pass
+
+
+class TimeoutError_(DfkError):
+    """A fused all-reduce wait on a peer gave up (dfk_context_sync)."""
 
 
 def library_path() -> str:
@@ -135,9 +139,14 @@ _sigs = {
     "dfk_forward_host_async": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
     "dfk_candidates": ([_vp, _vp, _i64, C.POINTER(Config), _i32, C.POINTER(_i32)],
                        C.c_int),
+    "dfk_candidates_shape": ([_vp, _i64, _i64, _i64, C.POINTER(Config), _i32,
+                              C.POINTER(_i32)], C.c_int),
     "dfk_tune": ([_vp, _vp, _i64, C.c_char_p, _i32, _i32, C.POINTER(Config),
                   C.POINTER(_i32), C.c_char_p, C.c_size_t], C.c_int),
     "dfk_select_config": ([_vp, _vp, _i64, C.POINTER(Config)], C.c_int),
+    "dfk_cache_lookup": ([C.c_char_p, _i64, _i64, _i64, C.c_char_p, C.c_char_p, C.c_size_t,
+                          C.POINTER(C.c_size_t), C.POINTER(_i32)], C.c_int),
+    "dfk_cache_store": ([C.c_char_p, C.c_char_p], C.c_int),
     "dfk_tp_unique_id": ([_vp], C.c_int),
     "dfk_tp_init": ([_vp, _vp, C.c_int, C.c_int], C.c_int),
     "dfk_tp_init_all": ([C.POINTER(_vp), C.c_int], C.c_int),
@@ -148,7 +157,7 @@ _sigs = {
     "dfk_tp_sym_create": ([_vp, _i64, _i64, _vp], C.c_int),
     "dfk_tp_sym_open": ([_vp, _vp, C.c_int, C.c_int], C.c_int),
     "dfk_tp_sym_attach": ([C.POINTER(_vp), C.c_int], C.c_int),
-    "dfk_tp_forward_fused": ([_vp, _vp, _vp, _i64, _vp, C.POINTER(Config)], C.c_int),
+    "dfk_tp_forward_fused": ([_vp, _vp, _vp, _i64, _vp, _i32, C.POINTER(Config)], C.c_int),
     "dfk_profiler_range": ([_vp, C.c_int32], C.c_int),
     "dfk_decode": ([_vp, C.POINTER(_vp), C.c_int32, _vp, _i64, C.c_int32, _vp,
                     C.POINTER(Config), C.c_int32], C.c_int),
@@ -193,6 +202,8 @@ def _check(status: int) -> None:
         raise GateError(status, msg)
     if status == ERR_CACHE:
         raise CacheError(status, msg)
+    if status == ERR_TIMEOUT:
+        raise TimeoutError_(status, msg)
     raise DfkError(status, msg)
 
 
@@ -213,6 +224,27 @@ def block_bytes(batch: int, d_model: int, d_ff: int) -> Tuple[int, int]:
     s1, s2 = _i64(), _i64()
     _check(lib.dfk_block_bytes(batch, d_model, d_ff, C.byref(s1), C.byref(s2)))
     return s1.value, s2.value
+
+
+def cache_lookup(path: str, batch: int, d_model: int, d_ff: int,
+                 fingerprint: str) -> Optional[dict]:
+    """dfk_cache_lookup: the stored ScheduleEntry (a dict) or None on a miss;
+    CacheError on a corrupt / other-version file (tuner.hpp:108-113)."""
+    need, found = C.c_size_t(0), _i32(0)
+    _check(lib.dfk_cache_lookup(path.encode(), batch, d_model, d_ff, fingerprint.encode(),
+                                None, 0, C.byref(need), C.byref(found)))
+    if not found.value:
+        return None
+    buf = C.create_string_buffer(need.value)
+    _check(lib.dfk_cache_lookup(path.encode(), batch, d_model, d_ff, fingerprint.encode(),
+                                buf, need.value, C.byref(need), C.byref(found)))
+    return json.loads(buf.value.decode())
+
+
+def cache_store(path: str, entry: dict) -> None:
+    """dfk_cache_store: insert or replace the entry keyed by its shape and
+    fingerprint (tuner.hpp:102-106)."""
+    _check(lib.dfk_cache_store(path.encode(), json.dumps(entry).encode()))
 
 
 # --- bf16 helpers (host) ------------------------------------------------------
@@ -247,9 +279,9 @@ class DeviceArray:
         _check(lib.dfk_malloc(ctx.h, max(self.nbytes, 16), C.byref(p)))
         self.ptr = p.value
 
-    def __del__(self):
+    def __del__(self, _lib=lib):  # (module globals may be gone at exit)
         if getattr(self, "ptr", None) and self.ctx.h:
-            lib.dfk_free(self.ctx.h, self.ptr)
+            _lib.dfk_free(self.ctx.h, self.ptr)
             self.ptr = None
 
     def upload(self, host: np.ndarray) -> "DeviceArray":
@@ -298,29 +330,46 @@ class Weights:
     """One block's prepacked weights (dfk_weights_create)."""
 
     def __init__(self, ctx: "Context", w_gate, w_up, w_down, ff_range=None):
+        """w_down None: a stage-1-only set; w_gate and w_up None: a
+        down-only set (dfk_weights_create)."""
         self.ctx = ctx
         self.h = None
-        if isinstance(w_gate, DeviceArray):
-            dm, df = w_gate.shape
-            dtype, mem = w_gate.dtype, DEVICE
-            ptrs = [w_gate.ptr, w_up.ptr, w_down.ptr]
+        present = [a for a in (w_gate, w_up, w_down) if a is not None]
+        if not present:
+            raise InvalidArgument("no weight matrix given")
+        if isinstance(present[0], DeviceArray):
+            if w_gate is not None:
+                dm, df = w_gate.shape
+            else:
+                df, dm = w_down.shape
+            dtype, mem = present[0].dtype, DEVICE
+            ptrs = [a.ptr if a is not None else None for a in (w_gate, w_up, w_down)]
             keep = ()
         else:
-            w_gate, w_up, w_down = (np.asarray(a) for a in (w_gate, w_up, w_down))
-            dm, df = w_gate.shape
-            if w_up.shape != (dm, df) or w_down.shape != (df, dm):
+            w_gate, w_up, w_down = (np.asarray(a) if a is not None else None
+                                    for a in (w_gate, w_up, w_down))
+            if w_gate is not None:
+                dm, df = w_gate.shape
+            else:
+                df, dm = w_down.shape
+            if ((w_up is not None and w_up.shape != (dm, df)) or
+                    (w_gate is not None and w_gate.shape != (dm, df)) or
+                    (w_down is not None and w_down.shape != (df, dm))):
                 raise ShapeError(
-                    f"MlpWeights: w_up {w_up.shape}, w_gate {w_gate.shape}, "
-                    f"w_down {w_down.shape} are inconsistent")
-            if w_gate.dtype == np.uint16:
+                    f"MlpWeights: w_up {getattr(w_up, 'shape', None)}, w_gate "
+                    f"{getattr(w_gate, 'shape', None)}, w_down "
+                    f"{getattr(w_down, 'shape', None)} are inconsistent")
+            first = next(a for a in (w_gate, w_up, w_down) if a is not None)
+            if first.dtype == np.uint16:
                 dtype = BF16
-            elif w_gate.dtype == np.float32:
+            elif first.dtype == np.float32:
                 dtype = F32
             else:
                 dtype = F64
             npdt = {BF16: np.uint16, F32: np.float32, F64: np.float64}[dtype]
-            keep = tuple(np.ascontiguousarray(a, dtype=npdt) for a in (w_gate, w_up, w_down))
-            ptrs = [a.ctypes.data for a in keep]
+            keep = tuple(np.ascontiguousarray(a, dtype=npdt) if a is not None else None
+                         for a in (w_gate, w_up, w_down))
+            ptrs = [a.ctypes.data if a is not None else None for a in keep]
             mem = HOST
         f0, f1 = ff_range if ff_range is not None else (0, df)
         h = _vp()
@@ -331,11 +380,11 @@ class Weights:
         self.d_model, self.d_ff_total = int(dm), int(df)
         self.ff_begin, self.d_ff = int(f0), int(f1 - f0)
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         # The context frees every weight set it still owns when it is closed;
         # only destroy explicitly while it is alive.
         if getattr(self, "h", None) and getattr(self.ctx, "h", None):
-            lib.dfk_weights_destroy(self.h)
+            _lib.dfk_weights_destroy(self.h)
         self.h = None
 
     @property
@@ -355,9 +404,9 @@ class Context:
         self.h = h.value
         self.device = device
 
-    def close(self):
+    def close(self, _lib=lib):
         if getattr(self, "h", None):
-            lib.dfk_context_destroy(self.h)
+            _lib.dfk_context_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -522,8 +571,9 @@ class Context:
 
     def tp_forward_fused(self, w: Weights, x: DeviceArray, y: DeviceArray,
                          cfg: Optional[Config] = None):
-        assert y.dtype == F32
-        _check(lib.dfk_tp_forward_fused(self.h, w.h, x.ptr, x.shape[0], y.ptr,
+        """This rank's block with the all-reduce inside the kernel; y (F32 or
+        BF16) receives the full sum over ranks."""
+        _check(lib.dfk_tp_forward_fused(self.h, w.h, x.ptr, x.shape[0], y.ptr, y.dtype,
                                         self._cfg(cfg)))
 
     def tp_forward(self, w: Weights, x: DeviceArray, y: DeviceArray,
@@ -538,9 +588,9 @@ class Event:
         _check(lib.dfk_event_create(C.byref(h)))
         self.h = h.value
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "h", None):
-            lib.dfk_event_destroy(self.h)
+            _lib.dfk_event_destroy(self.h)
             self.h = None
 
     def record(self, ctx: Context):
@@ -564,8 +614,8 @@ class PinnedHost:
         buf = (C.c_char * n).from_address(self.ptr)
         self.arr = np.frombuffer(buf, dtype=dtype).reshape(shape)
 
-    def __del__(self):
+    def __del__(self, _lib=lib):
         if getattr(self, "ptr", None):
             self.arr = None
-            lib.dfk_host_free(self.ptr)
+            _lib.dfk_host_free(self.ptr)
             self.ptr = None

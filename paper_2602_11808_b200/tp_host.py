@@ -13,6 +13,10 @@ it can be exercised on CPU with the gloo backend (tests/test_tp_gloo.py):
 * setup_fused  — the fused all-reduce's symmetric workspaces: every rank's
                  64-byte CUDA IPC handle all-gathered, peers opened, and the
                  ranks agree (all or none) on using it.
+
+`dist` is any object with torch.distributed's object collectives
+(broadcast_object_list, all_gather_object) -- the launcher's process group;
+this module imports no torch itself.
 """
 from __future__ import annotations
 
@@ -40,23 +44,27 @@ def exchange_uid(dist, rank: int, make_uid: Optional[Callable[[], bytes]] = None
     return bytes(uid)
 
 
-def max_over_ranks(dist, value: float) -> float:
+def _gather(dist, obj) -> list:
     if dist is None:
-        return value
-    import torch
-    t = torch.tensor([value], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+def max_over_ranks(dist, value: float) -> float:
+    return float(max(_gather(dist, float(value))))
 
 
 def sum_partials(dist, partial: np.ndarray) -> np.ndarray:
-    """All-reduce(sum) of a host fp64 partial (one collective of B x d_model)."""
-    if dist is None:
-        return partial
-    import torch
-    t = torch.from_numpy(np.ascontiguousarray(partial, dtype=np.float64).copy())
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return t.numpy()
+    """All-reduce(sum) of a host fp64 partial (one collective of B x d_model),
+    summed in rank order like the reference's simulated_all_reduce
+    (tp.cpp:90-105)."""
+    parts = _gather(dist, np.ascontiguousarray(partial, dtype=np.float64))
+    total = np.zeros_like(parts[0])
+    for p in parts:
+        total += p
+    return total
 
 
 def setup_fused(dist, ctx, rank: int, world: int, max_batch: int, d_model: int) -> bool:
@@ -78,9 +86,4 @@ def setup_fused(dist, ctx, rank: int, world: int, max_batch: int, d_model: int) 
             ctx.tp_sym_open(handles, rank, world)
         except Exception:  # noqa: BLE001
             ok = 0
-    if dist is not None:
-        import torch
-        t = torch.tensor([ok], dtype=torch.int32)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        ok = int(t.item())
-    return bool(ok)
+    return bool(min(_gather(dist, ok)))

@@ -275,20 +275,70 @@ TEST_CASE("fill_uniform is deterministic and in range", t_fill) {
   }
 }
 
-// tuner.cpp:408-424: warm cache skips profiling
-TEST_CASE("Tuner: warm cache skips profiling", t_tuner) {
+// The library's on-device scheduler through the shim (dfk_tune): a second
+// call with the same shape and cache file is a cache hit.
+TEST_CASE("tune_on_device: warm cache skips profiling", t_tuner) {
   Instance inst = random_instance({4, 256, 512}, 7, 1.0 / 16);
   const std::string path = std::string(std::getenv("DFK_TEST_TMP") ? std::getenv("DFK_TEST_TMP") : "/tmp") +
                            "/dfk_cpp_tuner_cache.json";
   std::remove(path.c_str());
-  Tuner t({path, 1, 3});
-  const ScheduleEntry e1 = t.get_or_tune({4, 256, 512}, inst.w);
-  CHECK(!e1.from_cache && t.profile_invocations() == 1 && !e1.chosen.empty());
-  const ScheduleEntry e2 = t.get_or_tune({4, 256, 512}, inst.w);
-  CHECK(e2.from_cache && t.last_was_cache_hit() && t.profile_invocations() == 1);
+  const ScheduleEntry e1 = tune_on_device({4, 256, 512}, inst.w, path, 1, 3);
+  CHECK(!e1.chosen.empty() && e1.all_results.size() > 3);
+  for (const BenchmarkResult& r : e1.all_results)
+    if (!r.disqualified) CHECK(r.samples_ns.size() == 3 && r.median_ns > 0);
+  const ScheduleEntry e2 = tune_on_device({4, 256, 512}, inst.w, path, 1, 3);
   CHECK(e2.chosen == e1.chosen);
   CHECK(!default_fingerprint().empty());
+  // the chosen configuration runs through the reference entry point
+  const Matrix y = run_variant({VariantTag::Fused, {}, e1.chosen}, inst.x, inst.w);
+  CHECK(rel_err(y, oracle_forward(inst.x, inst.w)) <= 1e-2);
   std::remove(path.c_str());
+}
+
+// The weight-pack cache keys on the matrices' exact contents: an in-place
+// edit (same storage, same shape) is seen by the next call.
+TEST_CASE("in-place weight edits are never served a stale GPU pack", t_stale) {
+  Instance inst = random_instance({3, 128, 384}, 11, 1.0 / 8);
+  const Matrix y0 = run_fused(inst.x, inst.w, {});
+  CHECK(rel_err(y0, oracle_forward(inst.x, inst.w)) <= 1e-2);
+  for (Index i = 0; i < inst.w.w_down.size(); ++i) inst.w.w_down.data()[i] *= -0.5;
+  const Matrix y1 = run_fused(inst.x, inst.w, {});
+  CHECK(rel_err(y1, oracle_forward(inst.x, inst.w)) <= 1e-2);
+  inst.w.w_up(5, 7) = 3.0;  // one element, through operator()
+  Matrix a2(3, 384), a2b(3, 384);
+  run_fused_stage1(inst.x, inst.w.w_up, inst.w.w_gate, {}, a2);
+  run_two_kernel_stage1(inst.x, inst.w, a2b);
+  CHECK(rel_err(a2, a2b) <= 1e-2);
+  // stage-only sets: the down projection alone, same matrix reused
+  const Matrix y2 = down_projection(a2b, inst.w.w_down);
+  CHECK(rel_err(y2, oracle_forward(inst.x, inst.w)) <= 2e-2);
+}
+
+// fused.cpp:218-239
+TEST_CASE("predicted_reuse_counts: weights once in column-major order", t_reuse) {
+  const ReuseCounts col = predicted_reuse_counts({4, 8, 16}, {4, 4, 8, LoopOrder::ColumnMajorTiling});
+  CHECK(col.x_reads == 4u * 8u * 4u && col.weight_reads == 2u * 8u * 16u && col.a2_writes == 64u);
+  const ReuseCounts row = predicted_reuse_counts({4, 8, 16}, {2, 16, 8, LoopOrder::RowMajorTiling});
+  CHECK(row.x_reads == 32u && row.weight_reads == 2u * 8u * 16u * 2u);
+}
+
+// verification.hpp:27-53: the injectable fused stage 1 and its mutants.
+TEST_CASE("verification seam: mutants deviate, the product does not", t_mutants) {
+  Instance inst = random_instance({4, 512, 384}, 13, 1.0 / 16);
+  Matrix ref(4, 384);
+  run_two_kernel_stage1(inst.x, inst.w, ref);
+  using namespace verification;
+  CHECK(mutant_from_string("silu-per-k-chunk") == Mutant::SiluPerKChunk);
+  CHECK(!mutant_from_string("bogus").has_value());
+  const TileConfig tile{4, 64, 128};
+  Matrix a(4, 384), b(4, 384), c(4, 384);
+  fused_stage1_for(Mutant::None)(inst.x, inst.w.w_up, inst.w.w_gate, tile, a);
+  fused_stage1_for(Mutant::SiluPerKChunk)(inst.x, inst.w.w_up, inst.w.w_gate, tile, b);
+  fused_stage1_for(Mutant::MaterializeIntermediate)(inst.x, inst.w.w_up, inst.w.w_gate, tile, c);
+  CHECK(rel_err(a, ref) <= 1e-2);
+  CHECK(rel_err(b, ref) > 5e-2);   // SiLU per K chunk: numerics break
+  CHECK(rel_err(c, ref) <= 1e-2);  // materialising: numerics intact (traffic trips)
+  CHECK(max_abs_diff(a, a) == 0.0);
 }
 
 int main() {

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _built():
     from paper_2602_11808_b200 import build as b
-    if not (os.path.exists(b.SHIM_LIB) and os.path.exists(b.CPP_TEST)):
+    if not all(os.path.exists(p) for p in (b.SHIM_LIB, b.CPP_TEST, b.CPP_TUNER_TEST)):
         b.build_cpp()
     return b
 
@@ -26,17 +26,30 @@ def test_shim_exports_reference_api():
                 "deepfusion::run_stage1(", "deepfusion::run_tp_mlp(",
                 "deepfusion::balanced_ranges(", "deepfusion::make_plan(",
                 "deepfusion::Tuner::get_or_tune(", "deepfusion::make_random_weights(",
-                "deepfusion::run_four_kernel(", "deepfusion::run_two_kernel("):
+                "deepfusion::run_four_kernel(", "deepfusion::run_two_kernel(",
+                "deepfusion::default_candidates(", "deepfusion::gpu_candidates(",
+                "deepfusion::make_runner(", "deepfusion::make_runners(",
+                "deepfusion::profile(", "deepfusion::select(", "deepfusion::cache_store(",
+                "deepfusion::cache_lookup(", "deepfusion::default_fingerprint",
+                "deepfusion::tune_on_device(", "deepfusion::predicted_reuse_counts(",
+                "deepfusion::verification::fused_stage1_for(",
+                "deepfusion::verification::fused_stage1_silu_per_k_chunk(",
+                "deepfusion::verification::fused_stage1_materializing("):
         assert sym in out, sym
     deps = subprocess.run(["ldd", b.SHIM_LIB], capture_output=True, text=True).stdout
     assert "libdfk.so" in deps
 
 
 @pytest.mark.gpu
-def test_reference_unit_tests_on_gpu(tmp_path):
+@pytest.mark.parametrize("which", ["CPP_TEST", "CPP_TUNER_TEST"])
+def test_reference_unit_tests_on_gpu(tmp_path, which):
+    """tests/cpp/test_deepfusion_gpu.cpp (operator API, TP, verification
+    seam) and tests/cpp/test_tuner_gpu.cpp (proj/tests/test_tuner.cpp
+    restated case for case)."""
     b = _built()
-    env = dict(os.environ, DFK_TEST_TMP=str(tmp_path))
-    r = subprocess.run([b.CPP_TEST], capture_output=True, text=True, env=env, timeout=600)
+    env = dict(os.environ, DFK_TEST_TMP=str(tmp_path), TMPDIR=str(tmp_path))
+    r = subprocess.run([getattr(b, which)], capture_output=True, text=True, env=env,
+                       timeout=900)
     print(r.stdout)
     print(r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
