@@ -309,6 +309,98 @@ def tp_shards(rt, ctx, ev0, ev1, batches=(1, 16, 64), reps=20):
     return out
 
 
+# --- configs 4/5 at N > 1: the whole tensor-parallel block, all-reduce included
+def tp_configs(rt, ctx, ev0, ev1, rank, P, tp_mode, barrier, max_over_ranks,
+               batches=(1, 16, 64), reps=20):
+    """BASELINE configs[3] (Qwen2.5-32B, TP 1/2/4/8) and configs[4]
+    (Llama-3.1-70B, TP 2/4/8) end to end on P ranks: every rank holds its
+    balanced_ranges shard (tp.cpp:8-29), the block ends in the ONE
+    all-reduce (tp.cpp:140-167) -- fused into the block kernel over NVLink
+    peer memory when tp_mode is "fused-nvlink", and NCCL's ncclAllReduce
+    after the block as the comparator.  µs per call = max over ranks of the
+    event-timed mean over `reps` calls on rotating weight sets (> 3x L2)."""
+    import math
+    out = {}
+    for name, dm, df, Ps in TP_SHAPES:
+        if P not in Ps:
+            continue
+        b0, b1 = rt.balanced_range(df, P, rank)
+        dfs = b1 - b0
+        nsets = max(2, math.ceil(3 * 126e6 / (3 * dm * dfs * 2)))
+        s = 1.0 / np.sqrt(dm)
+        ws = []
+        for i in range(nsets):
+            g = ctx.array((dm, df)).fill_uniform(9000 + 3 * i, -s, s)
+            u = ctx.array((dm, df)).fill_uniform(9001 + 3 * i, -s, s)
+            d = ctx.array((df, dm)).fill_uniform(9002 + 3 * i, -s, s)
+            ws.append(ctx.weights(g, u, d, ff_range=(b0, b1)))
+            del g, u, d
+        ctx.sync()
+        row = {}
+        for B in batches:
+            x = ctx.array((B, dm)).fill_uniform(31 + B)
+            y = ctx.array((B, dm), rt.F32)
+            arms = {}
+            fns = {"nccl": lambda w: ctx.tp_forward(w, x, y)}
+            if tp_mode == "fused-nvlink":
+                fns["fused"] = lambda w: ctx.tp_forward_fused(w, x, y)
+            for arm, fn in fns.items():
+                for i in range(4):
+                    fn(ws[i % nsets])
+                ctx.sync()
+                barrier()
+                ev0.record(ctx)
+                for i in range(reps):
+                    fn(ws[i % nsets])
+                ev1.record(ctx)
+                ctx.sync()
+                arms[arm] = max_over_ranks(ev0.elapsed_ms(ev1) * 1e3 / reps)
+            us = arms.get("fused", arms["nccl"])
+            gbs = block_bytes(B, dm, df // P) * P / (us * 1e-6) / 1e9
+            row[str(B)] = {"us": round(us, 2), "gbs_aggregate": round(gbs, 1),
+                           "nccl_allreduce_us": round(arms["nccl"], 2)}
+        out[f"{name} tp{P}"] = {"d_model": dm, "d_ff": df, "d_ff_shard": dfs,
+                                "allreduce": tp_mode, "per_batch": row}
+        del ws
+    return out
+
+
+# --- launcher: `bench.py --gpus N` without torchrun ----------------------------
+def self_launch(args) -> int:
+    """Starts N ranks of this script (one process per GPU, RANK / LOCAL_RANK /
+    WORLD_SIZE / MASTER_* in the environment, rendezvous on 127.0.0.1), the
+    way torchrun would; fails if fewer than N GPUs are visible."""
+    import socket
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True,
+                             timeout=60).stdout
+        visible = sum(1 for ln in out.splitlines() if ln.startswith("GPU "))
+    except Exception:  # noqa: BLE001
+        visible = 0
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if cvd is not None:
+        visible = min(visible, len([d for d in cvd.split(",") if d.strip()]))
+    if visible < args.gpus and not args.tp_emulate:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+              f"found {visible}", file=sys.stderr, flush=True)
+        return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
 # --- GPU arm -----------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
@@ -328,8 +420,13 @@ def main():
     args.warmup = max(args.warmup, 3)
     sweep = [int(b) for b in args.sweep.split(",")]
 
+    if (args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours"):
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(1)
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1:
@@ -346,6 +443,9 @@ def main():
     from paper_2602_11808_b200 import tp_host
 
     P = world
+    if not args.tp_emulate and local_rank >= rt.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local_rank}, "
+                         f"{rt.device_count()} visible")
     dev = local_rank % rt.device_count() if args.tp_emulate else local_rank
     ctx = rt.Context(dev)
     tp_mode = None
@@ -528,6 +628,9 @@ def main():
     shards = None
     if P == 1 and not args.no_tp_shards:
         shards = tp_shards(rt, ctx, ev0, ev1)
+    tp_full = None
+    if P > 1 and not args.no_tp_shards and not args.tp_emulate:
+        tp_full = tp_configs(rt, ctx, ev0, ev1, rank, P, tp_mode, barrier, max_over_ranks)
 
     # ---- CPU baseline: reference path, rank 0, N=1 only ----
     cpu = None
@@ -580,6 +683,7 @@ def main():
             "cpu_baseline": cpu,
             "decode_loop": decode,
             "tp_rank_blocks": shards,
+            "tp_configs": tp_full,
         }
         print(json.dumps(line), flush=True)
     barrier()

@@ -599,6 +599,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
         a.tp_y[r] = tp->tp_y[r] ? tp->tp_y[r] + b0 * y_ld : nullptr;
       }
       a.yacc_ld = tp->yacc_ld;
+      a.tp_late_trigger = ctx->tp_colocated ? 1 : 0;
     }
     if (ctx->pend_x_ready && b0 == 0 && B <= L.chunk) {  // host-buffer X flags
       a.x_ready = ctx->pend_x_ready;
@@ -630,6 +631,9 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
                               ctx->sm_count * 3 / 4);
     if (knobs().grid > 0 && cfg.s1_ctas <= 0) grid = knobs().grid;
     grid = std::max(1, std::min(grid, ctx->sm_count));
+    // Ranks sharing this GPU (emulation): every rank's launch must fit
+    // beside the others' (they wait for each other's contributions).
+    if (tp && ctx->tp_colocated) grid = std::max(1, std::min(grid, ctx->sm_count / tp->tp_size));
     grid = std::min(grid / a.split_k, cluster_cap(kModeBlock, a)) * a.split_k;
     grid = std::max(grid, a.split_k);
     block_plan(grid, w, &a);
@@ -1228,8 +1232,7 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
   const size_t xb = xn * 2;
   const size_t yb = xn * 4;
   if (ctx->hx_pinned_bytes < xb) {
-    if (ctx->err_host) cudaFreeHost(ctx->err_host);
-  if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
+    if (ctx->hx_pinned) cudaFreeHost(ctx->hx_pinned);
     DFK_CUDA(cudaMallocHost(&ctx->hx_pinned, xb));
     ctx->hx_pinned_bytes = xb;
   }

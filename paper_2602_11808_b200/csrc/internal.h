@@ -137,6 +137,12 @@ struct dfk_context_s {
   int* err_dev = nullptr;
   void* tp_peer[8] = {};
   bool tp_peer_ipc[8] = {};
+  // Some peer rank runs on THIS GPU (tests emulate ranks this way): its
+  // kernels must be able to become resident next to ours, so fused-TP
+  // launches take at most sm_count / P CTAs and let the next launch in the
+  // stream start only after their Y is complete (see the kernel's PDL
+  // trigger).
+  bool tp_colocated = false;
 
   // Decode loop (decode.cpp): bf16 ping-pong activations, fp32 TP partial,
   // captured sequences keyed by (layers, batch, steps, buffers, config).

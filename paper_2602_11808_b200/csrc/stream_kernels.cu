@@ -1473,7 +1473,8 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
 
   // Let the next kernel in the stream get scheduled as SMs drain; it only
   // touches our outputs after its own griddepcontrol.wait.
-  pdl_launch_dependents();
+  const bool late_trigger = kMode == kModeBlock && a.tp_size > 1 && a.tp_late_trigger;
+  if (!late_trigger) pdl_launch_dependents();
 
   if (w == 0) {
     produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty, pq);
@@ -1495,6 +1496,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   if (kMode == kModeBlock && a.tp_size > 1) {
     tp_collect_y(a, smem_flag);
     __syncthreads();
+    if (late_trigger) pdl_launch_dependents();
   }
   if (a.dynamic && threadIdx.x == 0) {
     // The last CTA out re-arms the work counter for the next launch.

@@ -130,6 +130,10 @@ struct StreamArgs {
   int* tp_cnt[kMaxTp];
   int* tp_done[kMaxTp];  // per down tile
   float* tp_y[kMaxTp];
+  // A peer rank shares this GPU: trigger the next PDL launch only after
+  // this rank's Y is complete (an early dependent would occupy the SMs the
+  // peer's kernel needs to make progress).
+  int tp_late_trigger;
   // Error word (host-mapped; dfk_context_sync reports it): set when a wait
   // on another rank (or on the host path's X copy) gives up after 4 s.
   int* tp_error;

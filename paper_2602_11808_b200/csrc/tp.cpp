@@ -58,6 +58,7 @@ void close_peers(dfk_context_s* ctx) {
     ctx->tp_peer[r] = nullptr;
     ctx->tp_peer_ipc[r] = false;
   }
+  ctx->tp_colocated = false;
 }
 
 }  // namespace
@@ -274,6 +275,12 @@ int dfk_tp_sym_open(dfk_context ctx, const void* handles, int rank, int nranks) 
     }
     ctx->tp_peer[r] = p;
     ctx->tp_peer_ipc[r] = true;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, p) == cudaSuccess) {
+      if (pa.device == ctx->device) ctx->tp_colocated = true;
+    } else {
+      cudaGetLastError();
+    }
   }
   ctx->tp_sym_rank = rank;
   ctx->tp_sym_size = nranks;
@@ -292,6 +299,7 @@ int dfk_tp_sym_attach(dfk_context* ctxs, int n) {
     DFK_CUDA(cudaSetDevice(ctxs[i]->device));
     close_peers(ctxs[i]);
     for (int j = 0; j < n; ++j) {
+      if (j != i && ctxs[j]->device == ctxs[i]->device) ctxs[i]->tp_colocated = true;
       if (ctxs[j]->device != ctxs[i]->device) {
         cudaError_t e = cudaDeviceEnablePeerAccess(ctxs[j]->device, 0);
         if (e == cudaErrorPeerAccessAlreadyEnabled) {
