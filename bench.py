@@ -75,7 +75,7 @@ def stream_floor():
         return None
     best = None
     for ln in out.splitlines():
-        if ln.startswith("launch pdl=1") and "GB/s" in ln:
+        if ln.startswith("launch") and "pdl=1" in ln and "GB/s" in ln:
             us = float(ln.split(":")[1].split("us/launch")[0])
             gbs = float(ln.split("us/launch")[1].split("GB/s")[0])
             if best is None or gbs > best["gbs"]:

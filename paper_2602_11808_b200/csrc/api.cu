@@ -262,6 +262,8 @@ struct Knobs {
   int grid = env_int("DFK_GRID", 0);                // block-kernel CTAs (0 = heuristic)
   int host_stagek = env_int("DFK_HOST_STAGEK", 0);  // host path: staging kernel
   int red_v4 = env_int("DFK_RED_V4", 1);            // 0 off, 1 small shards, 2 always
+  int trace_rel = env_int("DFK_TRACE_REL", 0);      // trace: stage release / MMA issue times
+  int bal = env_int("DFK_BAL", 0);                  // balanced stream-K: 0 off, 1 small shards, 2 always
 };
 
 const Knobs& knobs() {
@@ -385,7 +387,10 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
   const int sk = a->split_k > 1 ? a->split_k : 1;
   a->kbs = pick_kbs(ctx, n_pad, cfg.kbs, sk, a->a2_tma);
   a->trace = ctx->trace;
-  if (a->trace) a->trace_s0 = knobs().trace_s0;
+  if (a->trace) {
+    a->trace_s0 = knobs().trace_s0;
+    a->trace_rel = knobs().trace_rel;
+  }
   a->tp_error = ctx->err_dev;
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
@@ -638,6 +643,18 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     grid = std::max(grid, a.split_k);
     block_plan(grid, w, &a);
     if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
+    if (a.dynamic && (knobs().bal >= 2 || (knobs().bal == 1 && w->s1_tiles < grid))) {
+      // balanced stream-K pieces: partial stage-1 tiles need the workspace
+      a.bal = 1;
+      a.red_v4 = knobs().red_v4 >= 1;
+      DFK_TRY(ensure_buf(ctx, ctx->s1acc,
+                         static_cast<size_t>(w->s1_tiles) * a.n_pad * kBlockRows * 4, true,
+                         ctx->stream));
+      DFK_TRY(ensure_buf(ctx, ctx->s1cnt, static_cast<size_t>(w->s1_tiles) * 4, true,
+                         ctx->stream));
+      a.s1acc = static_cast<float*>(ctx->s1acc.p);
+      a.s1cnt = static_cast<int*>(ctx->s1cnt.p);
+    }
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,

@@ -226,6 +226,48 @@ __device__ __forceinline__ bool decode_dyn(const StreamArgs& a, int mode,
   return true;
 }
 
+// Balanced stream-K: the qi-th piece of CTA c of G (see StreamArgs::bal).
+// Stage-1 pieces first, then down pieces, each range split at tile
+// boundaries of its flattened (tile, K block) space.
+__device__ __forceinline__ bool bal_range_piece(int64_t r0, int64_t r1, int kbt, int qi,
+                                                int* tile, int* kb0, int* kb1, int* n) {
+  if (r1 <= r0) {
+    *n = 0;
+    return false;
+  }
+  const int t0 = static_cast<int>(r0 / kbt);
+  *n = static_cast<int>((r1 - 1) / kbt) - t0 + 1;
+  if (qi >= *n) return false;
+  const int t = t0 + qi;
+  const int64_t lo = static_cast<int64_t>(t) * kbt;
+  *tile = t;
+  *kb0 = static_cast<int>((r0 > lo ? r0 : lo) - lo);
+  *kb1 = static_cast<int>((r1 < lo + kbt ? r1 : lo + kbt) - lo);
+  return true;
+}
+
+__device__ __forceinline__ bool bal_piece(const StreamArgs& a, int mode, int64_t c,
+                                          int64_t G, int qi, Piece& out) {
+  int n1 = 0;
+  if (mode != kModeDown) {
+    const int64_t U1 = static_cast<int64_t>(a.t1) * a.kb1;
+    if (bal_range_piece(U1 * c / G, U1 * (c + 1) / G, a.kb1, qi, &out.tile, &out.kb0,
+                        &out.kb1, &n1)) {
+      out.down = 0;
+      return true;
+    }
+  }
+  if (mode == kModeStage1) return false;
+  const int64_t U2 = static_cast<int64_t>(a.t2) * a.kb2;
+  int n2 = 0;
+  if (bal_range_piece(U2 * c / G, U2 * (c + 1) / G, a.kb2, qi - n1, &out.tile, &out.kb0,
+                      &out.kb1, &n2)) {
+    out.down = 1;
+    return true;
+  }
+  return false;
+}
+
 // The consumers' view of the piece sequence (static plan or queue).
 struct PieceReader {
   int i = 0;
@@ -535,8 +577,10 @@ __device__ __forceinline__ void down_finish_tile(const StreamArgs& a,
   if (tid == 0) {
     if (stamp) trace_stamp(a, 41);
     if (stamp) trace_stamp(a, 42);
-    const int old = atom_add_acq_rel_gpu(&a.counters[t], 1);
-    const int last = (old == down_tile_pieces(a, p, t) - 1) ? 1 : 0;
+    // dynamic: count K blocks (pieces of a tile may differ in size)
+    const int old = atom_add_acq_rel_gpu(&a.counters[t], a.dynamic ? nk : 1);
+    const int last = a.dynamic ? (old + nk == a.kb2 ? 1 : 0)
+                               : (old == down_tile_pieces(a, p, t) - 1 ? 1 : 0);
     if (stamp) trace_stamp(a, 43);
     *smem_flag = last;  // the acquire is shared through the barrier below
   }
@@ -615,15 +659,16 @@ __device__ __forceinline__ float* s1acc_at(const StreamArgs& a, int t, int n) {
 
 // Tail of a partial stage-1 piece: the CTA adding the tile's last piece
 // turns the full sums into A2, re-zeroes the workspace and publishes.
-__device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t,
+__device__ __forceinline__ void s1_finish_tile(const StreamArgs& a, int t, int nk,
                                                int tid, int nthr,
                                                int* smem_flag, bool stamp = false) {
   named_bar(1, nthr);  // then one fence: see down_finish_tile
   if (tid == 0) {
     if (stamp) trace_stamp(a, 46);
     if (stamp) trace_stamp(a, 47);
-    const int old = atom_add_acq_rel_gpu(&a.s1cnt[t], 1);
-    const int last = (old == s1_pieces(a) - 1) ? 1 : 0;
+    // K blocks of the tile's pieces so far (pieces may differ in size)
+    const int old = atom_add_acq_rel_gpu(&a.s1cnt[t], nk);
+    const int last = (old + nk == a.kb1) ? 1 : 0;
     if (stamp) trace_stamp(a, 48);
     *smem_flag = last;  // the acquire is shared through the barrier below
   }
@@ -802,14 +847,18 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     if (!a.dynamic) {
       valid = pi.next(a, p, pc);
     } else {
-      int64_t idx = blockIdx.x;
-      if (qi > 0) {
-        if (!waited) flush();  // no global atomics before the previous grid ends
-        int got = 0;
-        if (leader) got = atomicAdd(a.sched, 1);
-        idx = static_cast<int64_t>(gridDim.x) + __shfl_sync(0xffffffffu, got, 0);
+      if (a.bal) {
+        valid = bal_piece(a, p.mode, blockIdx.x, gridDim.x, qi, pc);
+      } else {
+        int64_t idx = blockIdx.x;
+        if (qi > 0) {
+          if (!waited) flush();  // no global atomics before the previous grid ends
+          int got = 0;
+          if (leader) got = atomicAdd(a.sched, 1);
+          idx = static_cast<int64_t>(gridDim.x) + __shfl_sync(0xffffffffu, got, 0);
+        }
+        valid = decode_dyn(a, p.mode, idx, pc);
       }
-      valid = decode_dyn(a, p.mode, idx, pc);
       const int slot = qi % kPieceQueue;
       if (qi >= kPieceQueue) {
         if (leader)
@@ -841,6 +890,10 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
         if (npend > 0 && pend[0].it <= it - a.stages) flush();
         if (leader) mbar_wait(&empty[slot], phase ^ 1u);
         __syncwarp();
+        // trace_rel: when the producer saw stage (it - stages) released
+        if (leader && a.trace && a.trace_rel && it - a.stages >= a.trace_s0 &&
+            it - a.stages < a.trace_s0 + 12)
+          trace_stamp(a, 40 + static_cast<int>(it - a.stages - a.trace_s0));
       }
       uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
       if (leader) {
@@ -852,7 +905,8 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                  wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
                              static_cast<int64_t>(kBlockBytes),
                  static_cast<uint32_t>(nb) * kBlockBytes, &full[slot], policy);
-        if (a.trace && a.trace_s0 >= 0 && it >= a.trace_s0 && it < a.trace_s0 + 12)
+        if (a.trace && !a.trace_rel && a.trace_s0 >= 0 && it >= a.trace_s0 &&
+            it < a.trace_s0 + 12)
           trace_stamp(a, 40 + static_cast<int>(it - a.trace_s0));
       }
       // Activation loads stay in stage order: defer while anything is
@@ -970,7 +1024,7 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
           if (c == 0 && n < a.B) atomicAdd(s1acc_at(a, pc.tile, n) + row, v);
         }
       }
-      s1_finish_tile(a, pc.tile, tid, nthr, smem_flag);
+      s1_finish_tile(a, pc.tile, pc.kb1 - pc.kb0, tid, nthr, smem_flag);
     } else if (!pc.down) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -1072,7 +1126,8 @@ __device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
     for (int kb = pc.kb0; kb < pc.kb1; kb += a.kbs, ++it) {
       const int nb = min(a.kbs, pc.kb1 - kb);
       mbar_wait(&full[slot], phase);
-      if (a.trace && a.trace_s0 >= 0 && it >= a.trace_s0 && it < a.trace_s0 + 12)
+      if (a.trace && !a.trace_rel && a.trace_s0 >= 0 && it >= a.trace_s0 &&
+          it < a.trace_s0 + 12)
         trace_stamp(a, 52 + static_cast<int>(it - a.trace_s0));
       tc_fence_after();
       const uint32_t sbase = smem0 + static_cast<uint32_t>(slot * stage_bytes);
@@ -1080,6 +1135,9 @@ __device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
       const uint64_t dx = desc0 + ((sbase + wbytes_all) >> 4);
       mma_stage_nb<NACC>(nb, d, dw, dx, idesc, xblk16, chain_cols, kb == pc.kb0);
       tc_commit(&empty[slot]);
+      // trace_rel: the stage's MMAs and commit are issued
+      if (a.trace && a.trace_rel && it >= a.trace_s0 && it < a.trace_s0 + 12)
+        trace_stamp(a, 52 + static_cast<int>(it - a.trace_s0));
       if (++slot == a.stages) {
         slot = 0;
         phase ^= 1u;
@@ -1269,7 +1327,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      s1_finish_tile(a, pc.tile, tid, 128, smem_flag, s1_stamp);
+      s1_finish_tile(a, pc.tile, pc.kb1 - pc.kb0, tid, 128, smem_flag, s1_stamp);
     } else if (!pc.down && a.a2_tma) {
       // A2 tile -> swizzled smem [n][64 cols] bf16 -> one TMA store.  The
       // barrier first: the previous tile's store has been waited for by tid 0.

@@ -106,6 +106,13 @@ struct StreamArgs {
   // tile's flag and re-zeroes its workspace and counter.  Lets every SM
   // stream stage-1 weights when a (TP) shard has fewer tiles than SMs.
   int s1_chunk;
+  // Balanced stream-K (dynamic machinery, static pieces): CTA c takes the
+  // K-block ranges [c*U/G, (c+1)*U/G) of the flattened stage-1 space
+  // (U = t1*kb1) and then of the down space (U = t2*kb2), split at tile
+  // boundaries -- every CTA streams the same bytes in both phases.  Tile
+  // counters then count K blocks (a tile is complete when kb1 / kb2 of them
+  // have arrived).
+  int bal;
   float* s1acc;
   int* s1cnt;
   // K blocks of the first piece prefetched into L2 (cp.async.bulk.prefetch)
@@ -145,6 +152,10 @@ struct StreamArgs {
   // [40+j] weight copy issued, [52+j] full barrier passed (MMA lane).
   unsigned long long* trace;
   int trace_s0;
+  // trace_rel: slots 40+j / 52+j record when the producer saw ring stage
+  // trace_s0+j released / when the MMA lane finished issuing it (instead of
+  // weight-copy issue / full-barrier pass).
+  int trace_rel;
   // Partial-sum reductions (stage-1 stream-K, down pieces) as
   // red.global.add.v4.f32 after a 4 x 4 lane transpose (small shards).
   int red_v4;

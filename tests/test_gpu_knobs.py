@@ -4,7 +4,9 @@ in a fresh interpreter): stage-1 tiles writing A2 with per-thread global
 stores (DFK_A2_TMA=0), full 16-row activation boxes at B <= 8 (DFK_XROWS8=0),
 v4 partial-sum reductions on full shards too (DFK_RED_V4=2) or nowhere
 (DFK_RED_V4=0), two accumulator chains (DFK_NACC=2), the full grid and
-down chunks of 8 K blocks at every N (DFK_GRID / DFK_DN_CHUNK).  Shapes
+down chunks of 8 K blocks at every N (DFK_GRID / DFK_DN_CHUNK), balanced
+stream-K pieces (DFK_BAL: tile-straddling stage-1 and down ranges, K-block
+counted tile completion).  Shapes
 cover a full stage-1 wave (d_ff/64 >= SMs) and a small shard, B across the
 N = 16 / 32 / 64 MMA widths.
 """
@@ -51,6 +53,8 @@ print("worst", worst)
     {"DFK_RED_V4": "0"},
     {"DFK_NACC": "2"},
     {"DFK_GRID": "148", "DFK_DN_CHUNK": "8"},
+    {"DFK_BAL": "2"},
+    {"DFK_BAL": "1", "DFK_GRID": "140"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_knob_paths_match_oracle(env):
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)],

@@ -1,7 +1,7 @@
-export PYTHONFAULTHANDLER=1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()"; echo smoke rc=$?
-timeout 2400 python -m pytest tests -q -m gpu -rf --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
-tail -8 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --no-decode --sweep 1,16,64 --tp-emulate > gpurun_out/bench_emul2.json 2> gpurun_out/bench_emul2.err; echo emul rc=$?
-tail -c 1500 gpurun_out/bench_emul2.json; tail -5 gpurun_out/bench_emul2.err
-timeout 100 python bench.py --gpus 2 --steps 3; echo "gpus2-on-1 rc=$?"
+export AB_SHAPES=4096x1792,5120x3456,8192x3584,5120x6912
+AB_TAG=base python tools/shard_ab.py
+AB_TAG=static AB_CFG=block_kernel=1 python tools/shard_ab.py
+AB_TAG=sk2 AB_CFG=block_kernel=1,s1_split_k=2 python tools/shard_ab.py
+AB_TAG=sk4 AB_CFG=block_kernel=1,s1_split_k=4 python tools/shard_ab.py
+AB_TAG=sk8 AB_CFG=block_kernel=1,s1_split_k=8 python tools/shard_ab.py
+AB_TAG=nopdl AB_CFG=block_kernel=1,dynamic_sched=1,pdl=0 python tools/shard_ab.py

@@ -160,7 +160,11 @@ int main(int argc, char** argv) {
     // without PDL: the floor for a single-launch block of this size.
     cudaFuncSetAttribute(bulk_stream_pdl, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
-    const size_t per_launch = 352321536;
+    // optional per-launch sizes in MB after "launch" (default: 352 MB)
+    std::vector<size_t> sizes;
+    for (int i = 2; i < argc; ++i) sizes.push_back(size_t(atof(argv[i]) * 1e6) / 65536 * 65536);
+    if (sizes.empty()) sizes.push_back(352321536);
+    for (size_t per_launch : sizes)
     for (int pdl : {0, 1})
       for (int grid : {129, 148})
         for (int chunk : {32768, 65536}) {
@@ -181,8 +185,8 @@ int main(int argc, char** argv) {
             cudaLaunchKernelEx(&cfg, bulk_stream_pdl, src, per_cta, chunk, stages, sink);
           };
           float ms = time_it([&] { for (int i = 0; i < 40; ++i) one(i); });
-          printf("launch pdl=%d grid=%3d chunk=%6d stages=%d : %7.2f us/launch  %7.1f GB/s\n",
-                 pdl, grid, chunk, stages, ms * 1e3 / 40,
+          printf("launch %6.1fMB pdl=%d grid=%3d chunk=%6d stages=%d : %7.2f us/launch  %7.1f GB/s\n",
+                 per_launch / 1e6, pdl, grid, chunk, stages, ms * 1e3 / 40,
                  double(per_cta) * grid * 40 / ms / 1e6);
         }
     return 0;

@@ -166,10 +166,15 @@ if int(os.environ.get("DFK_TRACE_S0", 24)) < 0:
     sys.exit(0)
 iss = raw[:, 40:52].astype(np.int64)
 ful = raw[:, 52:64].astype(np.int64)
+nst = int(((iss > 0) & (ful > 0)).all(0).sum())  # stages every CTA traced
+iss, ful = iss[:, :max(nst, 2)], ful[:, :max(nst, 2)]
 ok = (iss > 0).all(1) & (ful > 0).all(1)
+if not ok.any():
+    print("ring stages: none traced on every CTA (pieces shorter than DFK_TRACE_S0 + 2)")
+    sys.exit(0)
 lat = (ful[ok] - iss[ok]) / 1e3
 gap = np.diff(ful[ok], axis=1) / 1e3
-print(f"ring stages {os.environ.get('DFK_TRACE_S0', 24)}+0..11 on {int(ok.sum())} CTAs: issue->full latency us "
+print(f"ring stages {os.environ.get('DFK_TRACE_S0', 24)}+0..{nst - 1} on {int(ok.sum())} CTAs: issue->full latency us "
       f"p10/med/p90 {np.percentile(lat, 10):.2f}/{np.median(lat):.2f}/"
       f"{np.percentile(lat, 90):.2f}; full->full spacing us p10/med/p90 "
       f"{np.percentile(gap, 10):.2f}/{np.median(gap):.2f}/{np.percentile(gap, 90):.2f}")
