@@ -52,6 +52,37 @@ void free_weights(dfk_weights_s* w) {
   delete w;
 }
 
+int clone_weights(dfk_context_s* ctx, const dfk_weights_s* w, dfk_weights_s** out) {
+  auto* c = new dfk_weights_s(*w);
+  c->s1_pack = c->dn_pack = nullptr;
+  c->cat_t = c->down_t = nullptr;
+  const size_t s1 = static_cast<size_t>(w->s1_tiles) * w->s1_kblocks * kBlockBytes;
+  const size_t dn = static_cast<size_t>(w->dn_tiles) * w->dn_kblocks * kBlockBytes;
+  if ((w->s1_pack && cudaMalloc(&c->s1_pack, s1) != cudaSuccess) ||
+      (w->dn_pack && cudaMalloc(&c->dn_pack, dn) != cudaSuccess)) {
+    cudaGetLastError();
+    free_weights(c);
+    return fail(DFK_ERR_NOMEM, "scheduler weight copy");
+  }
+  if (w->s1_pack) DFK_CUDA(cudaMemcpyAsync(c->s1_pack, w->s1_pack, s1,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+  if (w->dn_pack) DFK_CUDA(cudaMemcpyAsync(c->dn_pack, w->dn_pack, dn,
+                                           cudaMemcpyDeviceToDevice, ctx->stream));
+  *out = c;
+  return DFK_OK;
+}
+
+void release_clone(dfk_weights_s* w) {
+  if (w) free_weights(w);
+}
+
+int tp_degree(const dfk_context_s* ctx, const dfk_weights_s* w) {
+  int p = std::max(ctx->nranks, ctx->tp_sym_size);
+  if (w && w->d_ff > 0 && w->d_ff < w->d_ff_total)
+    p = std::max(p, static_cast<int>(std::lround(static_cast<double>(w->d_ff_total) / w->d_ff)));
+  return std::max(p, 1);
+}
+
 int ensure_buf(dfk_context_s* ctx, DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return DFK_OK;
@@ -263,6 +294,7 @@ struct Knobs {
   int host_stagek = env_int("DFK_HOST_STAGEK", 0);  // host path: staging kernel
   int red_v4 = env_int("DFK_RED_V4", 1);            // 0 off, 1 small shards, 2 always
   int trace_rel = env_int("DFK_TRACE_REL", 0);      // trace: stage release / MMA issue times
+  int lt_tune = env_int("DFK_LT_TUNE", 1);          // autotune the cuBLASLt comparator's algorithm
   int bal = env_int("DFK_BAL", 0);                  // balanced stream-K: 0 off, 1 small shards, 2 always
 };
 
@@ -729,10 +761,10 @@ int lt_gemm(dfk_context_s* ctx, const __nv_bfloat16* A, int64_t lda,
     size_t wsb = ws_bytes;
     cublasLtMatmulPreferenceSetAttribute(
         pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb));
-    cublasLtMatmulHeuristicResult_t res[4];
+    cublasLtMatmulHeuristicResult_t res[8];
     int got = 0;
     cublasStatus_t st = cublasLtMatmulAlgoGetHeuristic(
-        ctx->lt, op, la, lb, lc, lc, pref, 4, res, &got);
+        ctx->lt, op, la, lb, lc, lc, pref, 8, res, &got);
     cublasLtMatmulPreferenceDestroy(pref);
     if (st != CUBLAS_STATUS_SUCCESS || got == 0) {
       cublasLtMatmulDescDestroy(op);
@@ -741,7 +773,41 @@ int lt_gemm(dfk_context_s* ctx, const __nv_bfloat16* A, int64_t lda,
       cublasLtMatrixLayoutDestroy(lc);
       return fail(DFK_ERR_CUDA, "cuBLASLt: no algorithm for the unfused GEMM");
     }
-    algo = res[0].algo;
+    // Autotune the comparator: time every returned algorithm on these
+    // operands (1 warm-up + 5 calls each, events on the context stream)
+    // and keep the fastest -- the heuristic's first pick is often a
+    // split-K kernel far from the best on skinny (decode) GEMMs.  Not while
+    // the stream is being captured.
+    int best = 0;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ctx->stream, &cs);
+    if (got > 1 && cs == cudaStreamCaptureStatusNone && knobs().lt_tune) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      const float alpha = 1.f, beta = 0.f;
+      float best_ms = 1e30f;
+      for (int i = 0; i < got; ++i) {
+        bool ok = true;
+        for (int r = 0; r < 6 && ok; ++r) {
+          if (r == 1) cudaEventRecord(e0, ctx->stream);
+          ok = cublasLtMatmul(ctx->lt, op, &alpha, A, la, Bm, lb, &beta, C, lc, C, lc,
+                              &res[i].algo, ctx->lt_ws.p, ws_bytes,
+                              ctx->stream) == CUBLAS_STATUS_SUCCESS;
+        }
+        cudaEventRecord(e1, ctx->stream);
+        if (cudaEventSynchronize(e1) != cudaSuccess) ok = false;
+        float ms = 0.f;
+        if (ok && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < best_ms) {
+          best_ms = ms;
+          best = i;
+        }
+      }
+      cudaGetLastError();
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    algo = res[best].algo;
     ctx->lt_algos.emplace(key, algo);
   } else {
     algo = it->second;
@@ -1068,7 +1134,7 @@ int dfk_fingerprint(dfk_context ctx, char* buf, size_t len) {
   std::ostringstream o;
   o << ctx->name << "|sm_" << ctx->cc_major << ctx->cc_minor << "|" << ctx->sm_count
     << "SM|memclk" << mem_clock << "|drv" << ctx->driver_version << "|tp"
-    << ctx->nranks;
+    << tp_degree(ctx, nullptr);
   std::snprintf(buf, len, "%s", o.str().c_str());
   return DFK_OK;
 }

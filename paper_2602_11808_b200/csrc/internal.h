@@ -223,6 +223,14 @@ void default_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
                     dfk_config* out);
 int forward_impl(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
                  int64_t B, void* y, int y_dtype, const dfk_config* cfg);
+// An unregistered device copy of w's packs (the scheduler's rotating
+// weight sets: sub-L2 shards are timed cold, as in a layer chain), and its
+// release.
+int clone_weights(dfk_context_s* ctx, const dfk_weights_s* w, dfk_weights_s** out);
+void release_clone(dfk_weights_s* w);
+// Tensor-parallel degree a context / weight set stands for (the NCCL or
+// fused-TP rank count, or d_ff_total / d_ff of a balanced shard).
+int tp_degree(const dfk_context_s* ctx, const dfk_weights_s* w);
 struct StreamArgs;
 // One tensor-parallel block into fp32 Y (tp.cpp): the fused all-reduce when
 // the symmetric workspaces are set up, else the NCCL all-reduce, else

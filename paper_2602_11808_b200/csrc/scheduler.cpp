@@ -287,7 +287,13 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   int64_t dm = w->d_model, df = w->d_ff;
   char fpbuf[256];
   dfk_fingerprint(ctx, fpbuf, sizeof(fpbuf));
-  const std::string fp = fpbuf;
+  std::string fp = fpbuf;
+  {
+    // the TP degree this weight set stands for (a balanced shard tuned on
+    // one GPU, e.g. `tune --tp P`, keys like the P-rank run)
+    const size_t at = fp.rfind("|tp");
+    if (at != std::string::npos) fp = fp.substr(0, at) + "|tp" + std::to_string(tp_degree(ctx, w));
+  }
   const std::string path = cache_path ? cache_path : "";
   const auto key = std::make_tuple(batch, dm, df);
 
@@ -347,6 +353,29 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   cudaMemcpyAsync(href.data(), yref, yb, cudaMemcpyDeviceToHost, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
 
+  // Rotating weight copies: a shard whose packs fit in L2 would otherwise be
+  // timed from L2 on calls 2..8 of a run, unlike a decode chain whose every
+  // block streams its weights from HBM.  Enough copies that one run's
+  // working set exceeds ~3x L2 (at most one per call of a run).
+  std::vector<dfk_weights_s*> sets{w};
+  {
+    int64_t pack = 0;
+    dfk_weights_bytes(w, &pack);
+    const double l2 = static_cast<double>(ctx->l2_bytes > 0 ? ctx->l2_bytes : (126 << 20));
+    const int want = std::min<int>(kRepsPerRun, static_cast<int>(std::ceil(3.0 * l2 / std::max<int64_t>(pack, 1))));
+    for (int i = 1; i < want; ++i) {
+      dfk_weights_s* c = nullptr;
+      if (clone_weights(ctx, w, &c) != DFK_OK) break;  // fewer copies: still valid timings
+      sets.push_back(c);
+    }
+    cudaStreamSynchronize(ctx->stream);
+  }
+  auto release_sets = [&] {
+    cudaStreamSynchronize(ctx->stream);
+    for (size_t i = 1; i < sets.size(); ++i) release_clone(sets[i]);
+    sets.resize(1);
+  };
+
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -379,12 +408,14 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
       results.push_back(r);
       continue;
     }
-    for (int i = 0; i < warmup; ++i)
-      forward_impl(ctx, w, x, batch, y, DFK_F32, &c);
+    // warm-up touches every copy (the unfused layouts build their
+    // comparator matrices lazily, per weight set)
+    for (int i = 0; i < warmup * static_cast<int>(sets.size()); ++i)
+      forward_impl(ctx, sets[i % sets.size()], x, batch, y, DFK_F32, &c);
     for (int i = 0; i < runs; ++i) {
       cudaEventRecord(e0, ctx->stream);
       for (int k = 0; k < kRepsPerRun; ++k)
-        forward_impl(ctx, w, x, batch, y, DFK_F32, &c);
+        forward_impl(ctx, sets[k % sets.size()], x, batch, y, DFK_F32, &c);
       cudaEventRecord(e1, ctx->stream);
       cudaEventSynchronize(e1);
       float ms = 0.f;
@@ -398,6 +429,7 @@ int dfk_tune(dfk_context ctx, dfk_weights w, int64_t batch,
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  release_sets();
   cleanup();
 
   const Result* best = nullptr;

@@ -386,7 +386,7 @@ def test_scheduler_gate_select_and_cache(rt, ctx, oracle_lib, tmp_path):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("B", [1, 16])
+@pytest.mark.parametrize("B", [1, 16, 32, 64])
 def test_llama8b_full_shape_parity(rt, ctx, oracle_lib, B):
     """Config 1/2: Llama-3.1-8B MLP, d_model=4096,
     d_ff=14336, seed 20260809, vs the fp64 oracle on identical bf16 inputs."""
@@ -707,3 +707,43 @@ def test_fused_tp_and_decode_error_contract(rt, oracle_lib):
     finally:
         c0.close()
         c1.close()
+
+
+@pytest.mark.slow
+def test_llama8b_error_report(rt, ctx, oracle_lib):
+    """SURVEY §8c error report at the Llama-3.1-8B shape, default schedule,
+    B = 1 / 16 / 32 / 64: the gate (inf-norm relative error <= 1e-2), the
+    per-element relative error with a floor at 1e-3 * max|Y_ref|, and the
+    informational run against an oracle fed fp32 master weights (the total
+    bf16 quantisation error of inputs, A2 and accumulation order).  Written
+    to $DFK_REPORT_DIR/parity_errors.json (default gpurun_out/ when it
+    exists); profiles/r2_parity_errors.json is a committed copy."""
+    import json
+    dm, df = 4096, 14336
+    report = {"shape": {"d_model": dm, "d_ff": df}, "seed": 20260809,
+              "floor": "1e-3 * max|Y_ref|", "per_batch": {}}
+    for B in (1, 16, 32, 64):
+        x, wu, wg, wd = oracle_lib.make_instance(20260809, B, dm, df, 1.0 / np.sqrt(dm))
+        xq, wuq, wgq, wdq = (oracle_lib.quantize_bf16(a)[0] for a in (x, wu, wg, wd))
+        _, y_ref = oracle_lib.forward(xq, wuq, wgq, wdq)
+        f32 = [np.asarray(a, np.float32).astype(np.float64) for a in (x, wu, wg, wd)]
+        _, y_master = oracle_lib.forward(*f32)
+        w = ctx.weights(wgq, wuq, wdq)
+        xd = ctx.array((B, dm)).upload(xq)
+        y = ctx.array((B, dm), rt.F32)
+        ctx.forward(w, xd, y)
+        yg = y.download().astype(np.float64)
+        inf_err = rel_err(yg, y_ref)
+        floor = 1e-3 * np.abs(y_ref).max()
+        per_elem = float((np.abs(yg - y_ref) / np.maximum(np.abs(y_ref), floor)).max())
+        report["per_batch"][str(B)] = {
+            "inf_norm_rel": inf_err, "per_element_rel_floored": per_elem,
+            "inf_norm_rel_vs_fp32_master": rel_err(yg, y_master),
+            "oracle_bf16_vs_fp32_master": rel_err(y_ref, y_master)}
+        assert inf_err <= TOL, (B, inf_err)
+        del w
+    out_dir = os.environ.get("DFK_REPORT_DIR") or (
+        os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out"))
+    if os.path.isdir(out_dir):
+        with open(os.path.join(out_dir, "parity_errors.json"), "w") as f:
+            json.dump(report, f, indent=1)
