@@ -204,8 +204,9 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
 int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int split_k = 1, int a2_tma = 0) {
   const int avail = ctx->max_smem_optin - 1024 - 1024 - split_red_bytes(n_pad, split_k) -
                     a2_stage_bytes(n_pad, a2_tma);
-  int s = avail / stream_stage_bytes(n_pad, kbs);
-  return std::min(s, 32);
+  int s = std::min(avail / stream_stage_bytes(n_pad, kbs), 32);
+  while (s > 2 && stream_smem_bytes(n_pad, s, kbs, split_k, a2_tma) > ctx->max_smem_optin) --s;
+  return s;
 }
 
 // Bigger ring stages stream faster (tools/stream_probe.cu, profiles/): take

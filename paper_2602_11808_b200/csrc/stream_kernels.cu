@@ -774,7 +774,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                                         const CUtensorMap* xmap,
                                         const CUtensorMap* amap, uint8_t* smem,
                                         int stage_bytes, uint64_t* full,
-                                        uint64_t* empty, PieceQueue* pq) {
+                                        uint64_t* empty, PieceQueue* pq, int4* pend) {
   const bool leader = lane_id() == 0;
   const uint64_t policy = policy_evict_first();
   const uint32_t xblk = static_cast<uint32_t>(a.n_pad) * 128u;
@@ -783,12 +783,13 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
   // before griddepcontrol.wait (PDL), or -- down pieces -- until the stage-1
   // tiles they read have published.  Weight streaming never waits for
   // either: it runs ahead until the ring wraps onto a deferred stage.
-  struct Pend {
-    int slot, kb, nb, down, pk0, pk1, qi;
-    int64_t it;
-  };
-  Pend pend[32];  // stages <= 32, never more than a ring's worth deferred
+  // pend[] lives in shared memory (one entry per ring slot, written by the
+  // leader lane): a per-thread array indexed at run time would be a local
+  // memory stack frame whose write-backs add ~0.6 MB of L2 stores per launch.
+  // Entry: x = slot | nb << 8 | down << 12 | qi << 16, y = kb,
+  // z = pk0 | pk1 << 16 (the down piece's A2 K-block range).
   int npend = 0;
+  int64_t pend0_it = 0;  // ring stage of pend[0]
   ReadyCache rc;
   int64_t it = 0;
   bool waited = false;
@@ -832,13 +833,17 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       pdl_wait();
       waited = true;
     }
+    __syncwarp();  // the leader's pend[] writes
     for (int j = 0; j < npend; ++j) {
-      if (pend[j].down) ensure_ready(a, rc, pend[j].pk0, pend[j].pk1);
-      if (leader && pend[j].kb == pend[j].pk0 && pend[j].qi < 8)
-        trace_stamp(a, 32 + pend[j].qi);
-      act_loads(smem + static_cast<int64_t>(pend[j].slot) * stage_bytes + wbytes_all,
-                pend[j].kb, pend[j].nb, pend[j].down, &full[pend[j].slot]);
+      const int4 e = pend[j];
+      const int slot = e.x & 0xff, nb = (e.x >> 8) & 0xf, down = (e.x >> 12) & 1,
+                qi = e.x >> 16, kb = e.y, pk0 = e.z & 0xffff, pk1 = (e.z >> 16) & 0xffff;
+      if (down) ensure_ready(a, rc, pk0, pk1);
+      if (leader && kb == pk0 && qi < 8) trace_stamp(a, 32 + qi);
+      act_loads(smem + static_cast<int64_t>(slot) * stage_bytes + wbytes_all, kb, nb, down,
+                &full[slot]);
     }
+    __syncwarp();  // every lane has read pend[] before it is rewritten
     npend = 0;
   };
   for (int qi = 0;; ++qi) {
@@ -887,7 +892,7 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       if (it >= a.stages) {
         // The slot about to be reused holds a deferred stage: its consumer
         // cannot finish before we issue its activations.
-        if (npend > 0 && pend[0].it <= it - a.stages) flush();
+        if (npend > 0 && pend0_it <= it - a.stages) flush();
         if (leader) mbar_wait(&empty[slot], phase ^ 1u);
         __syncwarp();
         // trace_rel: when the producer saw stage (it - stages) released
@@ -914,7 +919,11 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       // yet published (non-blocking check).
       if (!waited || npend > 0 || (pc.down && !check_ready(a, rc, pc.kb0, pc.kb1))) {
         if (qi == 0 && !waited) first_issued += nb;
-        pend[npend++] = {slot, kb, nb, pc.down, pc.kb0, pc.kb1, qi, it};
+        if (npend == 0) pend0_it = it;
+        if (leader)
+          pend[npend] = make_int4(slot | (nb << 8) | (pc.down << 12) | (qi << 16), kb,
+                                  pc.kb0 | (pc.kb1 << 16), 0);
+        ++npend;
         continue;
       }
       if (leader && kb == pc.kb0 && qi < 8) trace_stamp(a, 32 + qi);
@@ -1487,9 +1496,11 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   uint64_t* red_free = red_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_free + 1);
   int* smem_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  // Split-K reduction buffer: after the barriers, 16-byte aligned.
-  float* red = reinterpret_cast<float*>(
+  // The producer's deferred-stage list (one int4 per ring slot), then the
+  // split-K reduction buffer, 16-byte aligned.
+  int4* pend = reinterpret_cast<int4*>(
       (reinterpret_cast<uintptr_t>(smem_flag + 4) + 15) & ~static_cast<uintptr_t>(15));
+  float* red = reinterpret_cast<float*>(pend + a.stages);
   const bool split = kMode != kModeDown && a.split_k > 1;
 
   const uint32_t w = warp_id();
@@ -1535,7 +1546,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   if (!late_trigger) pdl_launch_dependents();
 
   if (w == 0) {
-    produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty, pq);
+    produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty, pq, pend);
   } else if constexpr (kTC) {
     if (w == 1) {
       if (lane_id() == 0)
@@ -1697,7 +1708,7 @@ int stream_max_clusters(int mode, int split, int smem) {
 
 int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k, int a2_tma) {
   return 1024 + stages * stream_stage_bytes(n_pad, kbs) + a2_stage_bytes(n_pad, a2_tma) + (2 * stages + 4) * 8 +
-         static_cast<int>(sizeof(PieceQueue)) + 128 + split_red_bytes(n_pad, split_k);
+         static_cast<int>(sizeof(PieceQueue)) + 128 + 16 * stages + split_red_bytes(n_pad, split_k);
 }
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv,

@@ -1,2 +1,1 @@
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo rc=$?
-tail -3 gpurun_out/bench.err
+timeout 1500 python -m pytest tests/test_traffic_ncu.py -q -rf 2>&1 | tail -15
