@@ -378,9 +378,13 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
 // Stage-1 split-K (cluster of `split` CTAs per tile, DSMEM reduction): only
 // for the tcgen05 family, the static plan, N <= 64 (reduction buffer) and a
 // K-block count divisible by the split.  Returns 1 when not applicable.
-int effective_split(const dfk_config& cfg, const dfk_weights_s* w, int64_t nb) {
+int effective_split(const dfk_config& cfg, const dfk_weights_s* w, int64_t nb,
+                    int dyn_block_sms = 0) {
   const int sk = cfg.s1_split_k;
-  if (sk <= 1 || cfg.s1_family == DFK_FAMILY_GEMV || cfg.dynamic_sched) return 1;
+  if (sk <= 1 || cfg.s1_family == DFK_FAMILY_GEMV) return 1;
+  // Dynamic block kernel: every stage-1 tile's K parts are the first pieces
+  // of one cluster, so all t1 x sk of them must fit in one wave.
+  if (cfg.dynamic_sched && (dyn_block_sms <= 0 || w->s1_tiles * sk > dyn_block_sms)) return 1;
   if (sk > 8 || w->s1_kblocks % sk != 0) return 1;
   if (split_red_bytes(static_cast<int>(round_up(nb, 16)), sk) > 64 * 1024) return 1;
   return sk;
@@ -614,7 +618,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
   for (int64_t b0 = 0; b0 < B; b0 += L.chunk) {
     const int64_t nb = std::min(L.chunk, B - b0);
     StreamArgs a = {};
-    a.split_k = effective_split(cfg, w, nb);
+    a.split_k = effective_split(cfg, w, nb, ctx->sm_count);
     a.a2_tma = want_a2_tma(cfg, L.tc, a.split_k, a2 + b0 * a2_ld, a2_ld);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap xm, am;
@@ -674,8 +678,15 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     if (tp && ctx->tp_colocated) grid = std::max(1, std::min(grid, ctx->sm_count / tp->tp_size));
     grid = std::min(grid / a.split_k, cluster_cap(kModeBlock, a)) * a.split_k;
     grid = std::max(grid, a.split_k);
+    if (cfg.dynamic_sched && a.split_k > 1 && w->s1_tiles * a.split_k > grid) {
+      // (the 7/8 grid rounded to clusters can fall below t1 x sk)
+      grid = std::min(ctx->sm_count / a.split_k, cluster_cap(kModeBlock, a)) * a.split_k;
+      if (w->s1_tiles * a.split_k > grid)
+        return fail(DFK_ERR_INVALID, "dynamic split-K: stage-1 parts exceed one wave");
+    }
     block_plan(grid, w, &a);
-    if (a.split_k == 1) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
+    if (a.split_k == 1 || cfg.dynamic_sched) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
+    if (a.dynamic && a.split_k > 1) a.s1_chunk = w->s1_kblocks;  // K split by the cluster
     if (a.dynamic && (knobs().bal >= 2 || (knobs().bal == 1 && w->s1_tiles < grid))) {
       // balanced stream-K pieces: partial stage-1 tiles need the workspace
       a.bal = 1;

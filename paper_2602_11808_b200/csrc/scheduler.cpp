@@ -149,6 +149,29 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, const ShapeTiles* w
         add(c);
       }
   }
+  // ... or split each tile's K over a cluster (DSMEM reduction) on the
+  // dynamic block kernel (every K part in the first wave) ...
+  for (int sk : {2, 4}) {
+    if (w->s1_kblocks % sk || w->s1_tiles * sk > ctx->sm_count || B > 64) continue;
+    dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 1, 1);
+    c.dynamic_sched = 1;
+    c.s1_split_k = sk;
+    std::snprintf(c.label, sizeof(c.label), "%s", "");
+    std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+    add(c);
+  }
+  // ... and (full shards, N >= 32) half-tile stage-1 stream-K pieces, which
+  // even out the second stage-1 wave (-0.8 us at B = 64, Llama-8B) ...
+  if (w->s1_tiles >= ctx->sm_count && B > 16) {
+    for (int kbs : {0, 3}) {
+      dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, kbs, 1, 1);
+      c.dynamic_sched = 1;
+      c.s1_chunk_kb = (w->s1_kblocks + 1) / 2;
+      std::snprintf(c.label, sizeof(c.label), "%s", "");
+      std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+      add(c);
+    }
+  }
   // ... and split each tile's K over a cluster (DSMEM reduction), static plan.
   if (w->s1_tiles < ctx->sm_count && B <= 64) {
     for (int sk : {2, 4}) {

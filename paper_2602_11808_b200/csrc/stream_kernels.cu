@@ -268,6 +268,18 @@ __device__ __forceinline__ bool bal_piece(const StreamArgs& a, int mode, int64_t
   return false;
 }
 
+// Down piece idx of the dynamic queue (chunk-major, see decode_dyn).
+__device__ __forceinline__ bool decode_dyn_down(const StreamArgs& a, int64_t idx,
+                                                Piece& out) {
+  if (idx < 0 || idx >= static_cast<int64_t>(a.t2) * dyn_chunks(a)) return false;
+  const int kc = static_cast<int>(idx / a.t2);
+  out.down = 1;
+  out.tile = static_cast<int>(idx % a.t2);
+  out.kb0 = kc * a.chunk_kb;
+  out.kb1 = min(a.kb2, out.kb0 + a.chunk_kb);
+  return true;
+}
+
 // The consumers' view of the piece sequence (static plan or queue).
 struct PieceReader {
   int i = 0;
@@ -854,6 +866,29 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
     } else {
       if (a.bal) {
         valid = bal_piece(a, p.mode, blockIdx.x, gridDim.x, qi, pc);
+      } else if (p.split > 1) {
+        // Dynamic + cluster split-K (small shards): CTA c < t1 x split
+        // starts with K part c % split of stage-1 tile c / split (its
+        // cluster reduces the parts through DSMEM); every other piece is a
+        // down piece -- the first static for the remaining CTAs, then the
+        // queue.
+        const int n1s = a.t1 * p.split;
+        if (qi == 0 && static_cast<int>(blockIdx.x) < n1s) {
+          pc.down = 0;
+          pc.tile = p.q;
+          pc.kb0 = p.krank * a.kb1 / p.split;
+          pc.kb1 = (p.krank + 1) * a.kb1 / p.split;
+          valid = true;
+        } else {
+          int64_t didx = static_cast<int64_t>(blockIdx.x) - n1s;
+          if (qi > 0) {
+            if (!waited) flush();  // no global atomics before the previous grid ends
+            int got = 0;
+            if (leader) got = atomicAdd(a.sched, 1);
+            didx = static_cast<int64_t>(gridDim.x) - n1s + __shfl_sync(0xffffffffu, got, 0);
+          }
+          valid = decode_dyn_down(a, didx, pc);
+        }
       } else {
         int64_t idx = blockIdx.x;
         if (qi > 0) {
@@ -1717,7 +1752,9 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
                           cudaStream_t stream) {
   if (a.kbs < 1 || a.kbs > kMaxKbs || a.stages < 2 || a.stages > 32)
     return cudaErrorInvalidValue;
-  if (a.split_k > 1 && (!tc || a.dynamic || a.split_k > 8 || grid % a.split_k != 0))
+  if (a.split_k > 1 && (!tc || a.split_k > 8 || grid % a.split_k != 0 ||
+                        (a.dynamic && (mode != kModeBlock || a.bal ||
+                                       a.t1 * a.split_k > grid))))
     return cudaErrorInvalidValue;
   if (a.nacc > 4 || (a.nacc > 1 && (a.split_k > 1 || 2 * a.nacc * a.n_pad > 512)))
     return cudaErrorInvalidValue;

@@ -53,6 +53,9 @@ def configs(rt, B):
         "dyn_fused_s1k2_c7": rt.Config.make(dynamic_sched=1, s1_chunk_kb=2, s1_ctas=7),
         "dyn_block_wholetiles": rt.Config.make(block_kernel=1, dynamic_sched=1,
                                                s1_chunk_kb=1 << 20),
+        "dyn_block_sk2": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_split_k=2),
+        "dyn_block_sk4_c20": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_split_k=4,
+                                            chunk_kb=3),
         "fused_sk2": rt.Config.make(s1_split_k=2),
         "fused_sk4_c8": rt.Config.make(s1_split_k=4, s1_ctas=8, kbs=1),
         "block_sk2": rt.Config.make(block_kernel=1, s1_split_k=2),
