@@ -663,6 +663,18 @@ def main():
                 v.append((time.perf_counter() - t0) * 1e6)
             f64_host[str(B)] = round(statistics.median(v), 1)
 
+    # ---- the reference operator API through the C++ drop-in (fp64 Matrix in
+    # and out, tools/shim_timing): warm calls, weights cached by Matrix
+    # id + version after the first call ----
+    shim = None
+    exe = os.path.join(ROOT, "tools", "shim_timing")
+    if P == 1 and os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=300).stdout
+            shim = [json.loads(ln) for ln in out.splitlines() if ln.startswith("{")] or None
+        except Exception:  # noqa: BLE001
+            shim = None
+
     # ---- config 3: multi-layer decode loop (bench.cpp:98-115), CUDA graph ----
     decode = None
     if P == 1 and not args.no_decode:
@@ -732,6 +744,7 @@ def main():
                     "d2h_bytes_per_step": sum(B * DM * 4 for B in sweep)},
             "isolated_us_per_call": iso or None,
             "e2e_f64_host_us_per_call": f64_host or None,
+            "reference_api_us_per_call": shim,
             "parity_errors": parity,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -100,6 +100,7 @@ def build_probe(verbose: bool = False) -> None:
 SHIM_LIB = os.path.join(LIBDIR, "libdeepfusion_b200.so")
 CPP_TEST = os.path.join(ROOT, "tests", "cpp", "test_deepfusion_gpu")
 CPP_TUNER_TEST = os.path.join(ROOT, "tests", "cpp", "test_tuner_gpu")
+SHIM_TIMING = os.path.join(ROOT, "tools", "shim_timing")
 
 
 def build_cpp(verbose: bool = False) -> None:
@@ -110,11 +111,14 @@ def build_cpp(verbose: bool = False) -> None:
           f"-I{os.path.join(ROOT, 'include')}", f"-I{cpp}", f"-I{JSON_DIR}",
           os.path.join(cpp, "deepfusion_gpu.cpp"), "-o", SHIM_LIB,
           f"-L{LIBDIR}", "-ldfk", "-Wl,-rpath,$ORIGIN"], verbose)
-    for src, exe in (("test_deepfusion_gpu.cpp", CPP_TEST), ("test_tuner_gpu.cpp", CPP_TUNER_TEST)):
+    for src, exe in ((os.path.join("tests", "cpp", "test_deepfusion_gpu.cpp"), CPP_TEST),
+                     (os.path.join("tests", "cpp", "test_tuner_gpu.cpp"), CPP_TUNER_TEST),
+                     (os.path.join("tools", "shim_timing.cpp"), SHIM_TIMING)):
         _run(["g++", "-O2", "-std=c++20", "-Wall", f"-I{cpp}",
-              os.path.join(ROOT, "tests", "cpp", src), "-o", exe,
+              os.path.join(ROOT, src), "-o", exe,
               f"-L{LIBDIR}", "-ldeepfusion_b200", "-ldfk",
-              f"-Wl,-rpath,$ORIGIN/../../paper_2602_11808_b200/lib"], verbose)
+              f"-Wl,-rpath,$ORIGIN/../../paper_2602_11808_b200/lib",
+              f"-Wl,-rpath,$ORIGIN/../paper_2602_11808_b200/lib"], verbose)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,62 @@
+// Per-call cost of the reference operator API through the C++ drop-in
+// (paper_2602_11808_b200/cpp/deepfusion.hpp) at the Llama-3.1-8B shape:
+// fp64 Matrix in, fp64 Matrix out, exactly as a reference caller makes the
+// call (fused.hpp:61-67, swiglu.hpp:90).  The first call registers and
+// prepacks the weights (cached by Matrix id + version); warm calls pay the
+// fp64 -> bf16 conversion of X, the H2D copy, the kernels, the D2H copy and
+// the fp32 -> fp64 widening of the result only.
+//
+//   tools/shim_timing [d_model d_ff]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+
+#include "deepfusion.hpp"
+
+using namespace deepfusion;
+using clk = std::chrono::steady_clock;
+
+static double us_since(clk::time_point t0) {
+  return std::chrono::duration<double, std::micro>(clk::now() - t0).count();
+}
+
+int main(int argc, char** argv) {
+  const Index dm = argc > 2 ? std::atoll(argv[1]) : 4096;
+  const Index df = argc > 2 ? std::atoll(argv[2]) : 14336;
+  std::mt19937_64 rng(20260809);
+  const MlpWeights w = make_random_weights(MlpShape{1, dm, df}, rng, 1.0 / std::sqrt(double(dm)));
+  const TileConfig tile{1, 64, 64};
+  for (Index B : {1, 16, 64}) {
+    Matrix x(B, dm);
+    fill_uniform(x, rng, -1.0, 1.0);
+    Matrix a2(B, df);
+    const int reps = 20;
+    auto t0 = clk::now();
+    run_fused_stage1(x, w.w_up, w.w_gate, tile, a2);
+    const double first_s1 = us_since(t0);
+    t0 = clk::now();
+    for (int i = 0; i < reps; ++i) run_fused_stage1(x, w.w_up, w.w_gate, tile, a2);
+    const double s1 = us_since(t0) / reps;
+    t0 = clk::now();
+    Matrix y = down_projection(a2, w.w_down);
+    const double first_dn = us_since(t0);
+    t0 = clk::now();
+    for (int i = 0; i < reps; ++i) y = down_projection(a2, w.w_down);
+    const double dn = us_since(t0) / reps;
+    t0 = clk::now();
+    y = run_fused(x, w, tile);
+    const double first_f = us_since(t0);
+    t0 = clk::now();
+    for (int i = 0; i < reps; ++i) y = run_fused(x, w, tile);
+    const double f = us_since(t0) / reps;
+    std::printf("{\"d_model\": %lld, \"d_ff\": %lld, \"B\": %lld, "
+                "\"run_fused_stage1_us\": %.1f, \"down_projection_us\": %.1f, "
+                "\"run_fused_us\": %.1f, \"first_call_ms\": {\"run_fused_stage1\": %.1f, "
+                "\"down_projection\": %.1f, \"run_fused\": %.1f}}\n",
+                (long long)dm, (long long)df, (long long)B, s1, dn, f, first_s1 / 1e3,
+                first_dn / 1e3, first_f / 1e3);
+  }
+  release_gpu_cache();
+  return 0;
+}
