@@ -342,6 +342,16 @@ DFK_API int dfk_memcpy_h2d(dfk_context ctx, void* dst, const void* src,
 DFK_API int dfk_memcpy_d2h(dfk_context ctx, void* dst, const void* src,
                            size_t bytes);
 DFK_API int dfk_memset(dfk_context ctx, void* p, int value, size_t bytes);
+/* Host-side element conversions of the reference-facing calls (the
+ * reference's Matrix operands are fp64, tensor.hpp:73-128): round-to-nearest-
+ * even to bf16 bits (NaN kept quiet, as the device rounds), or widen fp32 /
+ * bf16 to the destination dtype.  Vectorised, on the calling thread. */
+DFK_API int dfk_host_to_bf16(const void* src, int32_t src_dtype, size_t n,
+                             uint16_t* dst);
+DFK_API int dfk_host_from_f32(const float* src, size_t n, void* dst,
+                              int32_t dst_dtype);
+DFK_API int dfk_host_from_bf16(const uint16_t* src, size_t n, void* dst,
+                               int32_t dst_dtype);
 /* Fills a device bf16 buffer with uniform values in [lo, hi) (synthetic
  * bench inputs; counter-based hash, seed-deterministic). */
 DFK_API int dfk_fill_uniform_bf16(dfk_context ctx, void* p, int64_t n,

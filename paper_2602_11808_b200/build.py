@@ -22,7 +22,7 @@ JSON_DIR = ("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/"
             "cudnn_frontend/thirdparty/nlohmann")
 
 SOURCES = ["stream_kernels.cu", "aux_kernels.cu", "api.cu", "scheduler.cpp",
-           "tuning_cache.cpp", "tp.cpp", "decode.cpp"]
+           "tuning_cache.cpp", "tp.cpp", "decode.cpp", "host_convert.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
           "-Xcompiler", "-fvisibility=hidden", f"-I{os.path.join(ROOT, 'include')}",

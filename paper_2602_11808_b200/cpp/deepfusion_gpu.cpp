@@ -119,28 +119,14 @@ dfk_weights weights_for_locked(const Matrix* w_gate, const Matrix* w_up,
   return h;
 }
 
+// Matrix <-> device element conversions on the library's host pool
+// (dfk_host_to_bf16 / dfk_host_from_bf16: RNE, as the device rounds).
 void to_bf16(const double* src, Index n, std::uint16_t* out) {
-  for (Index i = 0; i < n; ++i) {
-    float f = static_cast<float>(src[i]);
-    std::uint32_t u;
-    std::memcpy(&u, &f, 4);
-    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) {
-      out[i] = static_cast<std::uint16_t>((u >> 16) | 0x40u);
-    } else {
-      u += 0x7FFFu + ((u >> 16) & 1u);
-      out[i] = static_cast<std::uint16_t>(u >> 16);
-    }
-  }
+  check(dfk_host_to_bf16(src, DFK_F64, static_cast<size_t>(n), out));
 }
 
 void from_bf16(const std::uint16_t* v, Matrix& m) {
-  double* d = m.data();
-  for (Index i = 0; i < m.size(); ++i) {
-    const std::uint32_t u = static_cast<std::uint32_t>(v[i]) << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    d[i] = f;
-  }
+  check(dfk_host_from_bf16(v, static_cast<size_t>(m.size()), m.data(), DFK_F64));
 }
 
 const dfk_config* cfg_ptr(VariantTag v, dfk_config* storage) {
@@ -401,8 +387,7 @@ Matrix down_projection(const Matrix& a2, const Matrix& w_down, Accounting) {
   check(dfk_memcpy_d2h(c, out.data(), yd, out.size() * 4));
   check(dfk_context_sync(c));
   Matrix y(B, dm);
-  double* yv = y.data();
-  for (Index i = 0; i < y.size(); ++i) yv[i] = out[static_cast<size_t>(i)];
+  check(dfk_host_from_f32(out.data(), out.size(), y.data(), DFK_F64));
   return y;
 }
 
@@ -600,8 +585,8 @@ TpResult run_tp_mlp(const Matrix& x, const MlpWeights& w, const ShardPlan& plan,
       result.stage1_shards.push_back(std::move(shard));
     }
     result.output = Matrix(B, dm);
-    double* ov = result.output.data();
-    for (Index i = 0; i < result.output.size(); ++i) ov[i] = out[static_cast<size_t>(i)];
+    check(dfk_host_from_f32(out.data(), static_cast<size_t>(result.output.size()),
+                            result.output.data(), DFK_F64));
     for (Index p = 0; p < plan.num_devices; ++p) {
       dfk_context c = ctxs[static_cast<size_t>(p)];
       dfk_free(c, xs[static_cast<size_t>(p)]);

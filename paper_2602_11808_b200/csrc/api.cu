@@ -895,14 +895,6 @@ int check_handles(dfk_context_s* ctx, dfk_weights_s* w, bool need_s1 = true,
   return use_device(ctx);
 }
 
-uint16_t f32_to_bf16_bits(float f) {
-  uint32_t u;
-  std::memcpy(&u, &f, 4);
-  if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu))
-    return static_cast<uint16_t>((u >> 16) | 0x40u);
-  u += 0x7FFFu + ((u >> 16) & 1u);
-  return static_cast<uint16_t>(u >> 16);
-}
 
 
 size_t dtype_size(int dt) { return dt == DFK_F64 ? 8 : dt == DFK_F32 ? 4 : 2; }
@@ -1337,18 +1329,11 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
     ctx->hy_pinned_bytes = yb;
   }
   auto* hx = static_cast<uint16_t*>(ctx->hx_pinned);
-  if (x_dtype == DFK_BF16) {
-    std::memcpy(hx, x, xb);
-  } else if (x_dtype == DFK_F32) {
-    const float* xf = static_cast<const float*>(x);
-    for (size_t i = 0; i < xn; ++i) hx[i] = f32_to_bf16_bits(xf[i]);
-  } else if (x_dtype == DFK_F64) {
-    const double* xd = static_cast<const double*>(x);
-    for (size_t i = 0; i < xn; ++i)
-      hx[i] = f32_to_bf16_bits(static_cast<float>(xd[i]));
-  } else {
+  if (x_dtype != DFK_BF16 && x_dtype != DFK_F32 && x_dtype != DFK_F64)
     return fail(DFK_ERR_INVALID, "unknown x dtype");
-  }
+  if (y_dtype != DFK_BF16 && y_dtype != DFK_F32 && y_dtype != DFK_F64)
+    return fail(DFK_ERR_INVALID, "unknown y dtype");
+  host_to_bf16(x, x_dtype, xn, hx);  // RNE, on the host-conversion pool
   DFK_TRY(ensure_buf(ctx, ctx->hx_dev, xb, false, ctx->stream));
   DFK_TRY(ensure_buf(ctx, ctx->hy_dev, yb, false, ctx->stream));
   DFK_CUDA(cudaMemcpyAsync(ctx->hx_dev.p, hx, xb, cudaMemcpyHostToDevice,
@@ -1363,18 +1348,7 @@ int dfk_forward_host(dfk_context ctx, dfk_weights w, const void* x,
   DFK_CUDA(cudaMemcpyAsync(ctx->hy_pinned, ctx->hy_dev.p, yb,
                            cudaMemcpyDeviceToHost, ctx->stream));
   DFK_CUDA(cudaStreamSynchronize(ctx->stream));
-  const float* hy = static_cast<const float*>(ctx->hy_pinned);
-  if (y_dtype == DFK_F32) {
-    std::memcpy(y, hy, yb);
-  } else if (y_dtype == DFK_F64) {
-    double* yd = static_cast<double*>(y);
-    for (size_t i = 0; i < xn; ++i) yd[i] = hy[i];
-  } else if (y_dtype == DFK_BF16) {
-    uint16_t* yh = static_cast<uint16_t*>(y);
-    for (size_t i = 0; i < xn; ++i) yh[i] = f32_to_bf16_bits(hy[i]);
-  } else {
-    return fail(DFK_ERR_INVALID, "unknown y dtype");
-  }
+  host_from_f32(static_cast<const float*>(ctx->hy_pinned), xn, y, y_dtype);
   return DFK_OK;
 }
 

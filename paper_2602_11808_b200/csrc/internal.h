@@ -247,6 +247,10 @@ int block_fused_tp(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t 
                    void* y, bool y_bf16, const dfk_config& cfg, const StreamArgs* tp);
 int ensure_buf(dfk_context_s* ctx, DeviceBuf& b, size_t bytes, bool zero, cudaStream_t s);
 std::string config_label(const dfk_config& c);
+// Host-side conversions on the worker pool (host_convert.cpp).
+void host_to_bf16(const void* src, int dtype, size_t n, uint16_t* dst);
+void host_from_f32(const float* src, size_t n, void* dst, int dtype);
+void host_from_bf16(const uint16_t* src, size_t n, void* dst, int dtype);
 // Tuning cache (tuning_cache.cpp): lookup (false + *err set on a bad file)
 // and insert-or-replace ("" on success, else the error).
 bool cache_find(const std::string& path, int64_t B, int64_t dm, int64_t df,

@@ -171,6 +171,9 @@ _sigs = {
     "dfk_memcpy_h2d": ([_vp, _vp, _vp, C.c_size_t], C.c_int),
     "dfk_memcpy_d2h": ([_vp, _vp, _vp, C.c_size_t], C.c_int),
     "dfk_memset": ([_vp, _vp, C.c_int, C.c_size_t], C.c_int),
+    "dfk_host_to_bf16": ([_vp, _i32, C.c_size_t, _vp], C.c_int),
+    "dfk_host_from_f32": ([_vp, C.c_size_t, _vp, _i32], C.c_int),
+    "dfk_host_from_bf16": ([_vp, C.c_size_t, _vp, _i32], C.c_int),
     "dfk_fill_uniform_bf16": ([_vp, _vp, _i64, C.c_uint64, C.c_float, C.c_float],
                               C.c_int),
     "dfk_event_create": ([C.POINTER(_vp)], C.c_int),

@@ -4,13 +4,15 @@
 // call (fused.hpp:61-67, swiglu.hpp:90).  The first call registers and
 // prepacks the weights (cached by Matrix id + version); warm calls pay the
 // fp64 -> bf16 conversion of X, the H2D copy, the kernels, the D2H copy and
-// the fp32 -> fp64 widening of the result only.
+// the fp32 -> fp64 widening of the result only.  Medians of 20 calls.
 //
 //   tools/shim_timing [d_model d_ff]
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
+#include <vector>
 
 #include "deepfusion.hpp"
 
@@ -19,6 +21,19 @@ using clk = std::chrono::steady_clock;
 
 static double us_since(clk::time_point t0) {
   return std::chrono::duration<double, std::micro>(clk::now() - t0).count();
+}
+
+// Median of `reps` timed calls (robust to a descheduled host thread).
+template <class F>
+static double median_us(int reps, F&& f) {
+  std::vector<double> v;
+  for (int i = 0; i < reps; ++i) {
+    const auto t0 = clk::now();
+    f();
+    v.push_back(us_since(t0));
+  }
+  std::sort(v.begin(), v.end());
+  return v[v.size() / 2];
 }
 
 int main(int argc, char** argv) {
@@ -35,21 +50,15 @@ int main(int argc, char** argv) {
     auto t0 = clk::now();
     run_fused_stage1(x, w.w_up, w.w_gate, tile, a2);
     const double first_s1 = us_since(t0);
-    t0 = clk::now();
-    for (int i = 0; i < reps; ++i) run_fused_stage1(x, w.w_up, w.w_gate, tile, a2);
-    const double s1 = us_since(t0) / reps;
+    const double s1 = median_us(reps, [&] { run_fused_stage1(x, w.w_up, w.w_gate, tile, a2); });
     t0 = clk::now();
     Matrix y = down_projection(a2, w.w_down);
     const double first_dn = us_since(t0);
-    t0 = clk::now();
-    for (int i = 0; i < reps; ++i) y = down_projection(a2, w.w_down);
-    const double dn = us_since(t0) / reps;
+    const double dn = median_us(reps, [&] { y = down_projection(a2, w.w_down); });
     t0 = clk::now();
     y = run_fused(x, w, tile);
     const double first_f = us_since(t0);
-    t0 = clk::now();
-    for (int i = 0; i < reps; ++i) y = run_fused(x, w, tile);
-    const double f = us_since(t0) / reps;
+    const double f = median_us(reps, [&] { y = run_fused(x, w, tile); });
     std::printf("{\"d_model\": %lld, \"d_ff\": %lld, \"B\": %lld, "
                 "\"run_fused_stage1_us\": %.1f, \"down_projection_us\": %.1f, "
                 "\"run_fused_us\": %.1f, \"first_call_ms\": {\"run_fused_stage1\": %.1f, "
