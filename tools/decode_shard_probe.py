@@ -15,7 +15,9 @@ import numpy as np  # noqa: E402
 from paper_2602_11808_b200 import runtime as rt  # noqa: E402
 
 SHAPES = {"llama8b/8": (4096, 1792), "llama8b/4": (4096, 3584), "qwen32b/8": (5120, 3456),
-          "llama70b/8": (8192, 3584), "llama8b/1": (4096, 14336)}
+          "llama70b/8": (8192, 3584), "llama8b/1": (4096, 14336), "qwen7b/1": (3584, 18944),
+          "qwen32b/4": (5120, 6912), "qwen32b/2": (5120, 13824), "llama70b/4": (8192, 7168),
+          "llama70b/2": (8192, 14336)}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--shapes", default="llama8b/8,llama8b/4,qwen32b/8,llama70b/8,llama8b/1")
