@@ -305,7 +305,7 @@ const Knobs& knobs() {
 }
 
 int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
-                 int grid, StreamArgs* a, bool down_only = false) {
+                 int grid, StreamArgs* a, bool down_only = false, bool block = false) {
   if (!cfg.dynamic_sched) return DFK_OK;
   DFK_TRY(ensure_buf(ctx, ctx->sched, 64, true, ctx->stream));
   a->dynamic = 1;
@@ -341,6 +341,13 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
         1, static_cast<int>(std::lround(static_cast<double>(grid) / w->dn_tiles)));
     chunk = std::max(std::min(4, w->dn_kblocks), (w->dn_kblocks + per_tile - 1) / per_tile);
   }
+  // Block kernel at N <= 32: the stage-1 split below (about two stage-1
+  // pieces per CTA) goes with 16-K-block down chunks.
+  const int s1_per_tile = block && a->n_pad <= 32 && a->split_k <= 1
+                              ? std::min(4, std::max(1, static_cast<int>(std::lround(
+                                                            2.0 * grid / w->s1_tiles))))
+                              : 1;
+  if (s1_per_tile > 1) chunk = std::min(16, w->dn_kblocks);
   if (knobs().dn_chunk > 0) chunk = std::min(knobs().dn_chunk, w->dn_kblocks);
   a->chunk_kb = cfg.chunk_kb > 0 ? cfg.chunk_kb : chunk;
   // Vector partial-sum reductions on shards with fewer stage-1 tiles than
@@ -352,6 +359,16 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   int s1c = w->s1_kblocks;
   if (cfg.s1_chunk_kb > 0) {
     s1c = std::min(cfg.s1_chunk_kb, w->s1_kblocks);
+  } else if (s1_per_tile > 1) {
+    // Block kernel at N <= 32 on shards with up to ~1.3 x grid stage-1
+    // tiles (TP shards): split each tile's K range into round(2 x grid /
+    // tiles) pieces, at most 4, each >= 16 K blocks -- the fit to the sweep
+    // over the TP shards of BASELINE configs 2-5 at TP 2/4/8 and B = 1..32
+    // (tools/chunk_sweep.py, profiles/r2_chunk_sweep.md): mean gap to the
+    // best swept configuration 5.8 % -> 2.3 % at N <= 16, 5.8 % -> 3.7 % at
+    // N = 32.
+    s1c = std::max(std::min(16, w->s1_kblocks),
+                   (w->s1_kblocks + s1_per_tile - 1) / s1_per_tile);
   } else if (w->s1_tiles < grid) {
     // About 0.87 stage-1 pieces per CTA (rounded to whole pieces per tile),
     // each >= 256 KiB (16 K blocks): the best of chunk-size sweeps over the
@@ -685,7 +702,8 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
         return fail(DFK_ERR_INVALID, "dynamic split-K: stage-1 parts exceed one wave");
     }
     block_plan(grid, w, &a);
-    if (a.split_k == 1 || cfg.dynamic_sched) DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a));
+    if (a.split_k == 1 || cfg.dynamic_sched)
+      DFK_TRY(fill_dynamic(ctx, w, cfg, grid, &a, false, true));
     if (a.dynamic && a.split_k > 1) a.s1_chunk = w->s1_kblocks;  // K split by the cluster
     if (a.dynamic && (knobs().bal >= 2 || (knobs().bal == 1 && w->s1_tiles < grid))) {
       // balanced stream-K pieces: partial stage-1 tiles need the workspace
@@ -907,14 +925,16 @@ size_t dtype_size(int dt) { return dt == DFK_F64 ? 8 : dt == DFK_F32 ? 4 : 2; }
 void default_config(dfk_context_s* ctx, dfk_weights_s* w, int64_t B,
                     dfk_config* out) {
   (void)ctx;
-  (void)w;
-  (void)B;
   // The single persistent block kernel with dynamic scheduling: the fastest
-  // configuration in the measured sweeps at every batch (profiles/).
+  // configuration in the measured sweeps at every batch (profiles/).  At
+  // B = 1 on the smallest shards (<= 40 stage-1 tiles, e.g. Llama-8B or
+  // Qwen-7B at TP 8) the warp-GEMV consumers beat tcgen05 by 7-10 %
+  // (profiles/r2_chunk_sweep.md); tcgen05 everywhere else.
+  const bool gemv = B == 1 && w->s1_pack && w->dn_pack && w->s1_tiles <= 40;
   std::memset(out, 0, sizeof(*out));
   out->variant = DFK_VARIANT_FUSED;
-  out->s1_family = DFK_FAMILY_TC;
-  out->down_family = DFK_FAMILY_TC;
+  out->s1_family = gemv ? DFK_FAMILY_GEMV : DFK_FAMILY_TC;
+  out->down_family = gemv ? DFK_FAMILY_GEMV : DFK_FAMILY_TC;
   out->s1_split_k = 1;
   out->block_kernel = 1;
   out->dynamic_sched = 1;
