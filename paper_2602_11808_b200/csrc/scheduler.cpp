@@ -160,17 +160,19 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, const ShapeTiles* w
     std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
     add(c);
   }
-  // ... and (full shards, N >= 32) half-tile stage-1 stream-K pieces, which
-  // even out the second stage-1 wave (-0.8 us at B = 64, Llama-8B) ...
+  // ... and (full shards, N >= 32) half- and third-tile stage-1 stream-K
+  // pieces, which even out the second stage-1 wave (Llama-8B: -0.8 us at
+  // B = 64 with halves, -1.5 us at B = 32 with thirds; profiles/r2_chunk_sweep.md) ...
   if (w->s1_tiles >= ctx->sm_count && B > 16) {
-    for (int kbs : {0, 3}) {
-      dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, kbs, 1, 1);
-      c.dynamic_sched = 1;
-      c.s1_chunk_kb = (w->s1_kblocks + 1) / 2;
-      std::snprintf(c.label, sizeof(c.label), "%s", "");
-      std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
-      add(c);
-    }
+    for (int parts : {2, 3})
+      for (int kbs : {0, 3}) {
+        dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, kbs, 1, 1);
+        c.dynamic_sched = 1;
+        c.s1_chunk_kb = (w->s1_kblocks + parts - 1) / parts;
+        std::snprintf(c.label, sizeof(c.label), "%s", "");
+        std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+        add(c);
+      }
   }
   // ... and split each tile's K over a cluster (DSMEM reduction), static plan.
   if (w->s1_tiles < ctx->sm_count && B <= 64) {
