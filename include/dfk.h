@@ -230,6 +230,12 @@ DFK_API int dfk_decode(dfk_context ctx, const dfk_weights* layers,
 /* --- scheduler (tuner.cpp semantics) ----------------------------------- */
 /* Candidate grid for (weights, B): fills up to `cap` configs, returns the
  * count in *n (default_candidates, tuner.cpp:59-88). */
+/* The configuration a compute call with `cfg` runs at this batch: cfg
+ * itself, or (NULL) the scheduler's stored decision for the shape, else the
+ * library default (the dynamic block kernel; warp-GEMV at B = 1 on shards
+ * with <= 40 stage-1 tiles). */
+DFK_API int dfk_resolve_config(dfk_context ctx, dfk_weights w, int64_t batch,
+                               const dfk_config* cfg, dfk_config* out);
 DFK_API int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
                            dfk_config* out, int32_t cap, int32_t* n);
 /* The same grid for a shape (B, d_model, d_ff shard) without registered

@@ -280,6 +280,15 @@ int dfk_candidates(dfk_context ctx, dfk_weights w, int64_t batch,
   return dfk_candidates_shape(ctx, batch, w->d_model, w->d_ff, out, cap, n);
 }
 
+int dfk_resolve_config(dfk_context ctx, dfk_weights w, int64_t batch, const dfk_config* cfg,
+                       dfk_config* out) {
+  if (!ctx || !w || !out) return fail(DFK_ERR_INVALID, "null argument");
+  if (batch < 1) return fail(DFK_ERR_SHAPE, "batch must be >= 1");
+  DFK_TRY(resolve_config(ctx, w, batch, cfg, out));
+  if (!out->label[0]) std::snprintf(out->label, sizeof(out->label), "%s", config_label(*out).c_str());
+  return DFK_OK;
+}
+
 int dfk_candidates_shape(dfk_context ctx, int64_t batch, int64_t d_model, int64_t d_ff,
                          dfk_config* out, int32_t cap, int32_t* n) {
   if (!ctx || !n) return fail(DFK_ERR_INVALID, "null argument");

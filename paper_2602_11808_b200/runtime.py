@@ -172,6 +172,7 @@ _sigs = {
     "dfk_memcpy_d2h": ([_vp, _vp, _vp, C.c_size_t], C.c_int),
     "dfk_memset": ([_vp, _vp, C.c_int, C.c_size_t], C.c_int),
     "dfk_host_to_bf16": ([_vp, _i32, C.c_size_t, _vp], C.c_int),
+    "dfk_resolve_config": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "dfk_host_from_f32": ([_vp, C.c_size_t, _vp, _i32], C.c_int),
     "dfk_host_from_bf16": ([_vp, C.c_size_t, _vp, _i32], C.c_int),
     "dfk_fill_uniform_bf16": ([_vp, _vp, _i64, C.c_uint64, C.c_float, C.c_float],
@@ -435,6 +436,13 @@ class Context:
         buf = C.create_string_buffer(256)
         _check(lib.dfk_fingerprint(self.h, buf, 256))
         return buf.value.decode()
+
+    def resolve_config(self, w: Weights, batch: int, cfg: Optional[Config] = None) -> Config:
+        """The configuration a call with `cfg` (None: the scheduler's decision
+        or the library default) runs at this batch."""
+        out = Config()
+        _check(lib.dfk_resolve_config(self.h, w.h, batch, self._cfg(cfg), C.byref(out)))
+        return out
 
     def launch_count(self) -> int:
         n = _i64()

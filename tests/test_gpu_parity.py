@@ -750,3 +750,29 @@ def test_llama8b_error_report(rt, ctx, oracle_lib):
     if os.path.isdir(out_dir):
         with open(os.path.join(out_dir, "parity_errors.json"), "w") as f:
             json.dump(report, f, indent=1)
+
+
+@pytest.mark.parametrize("dm,df_total,P", [(4096, 14336, 8), (3584, 18944, 8), (8192, 28672, 8),
+                                           (5120, 27648, 4)])
+def test_tp_shard_defaults_match_oracle(rt, ctx, oracle_lib, dm, df_total, P):
+    """Rank 0's shard of the TP configs (balanced_ranges, tp.cpp:8-29) through
+    the library default at B = 1..32: the warp-GEMV family at B = 1 on shards
+    with <= 40 stage-1 tiles, the stage-1 stream-K split fitted in
+    profiles/r2_chunk_sweep.md elsewhere -- each against the oracle."""
+    b0, b1 = rt.balanced_range(df_total, P, 0)
+    df = b1 - b0
+    x_all, wu, wg, wd = instance(oracle_lib, 7000 + dm + P, 32, dm, df)
+    w = ctx.weights(wg, wu, wd)
+    tiles = (df + 63) // 64
+    for B in (1, 2, 5, 16, 32):
+        cfg = ctx.resolve_config(w, B)
+        gemv = cfg.s1_family == rt.FAMILY_GEMV
+        assert gemv == (B == 1 and tiles <= 40), (B, tiles, cfg.label)
+        assert cfg.block_kernel == 1 and cfg.dynamic_sched == 1
+        x = x_all[:B]
+        _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+        xd = ctx.array((B, dm)).upload(x)
+        y = ctx.array((B, dm), rt.F32)
+        ctx.forward(w, xd, y)
+        ctx.sync()
+        assert rel_err(y.download(), y_ref) <= TOL, (B, cfg.label, rel_err(y.download(), y_ref))
