@@ -491,6 +491,16 @@ def main():
     bmax = max(sweep)
     xs = {B: ctx.array((B, DM)).fill_uniform(7 + B) for B in sweep}
     ys = {B: ctx.array((B, DM), rt.F32) for B in sweep}
+    fused_check = None
+    if tp_mode == "fused-nvlink" and not args.tp_emulate:
+        # first contact with a multi-GPU box: the fused all-reduce must agree
+        # with NCCL (and not time out) on every rank before it is timed
+        yn = ctx.array((bmax, DM), rt.F32)
+        ok, why = tp_host.check_fused(dist, ctx, sets[0], xs[bmax], ys[bmax], yn)
+        fused_check = "ok" if ok else f"fell back to NCCL ({why} on rank {rank})"
+        if not ok:
+            tp_mode = "nccl"
+        del yn
 
     # Scheduler: profile once per batch size (tuner.cpp get_or_tune).
     chosen = {}
@@ -727,6 +737,7 @@ def main():
                               for B in sweep},
             "unfused_us_per_call": {str(B): round(us_unfused[B], 2) for B in sweep},
             "tp_allreduce": tp_mode,
+            "tp_fused_check": fused_check,
             "nccl_allreduce_us_per_call": ({str(B): round(us_nccl[B], 2) for B in sweep}
                                            if us_nccl else None),
             "speedup_vs_unfused": {str(B): round(us_unfused[B] / us[B], 3) for B in sweep},

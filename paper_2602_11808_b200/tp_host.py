@@ -67,6 +67,28 @@ def sum_partials(dist, partial: np.ndarray) -> np.ndarray:
     return total
 
 
+def check_fused(dist, ctx, w, x, y_fused, y_nccl, tol: float = 1e-2) -> Tuple[bool, str]:
+    """One call of the fused all-reduce and one of the NCCL comparator on the
+    same rank shard and input; every rank must see the same Y within the bf16
+    gate and no rank may report a cross-rank timeout.  Returns (all ranks
+    ok, this rank's reason) -- the caller falls back to NCCL when not ok, so a
+    fused path that misbehaves on a new box never produces the timing."""
+    ok, why = 1, "ok"
+    try:
+        ctx.tp_forward_fused(w, x, y_fused)
+        ctx.tp_forward(w, x, y_nccl)
+        ctx.sync()
+        a = y_fused.download().astype(np.float64)
+        b = y_nccl.download().astype(np.float64)
+        den = float(np.abs(b).max()) or 1.0
+        err = float(np.abs(a - b).max()) / den
+        if not np.isfinite(err) or err > tol:
+            ok, why = 0, f"fused vs NCCL max rel err {err:.3e} > {tol}"
+    except Exception as e:  # noqa: BLE001  (timeout word, CUDA error)
+        ok, why = 0, f"{type(e).__name__}: {e}"
+    return bool(min(_gather(dist, ok))), why
+
+
 def setup_fused(dist, ctx, rank: int, world: int, max_batch: int, d_model: int) -> bool:
     """dfk_tp_sym_create on every rank, all-gather the IPC handles,
     dfk_tp_sym_open; True only if every rank succeeded (then all ranks use

@@ -126,3 +126,69 @@ def test_fused_tp_handle_exchange_gloo(fail_rank):
         assert ok == (fail_rank < 0)
         if rank != fail_rank:
             assert opened == [bytes([r]) * 64 for r in range(world)]
+
+
+class _FakeArr:
+    def __init__(self, v):
+        self.v = np.asarray(v, dtype=np.float32)
+
+    def download(self):
+        return self.v
+
+
+class _FakeCtx:
+    """Stands in for a rank's context: the fused and the NCCL all-reduce
+    write given Y values (or the fused one raises, like a cross-rank
+    timeout reported by dfk_context_sync)."""
+
+    def __init__(self, fused, nccl, raise_fused=False):
+        self.fused, self.nccl, self.raise_fused = fused, nccl, raise_fused
+
+    def tp_forward_fused(self, w, x, y):
+        if self.raise_fused:
+            raise RuntimeError("[dfk status 9] peer rank timed out")
+        y.v[...] = self.fused
+
+    def tp_forward(self, w, x, y):
+        y.v[...] = self.nccl
+
+    def sync(self):
+        pass
+
+
+def _check_worker(rank, world, port, case, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_11808_b200 import tp_host
+        good = np.linspace(-1.0, 1.0, 8)
+        bad = good + (0.5 if (case == "mismatch" and rank == 1) else 0.0)
+        ctx = _FakeCtx(bad, good, raise_fused=(case == "timeout" and rank == 0))
+        ok, why = tp_host.check_fused(dist, ctx, None, None, _FakeArr(np.zeros(8)),
+                                      _FakeArr(np.zeros(8)))
+        out_q.put((rank, ok, why))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,want", [("agree", True), ("mismatch", False), ("timeout", False)])
+def test_fused_allreduce_self_check_all_ranks_agree(case, want):
+    """bench.py's first-contact check of the fused all-reduce (tp_host.check_fused):
+    one rank's disagreement with NCCL or a timeout makes EVERY rank fall back."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_check_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [want, want], res
+    if case == "mismatch":
+        assert "max rel err" in res[1][2]
+    if case == "timeout":
+        assert "timed out" in res[0][2]
