@@ -201,6 +201,46 @@ int get_tmap(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
   return DFK_OK;
 }
 
+// 3-D view of a [rows x inner] bf16 activation for one-TMA-per-stage loads
+// (StreamArgs::x3d): dims (64 K, rows, K blocks), the K-block dimension 128 B
+// apart; box (64, box_rows, box_kb).  inner must be a multiple of 64.
+int get_tmap3(dfk_context_s* ctx, const void* ptr, int64_t inner, int64_t rows,
+              int64_t ld, int box_rows, int box_kb, CUtensorMap* out) {
+  auto key = std::make_tuple(reinterpret_cast<uintptr_t>(ptr), inner, rows, ld,
+                             box_rows | (box_kb << 16) | (1 << 30));
+  auto it = ctx->tmaps.find(key);
+  if (it != ctx->tmaps.end()) {
+    *out = it->second;
+    return DFK_OK;
+  }
+  auto enc = tmap_encoder();
+  if (!enc) return fail(DFK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap m;
+  cuuint64_t dims[3] = {64u, static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(inner / 64)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * 2), 128u};
+  cuuint32_t box[3] = {64u, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_kb)};
+  cuuint32_t estr[3] = {1u, 1u, 1u};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DFK_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed (" +
+                                  std::to_string(static_cast<int>(r)) + ")");
+  if (ctx->tmaps.size() > 4096) ctx->tmaps.clear();
+  ctx->tmaps.emplace(key, m);
+  *out = m;
+  return DFK_OK;
+}
+
+// The stage-1 X map of a launch: 3-D (one TMA per ring stage) when a->x3d.
+int get_xmap(dfk_context_s* ctx, const StreamArgs& a, const void* x, int64_t dm, int64_t rows,
+             int64_t ld, CUtensorMap* out) {
+  if (a.x3d) return get_tmap3(ctx, x, dm, rows, ld, a.xrows, a.kbs, out);
+  return get_tmap(ctx, x, dm, rows, ld, a.xrows, out);
+}
+
 int max_stages(dfk_context_s* ctx, int n_pad, int kbs, int split_k = 1, int a2_tma = 0) {
   const int avail = ctx->max_smem_optin - 1024 - 1024 - split_red_bytes(n_pad, split_k) -
                     a2_stage_bytes(n_pad, a2_tma);
@@ -297,6 +337,7 @@ struct Knobs {
   int trace_rel = env_int("DFK_TRACE_REL", 0);      // trace: stage release / MMA issue times
   int lt_tune = env_int("DFK_LT_TUNE", 1);          // autotune the cuBLASLt comparator's algorithm
   int bal = env_int("DFK_BAL", 0);                  // balanced stream-K: 0 off, 1 small shards, 2 always
+  int x3d = env_int("DFK_X3D", 1);                  // one 3-D X / A2 TMA per ring stage
 };
 
 const Knobs& knobs() {
@@ -446,6 +487,8 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
     a->trace_rel = knobs().trace_rel;
   }
   a->tp_error = ctx->err_dev;
+  a->x3d = tc && knobs().x3d && w->d_model % 64 == 0;
+  a->a3d = tc && knobs().x3d && w->d_ff % 64 == 0;
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
   if (tc && sk == 1) {
@@ -494,10 +537,14 @@ int stage1_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x,
     a.split_k = effective_split(cfg, w, nb);
     a.a2_tma = want_a2_tma(cfg, L.tc, a.split_k, a2 + b0 * a2_ld, a2_ld);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
+    a.a3d = 0;  // stage 1 alone never loads A2
     CUtensorMap tm, am;
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
                      w->d_model, nb, x_ld, a.xrows, &tm));
     am = tm;
+    if (a.x3d)
+      DFK_TRY(get_xmap(ctx, a, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld, w->d_model, nb,
+                       x_ld, &tm));
     if (a.a2_tma)
       DFK_TRY(get_tmap(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.xrows, &am));
     a.a2 = a2 + b0 * a2_ld;
@@ -557,6 +604,10 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld,
                      w->d_ff, nb, a_ld, a.xrows, &tm));
     fill_down(ctx, w, y, b0, y_ld, y_bf16, &a);
+    CUtensorMap a3m = tm;
+    if (a.a3d)
+      DFK_TRY(get_tmap3(ctx, static_cast<const __nv_bfloat16*>(ap) + b0 * a_ld, w->d_ff, nb, a_ld,
+                        a.xrows, a.kbs, &a3m));
     const int64_t U = static_cast<int64_t>(w->dn_tiles) * w->dn_kblocks;
     // Default: every SM (the dynamic queue balances; 3/4 of the SMs, the
     // first session's optimum for the static plan, is 11-18 % slower now,
@@ -566,7 +617,7 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a, true));
     cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
                                   static_cast<int>(grid), cfg.pdl != 0,
-                                  ctx->stream);
+                                  ctx->stream, &a3m);
     if (e != cudaSuccess)
       return fail(DFK_ERR_CUDA,
                   std::string("down launch: ") + cudaGetErrorString(e));
@@ -639,9 +690,12 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     a.a2_tma = want_a2_tma(cfg, L.tc, a.split_k, a2 + b0 * a2_ld, a2_ld);
     fill_common(ctx, w, nb, L.tc, cfg.s1_stages, cfg, &a);
     CUtensorMap xm, am;
-    DFK_TRY(get_tmap(ctx, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld,
-                     w->d_model, nb, x_ld, a.xrows, &xm));
+    DFK_TRY(get_xmap(ctx, a, static_cast<const __nv_bfloat16*>(xp) + b0 * x_ld, w->d_model, nb,
+                     x_ld, &xm));
     DFK_TRY(get_tmap(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.xrows, &am));
+    CUtensorMap a3m = am;
+    if (a.a3d)
+      DFK_TRY(get_tmap3(ctx, a2 + b0 * a2_ld, w->d_ff, nb, a2_ld, a.xrows, a.kbs, &a3m));
     a.a2 = a2 + b0 * a2_ld;
     a.a2_ld = a2_ld;
     a.cols_valid = static_cast<int>(w->d_ff);
@@ -720,7 +774,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,
-                                  grid, cfg.pdl != 0, ctx->stream);
+                                  grid, cfg.pdl != 0, ctx->stream, &a3m);
     if (e != cudaSuccess)
       return fail(DFK_ERR_CUDA,
                   std::string("block launch: ") + cudaGetErrorString(e));

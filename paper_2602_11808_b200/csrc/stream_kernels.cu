@@ -784,7 +784,8 @@ __device__ __forceinline__ bool check_ready(const StreamArgs& a, ReadyCache& rc,
 
 __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
                                         const CUtensorMap* xmap,
-                                        const CUtensorMap* amap, uint8_t* smem,
+                                        const CUtensorMap* amap, const CUtensorMap* a3map,
+                                        uint8_t* smem,
                                         int stage_bytes, uint64_t* full,
                                         uint64_t* empty, PieceQueue* pq, int4* pend) {
   const bool leader = lane_id() == 0;
@@ -819,6 +820,10 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       x_ok = true;
     }
     if (!leader) return;
+    if (down ? a.a3d : a.x3d) {
+      tma_load_3d(xs, down ? a3map : xmap, 0, 0, kb, bar);
+      return;
+    }
     for (int b = 0; b < nb; ++b) {
       tma_load_2d(xs + b * xblk, down ? amap : xmap, (kb + b) * kBlockK, 0, bar);
     }
@@ -937,9 +942,11 @@ __device__ __forceinline__ void produce(const StreamArgs& a, const Plan& p,
       }
       uint8_t* st = smem + static_cast<int64_t>(slot) * stage_bytes;
       if (leader) {
+        // (a 3-D X box always brings kbs K blocks' rows, OOB included)
         mbar_arrive_expect_tx(&full[slot],
-                              static_cast<uint32_t>(nb) *
-                                  (kBlockBytes + static_cast<uint32_t>(a.xrows) * 128u));
+                              static_cast<uint32_t>(nb) * kBlockBytes +
+                                  static_cast<uint32_t>((pc.down ? a.a3d : a.x3d) ? a.kbs : nb) *
+                                      static_cast<uint32_t>(a.xrows) * 128u);
         // nb consecutive K blocks of one tile are contiguous in the pack.
         bulk_g2s(st,
                  wbase + (static_cast<int64_t>(pc.tile) * kbt + kb) *
@@ -1151,6 +1158,7 @@ __device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
                                          uint32_t tmem_base, PieceQueue* pq) {
   const uint32_t idesc = umma_idesc_bf16(128, static_cast<uint32_t>(a.n_pad));
   const uint32_t xblk16 = static_cast<uint32_t>(a.n_pad) * 128u / 16u;
+  const uint32_t xblk16_3d = static_cast<uint32_t>(a.xrows) * 128u / 16u;  // packed X (x3d)
   const uint32_t wbytes_all = static_cast<uint32_t>(a.kbs) * kBlockBytes;
   const uint32_t chain_cols = static_cast<uint32_t>(a.n_pad);
   const uint64_t desc0 = umma_desc_sw128(0);
@@ -1177,7 +1185,9 @@ __device__ __forceinline__ void mma_loop(const StreamArgs& a, const Plan& p,
       const uint32_t sbase = smem0 + static_cast<uint32_t>(slot * stage_bytes);
       const uint64_t dw = desc0 + (sbase >> 4);
       const uint64_t dx = desc0 + ((sbase + wbytes_all) >> 4);
-      mma_stage_nb<NACC>(nb, d, dw, dx, idesc, xblk16, chain_cols, kb == pc.kb0);
+      mma_stage_nb<NACC>(nb, d, dw, dx, idesc,
+                         (pc.down ? a.a3d : a.x3d) ? xblk16_3d : xblk16, chain_cols,
+                         kb == pc.kb0);
       tc_commit(&empty[slot]);
       // trace_rel: the stage's MMAs and commit are issued
       if (a.trace && a.trace_rel && it >= a.trace_s0 && it < a.trace_s0 + 12)
@@ -1515,6 +1525,7 @@ template <int kMode, bool kTC, int NB>
 __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
     stream_kernel(const __grid_constant__ CUtensorMap xmap,
                   const __grid_constant__ CUtensorMap amap,
+                  const __grid_constant__ CUtensorMap a3map,
                   const StreamArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -1542,6 +1553,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   if (w == 0 && lane_id() == 0) {
     if (kMode != kModeDown) prefetch_tmap(&xmap);
     if (kMode != kModeStage1) prefetch_tmap(&amap);
+    if (kMode != kModeStage1 && a.a3d) prefetch_tmap(&a3map);
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], kTC ? 1 : kGemvWarps);
@@ -1581,7 +1593,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
   if (!late_trigger) pdl_launch_dependents();
 
   if (w == 0) {
-    produce(a, plan, &xmap, &amap, smem, stage_bytes, full, empty, pq, pend);
+    produce(a, plan, &xmap, &amap, &a3map, smem, stage_bytes, full, empty, pq, pend);
   } else if constexpr (kTC) {
     if (w == 1) {
       if (lane_id() == 0)
@@ -1646,8 +1658,8 @@ cudaError_t allow_max_smem(const void* kern) {
 
 template <int kMode, bool kTC, int NB>
 cudaError_t launch_one(const CUtensorMap& xmap, const CUtensorMap& amap,
-                       const StreamArgs& a, int grid, int smem, bool pdl,
-                       cudaStream_t stream) {
+                       const CUtensorMap& a3map, const StreamArgs& a, int grid, int smem,
+                       bool pdl, cudaStream_t stream) {
   auto kern = stream_kernel<kMode, kTC, NB>;
   cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
@@ -1672,19 +1684,19 @@ cudaError_t launch_one(const CUtensorMap& xmap, const CUtensorMap& amap,
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, kern, xmap, amap, a);
+  return cudaLaunchKernelEx(&cfg, kern, xmap, amap, a3map, a);
 }
 
 template <int kMode>
 cudaError_t launch_mode(bool tc, int nb, const CUtensorMap& xmap,
-                        const CUtensorMap& amap, const StreamArgs& a, int grid,
-                        int smem, bool pdl, cudaStream_t s) {
-  if (tc) return launch_one<kMode, true, 0>(xmap, amap, a, grid, smem, pdl, s);
+                        const CUtensorMap& amap, const CUtensorMap& a3map,
+                        const StreamArgs& a, int grid, int smem, bool pdl, cudaStream_t s) {
+  if (tc) return launch_one<kMode, true, 0>(xmap, amap, a3map, a, grid, smem, pdl, s);
   switch (nb) {
-    case 1: return launch_one<kMode, false, 1>(xmap, amap, a, grid, smem, pdl, s);
-    case 2: return launch_one<kMode, false, 2>(xmap, amap, a, grid, smem, pdl, s);
-    case 4: return launch_one<kMode, false, 4>(xmap, amap, a, grid, smem, pdl, s);
-    case 8: return launch_one<kMode, false, 8>(xmap, amap, a, grid, smem, pdl, s);
+    case 1: return launch_one<kMode, false, 1>(xmap, amap, a3map, a, grid, smem, pdl, s);
+    case 2: return launch_one<kMode, false, 2>(xmap, amap, a3map, a, grid, smem, pdl, s);
+    case 4: return launch_one<kMode, false, 4>(xmap, amap, a3map, a, grid, smem, pdl, s);
+    case 8: return launch_one<kMode, false, 8>(xmap, amap, a3map, a, grid, smem, pdl, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -1749,7 +1761,9 @@ int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k, int a2_tma) {
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
                           const CUtensorMap& xmap, const CUtensorMap& amap,
                           const StreamArgs& a, int grid, bool pdl,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, const CUtensorMap* a3map) {
+  if (a.a3d && !a3map) return cudaErrorInvalidValue;
+  const CUtensorMap& a3 = a3map ? *a3map : amap;
   if (a.kbs < 1 || a.kbs > kMaxKbs || a.stages < 2 || a.stages > 32)
     return cudaErrorInvalidValue;
   if (a.split_k > 1 && (!tc || a.split_k > 8 || grid % a.split_k != 0 ||
@@ -1763,11 +1777,11 @@ cudaError_t launch_stream(int mode, bool tc, int nb_gemv,
                                      mode == kModeDown ? 1 : a.split_k, a.a2_tma);
   switch (mode) {
     case kModeStage1:
-      return launch_mode<kModeStage1>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);
+      return launch_mode<kModeStage1>(tc, nb_gemv, xmap, amap, a3, a, grid, smem, pdl, stream);
     case kModeDown:
-      return launch_mode<kModeDown>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);
+      return launch_mode<kModeDown>(tc, nb_gemv, xmap, amap, a3, a, grid, smem, pdl, stream);
     case kModeBlock:
-      return launch_mode<kModeBlock>(tc, nb_gemv, xmap, amap, a, grid, smem, pdl, stream);
+      return launch_mode<kModeBlock>(tc, nb_gemv, xmap, amap, a3, a, grid, smem, pdl, stream);
     default:
       return cudaErrorInvalidValue;
   }

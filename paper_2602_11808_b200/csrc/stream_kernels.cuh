@@ -30,6 +30,13 @@ struct StreamArgs {
   int B;       // batch rows present
   int n_pad;   // MMA N (tcgen05) / activation box rows (GEMV)
   int xrows;   // rows per activation TMA box (<= n_pad; the smem tile is n_pad rows)
+  // x3d: xmap is 3-D (64 K x xrows x K blocks, the K-block dimension 128 B
+  // apart), so ONE TMA per ring stage brings the X rows of all its K blocks,
+  // packed xrows x 128 B per K block (the MMA's N = 16 operand then reads
+  // rows 8..15 of a B <= 8 block from the next block: they only feed
+  // discarded accumulator columns).  Stage-1 loads only.
+  int x3d;
+  int a3d;     // the same for the down pieces' A2 loads (a3map)
   // Stage-1 A2 leaves through a swizzled smem tile and ONE TMA store per tile
   // (amap, box 64 x xrows) instead of per-element stores (tcgen05 family,
   // whole tiles; host sets it when A2 is TMA-addressable).
@@ -179,7 +186,8 @@ __host__ __device__ inline int split_red_bytes(int n_pad, int split_k) {
 
 cudaError_t launch_stream(int mode, bool tc, int nb_gemv, const CUtensorMap& xmap,
                           const CUtensorMap& amap, const StreamArgs& a, int grid,
-                          bool pdl, cudaStream_t stream);
+                          bool pdl, cudaStream_t stream,
+                          const CUtensorMap* a3map = nullptr);  // 3-D A2 loads (a3d)
 
 int stream_smem_bytes(int n_pad, int stages, int kbs, int split_k = 1, int a2_tma = 0);
 // Bytes of the A2 staging tile (a2_tma): n_pad rows of 128 B.
