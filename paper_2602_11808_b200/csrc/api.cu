@@ -487,8 +487,9 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
     a->trace_rel = knobs().trace_rel;
   }
   a->tp_error = ctx->err_dev;
-  a->x3d = tc && knobs().x3d && w->d_model % 64 == 0;
-  a->a3d = tc && knobs().x3d && w->d_ff % 64 == 0;
+  // (the GEMV family's 8-row boxes already pack 8 x 128 B per K block)
+  a->x3d = knobs().x3d && w->d_model % 64 == 0 && (tc || a->xrows == n_pad);
+  a->a3d = knobs().x3d && w->d_ff % 64 == 0 && (tc || a->xrows == n_pad);
   // Independent accumulator chains (tcgen05): 1, 2 or 4, as TMEM allows.
   a->nacc = 1;
   if (tc && sk == 1) {
