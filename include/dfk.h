@@ -134,7 +134,11 @@ typedef struct dfk_config {
                            over d_model with fp32 partial sums (0 = auto:
                            split only when the shard has fewer stage-1
                            tiles than CTAs)                                */
-  int32_t reserved[1];
+  int32_t s1_tail;      /* dynamic block kernel on shards with more stage-1
+                           tiles than CTAs: the first wave of tiles runs
+                           whole, every later tile is split into s1_tail
+                           K parts (stream-K), spreading the last stage-1
+                           wave over all CTAs (0/1 = off)                 */
   char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
 } dfk_config;
 

@@ -114,6 +114,7 @@ std::string config_label(const dfk_config& c) {
   if (c.block_kernel) {
     if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
     if (c.dynamic_sched && c.s1_chunk_kb) o << "s1k" << c.s1_chunk_kb << "_";
+    if (c.dynamic_sched && c.s1_tail > 1) o << "s1t" << c.s1_tail << "_";
     if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
@@ -338,6 +339,8 @@ struct Knobs {
   int lt_tune = env_int("DFK_LT_TUNE", 1);          // autotune the cuBLASLt comparator's algorithm
   int bal = env_int("DFK_BAL", 0);                  // balanced stream-K: 0 off, 1 small shards, 2 always
   int x3d = env_int("DFK_X3D", 1);                  // one 3-D X / A2 TMA per ring stage
+  int s1_tail = env_int("DFK_S1_TAIL", 0);          // overrides dfk_config.s1_tail (A/B runs)
+  int s1_whole = env_int("DFK_S1_WHOLE", 0);        // whole stage-1 tiles first (0 = grid)
 };
 
 const Knobs& knobs() {
@@ -421,7 +424,14 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
                    (w->s1_kblocks + per_tile - 1) / per_tile);
   }
   a->s1_chunk = s1c;
-  if (s1c < w->s1_kblocks) {
+  a->s1_tail = 0;
+  a->s1_whole = 0;
+  const int tail = knobs().s1_tail > 0 ? knobs().s1_tail : cfg.s1_tail;
+  if (block && s1c >= w->s1_kblocks && tail > 1 && w->s1_tiles > grid && a->split_k <= 1) {
+    a->s1_tail = std::min(tail, w->s1_kblocks);
+    a->s1_whole = knobs().s1_whole > 0 ? std::min(knobs().s1_whole, w->s1_tiles) : grid;
+  }
+  if (s1c < w->s1_kblocks || a->s1_tail > 1) {
     DFK_TRY(ensure_buf(ctx, ctx->s1acc,
                        static_cast<size_t>(w->s1_tiles) * a->n_pad * kBlockRows * 4,
                        true, ctx->stream));

@@ -174,6 +174,22 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, const ShapeTiles* w
         add(c);
       }
   }
+  // ... and the tail split: the first wave of stage-1 tiles whole, the rest
+  // in 2-4 K parts, so the last wave runs on every CTA (B = 32 on Llama-8B
+  // 57.2 -> 54.5 us, Qwen2.5-32B TP2 69.0 -> 63.8 us; the best part count
+  // differs per shape and batch, profiles/r2_tail_split.md) ...
+  if (w->s1_tiles > ctx->sm_count) {
+    for (int parts : {2, 3, 4})
+      for (int kbs : {0, 3}) {
+        if (B <= 16 && (parts > 2 || kbs)) continue;
+        dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, kbs, 1, 1);
+        c.dynamic_sched = 1;
+        c.s1_tail = parts;
+        std::snprintf(c.label, sizeof(c.label), "%s", "");
+        std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+        add(c);
+      }
+  }
   // ... and split each tile's K over a cluster (DSMEM reduction), static plan.
   if (w->s1_tiles < ctx->sm_count && B <= 64) {
     for (int sk : {2, 4}) {
@@ -199,7 +215,7 @@ json cfg_to_json(const dfk_config& c) {
               {"down_stages", c.down_stages}, {"down_ctas", c.down_ctas},
               {"pdl", c.pdl},                 {"dynamic_sched", c.dynamic_sched},
               {"chunk_kb", c.chunk_kb},       {"s1_chunk_kb", c.s1_chunk_kb},
-              {"label", std::string(c.label)}};
+              {"s1_tail", c.s1_tail},         {"label", std::string(c.label)}};
 }
 
 // The chosen_config object of a cache entry; throws on a malformed one.
@@ -214,7 +230,8 @@ dfk_config cfg_from_json(const json& j) {
       {"down_stages", &c.down_stages}, {"down_ctas", &c.down_ctas},
       {"pdl", &c.pdl},                 {"block_kernel", &c.block_kernel},
       {"kbs", &c.kbs},                 {"dynamic_sched", &c.dynamic_sched},
-      {"chunk_kb", &c.chunk_kb},       {"s1_chunk_kb", &c.s1_chunk_kb}};
+      {"chunk_kb", &c.chunk_kb},       {"s1_chunk_kb", &c.s1_chunk_kb},
+      {"s1_tail", &c.s1_tail}};
   for (const auto& [name, dst] : ints) {
     auto it = j.find(name);
     if (it == j.end()) continue;  // fields added later default to 0 (library default)

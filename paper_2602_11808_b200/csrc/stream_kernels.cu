@@ -205,11 +205,29 @@ __device__ __forceinline__ int s1_pieces(const StreamArgs& a) {
 __device__ __forceinline__ bool decode_dyn(const StreamArgs& a, int mode,
                                            int64_t idx, Piece& out) {
   const int s1c = s1_pieces(a);
-  const int64_t n1 = mode != kModeDown ? static_cast<int64_t>(a.t1) * s1c : 0;
+  const bool tail = a.s1_tail > 1;
+  const int64_t n1 =
+      mode == kModeDown ? 0
+      : tail ? a.s1_whole + static_cast<int64_t>(a.t1 - a.s1_whole) * a.s1_tail
+             : static_cast<int64_t>(a.t1) * s1c;
   const int64_t n2 =
       mode != kModeStage1 ? static_cast<int64_t>(a.t2) * dyn_chunks(a) : 0;
   if (idx < n1) {
     out.down = 0;
+    if (tail) {
+      if (idx < a.s1_whole) {
+        out.tile = static_cast<int>(idx);
+        out.kb0 = 0;
+        out.kb1 = a.kb1;
+      } else {
+        const int j = static_cast<int>(idx - a.s1_whole);
+        const int part = j % a.s1_tail;
+        out.tile = a.s1_whole + j / a.s1_tail;
+        out.kb0 = part * a.kb1 / a.s1_tail;
+        out.kb1 = (part + 1) * a.kb1 / a.s1_tail;
+      }
+      return true;
+    }
     out.tile = static_cast<int>(idx / s1c);
     const int kc = static_cast<int>(idx % s1c);
     out.kb0 = s1c > 1 ? kc * a.s1_chunk : 0;

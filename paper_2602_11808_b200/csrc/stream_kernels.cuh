@@ -113,6 +113,12 @@ struct StreamArgs {
   // tile's flag and re-zeroes its workspace and counter.  Lets every SM
   // stream stage-1 weights when a (TP) shard has fewer tiles than SMs.
   int s1_chunk;
+  // Tail split (dynamic path, whole-tile s1_chunk): the first s1_whole
+  // stage-1 tiles are whole pieces (one wave over the grid), every later
+  // tile is split into s1_tail K parts (stream-K through s1acc), so the
+  // last stage-1 wave is spread over all CTAs instead of a fraction of them.
+  int s1_tail;
+  int s1_whole;
   // Balanced stream-K (dynamic machinery, static pieces): CTA c takes the
   // K-block ranges [c*U/G, (c+1)*U/G) of the flattened stage-1 space
   // (U = t1*kb1) and then of the down space (U = t2*kb2), split at tile

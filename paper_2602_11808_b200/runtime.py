@@ -88,13 +88,13 @@ class Config(C.Structure):
                 ("block_kernel", C.c_int32), ("kbs", C.c_int32),
                 ("dynamic_sched", C.c_int32), ("chunk_kb", C.c_int32),
                 ("s1_chunk_kb", C.c_int32),
-                ("reserved", C.c_int32 * 1), ("label", C.c_char * 64)]
+                ("s1_tail", C.c_int32), ("label", C.c_char * 64)]
 
     @classmethod
     def make(cls, variant=VARIANT_FUSED, s1_family=FAMILY_TC, down_family=FAMILY_TC,
              s1_stages=0, down_stages=0, s1_ctas=0, down_ctas=0, pdl=1, mutant=0,
              s1_split_k=1, block_kernel=0, kbs=0, dynamic_sched=0, chunk_kb=0,
-             s1_chunk_kb=0, label=""):
+             s1_chunk_kb=0, s1_tail=0, label=""):
         c = cls()
         c.variant, c.s1_family, c.down_family = variant, s1_family, down_family
         c.s1_stages, c.down_stages, c.s1_ctas, c.down_ctas = (s1_stages, down_stages,
@@ -103,11 +103,12 @@ class Config(C.Structure):
         c.block_kernel, c.kbs = block_kernel, kbs
         c.dynamic_sched, c.chunk_kb = dynamic_sched, chunk_kb
         c.s1_chunk_kb = s1_chunk_kb
+        c.s1_tail = s1_tail
         c.label = label.encode()[:63]
         return c
 
     def as_dict(self) -> dict:
-        return {f: getattr(self, f) for f, _ in self._fields_ if f != "reserved"} | {
+        return {f: getattr(self, f) for f, _ in self._fields_ if f != "label"} | {
             "label": self.label.decode()}
 
     def __repr__(self) -> str:

@@ -60,6 +60,14 @@ def configs(rt, B):
         "fused_sk4_c8": rt.Config.make(s1_split_k=4, s1_ctas=8, kbs=1),
         "block_sk2": rt.Config.make(block_kernel=1, s1_split_k=2),
         "block_sk8": rt.Config.make(block_kernel=1, s1_split_k=8, kbs=2),
+        # tail split (whole first wave, later tiles in K parts): engages where
+        # the shard has more stage-1 tiles than CTAs -- the full Llama-8B
+        # shape at the default grid, medium shapes at 5 / 3 CTAs
+        "dyn_block_tail3": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=3),
+        "dyn_block_tail4_kbs3": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=4,
+                                               kbs=3),
+        "dyn_block_tail2_c5_ch3": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=2,
+                                                 s1_ctas=5, chunk_kb=3),
         "two_kernel": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
         "four_kernel": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
     }
@@ -77,6 +85,10 @@ def configs(rt, B):
                                                     s1_chunk_kb=2,
                                                     s1_family=rt.FAMILY_GEMV,
                                                     down_family=rt.FAMILY_GEMV)
+        out["dyn_block_gemv_tail3_c3"] = rt.Config.make(block_kernel=1, dynamic_sched=1,
+                                                        s1_tail=3, s1_ctas=3,
+                                                        s1_family=rt.FAMILY_GEMV,
+                                                        down_family=rt.FAMILY_GEMV)
     return out
 
 
@@ -472,6 +484,33 @@ def test_stage1_stream_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, fam):
         # the workspace is left all-zero: a second correct call still passes
         ctx.stage1(w, xd, a2, cfg=rt.Config.make(**kw))
         assert rel_err(a2.download(), a2_ref) <= TOL
+
+
+@pytest.mark.parametrize("fam,B", [("tc", 4), ("tc", 40), ("gemv", 4)])
+def test_stage1_tail_split_parity_and_mutant(rt, ctx, oracle_lib, fam, B):
+    """Tail split (dfk_config.s1_tail): the first wave of stage-1 tiles runs
+    whole, every later tile in s1_tail stream-K parts whose full sums get
+    SiLU*up from the CTA adding the last part.  Correct for several part
+    counts (uneven parts included), self-cleaning, and its SiluPerKChunk
+    mutant (verification.cpp:84-124) must FAIL parity."""
+    dm, df = 1024, 1024  # 16 stage-1 tiles of 16 K blocks
+    x, wu, wg, wd = instance(oracle_lib, 91 + B, B, dm, df)
+    a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    xd = ctx.array((B, dm)).upload(x)
+    y = ctx.array((B, dm), rt.F32)
+    f = rt.FAMILY_TC if fam == "tc" else rt.FAMILY_GEMV
+    for parts, ctas in ((2, 5), (3, 5), (5, 7), (4, 3)):
+        kw = dict(block_kernel=1, dynamic_sched=1, s1_tail=parts, s1_ctas=ctas,
+                  s1_family=f, down_family=f)
+        for _ in range(2):  # the second call sees the re-zeroed workspace
+            ctx.forward(w, xd, y, cfg=rt.Config.make(**kw))
+            assert rel_err(y.download(), y_ref) <= TOL, (parts, ctas)
+        ctx.forward(w, xd, y, cfg=rt.Config.make(mutant=1, **kw))
+        assert rel_err(y.download(), y_ref) > 10 * TOL, (parts, ctas)
+    ctx.forward(w, xd, y, cfg=rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=3,
+                                             s1_ctas=5, s1_family=f, down_family=f))
+    assert rel_err(y.download(), y_ref) <= TOL
 
 
 @pytest.mark.parametrize("P,B", [(2, 1), (3, 5), (4, 17), (8, 2)])
