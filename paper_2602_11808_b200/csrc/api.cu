@@ -339,6 +339,7 @@ struct Knobs {
   int lt_tune = env_int("DFK_LT_TUNE", 1);          // autotune the cuBLASLt comparator's algorithm
   int bal = env_int("DFK_BAL", 0);                  // balanced stream-K: 0 off, 1 small shards, 2 always
   int x3d = env_int("DFK_X3D", 1);                  // one 3-D X / A2 TMA per ring stage
+  int y_direct = env_int("DFK_Y_DIRECT", 1);        // block kernel red.adds into fp32 Y itself
   int s1_tail = env_int("DFK_S1_TAIL", 0);          // overrides dfk_config.s1_tail (A/B runs)
   int s1_whole = env_int("DFK_S1_WHOLE", 0);        // whole stage-1 tiles first (0 = grid)
 };
@@ -520,6 +521,17 @@ int ensure_down_workspace(dfk_context_s* ctx, dfk_weights_s* w, int64_t rows) {
                      true, ctx->stream));
   return ensure_buf(ctx, ctx->counters, static_cast<size_t>(w->dn_tiles) * 4, true,
                     ctx->stream);
+}
+
+// True for memory of a device (cudaMalloc / pool), false for host-mapped,
+// managed or unknown pointers.
+bool device_memory(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice;
 }
 
 void fill_down(dfk_context_s* ctx, dfk_weights_s* w, void* y, int64_t b0,
@@ -782,6 +794,12 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
       a.s1acc = static_cast<float*>(ctx->s1acc.p);
       a.s1cnt = static_cast<int*>(ctx->s1cnt.p);
     }
+    // Direct Y (stream_kernels.cuh): fp32 Y in this GPU's memory with whole
+    // 16-byte row groups; not under the fused TP all-reduce (its own tile
+    // owners) nor for Y in mapped host memory (no PCIe reductions).
+    if (a.dynamic && L.tc && !tp && knobs().y_direct && !y_bf16 && a.y_vec4 &&
+        w->d_model % 4 == 0 && device_memory(a.y))
+      a.y_direct = 1;
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");
     cudaError_t e = launch_stream(kModeBlock, L.tc, gemv_nb(nb), xm, am, a,

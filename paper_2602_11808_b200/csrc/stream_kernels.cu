@@ -1345,6 +1345,30 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
   int acc_it = 0;
   int split_iter = 0;
   bool dn_stamped = false;
+  bool y_zeroed = false;  // direct Y: every CTA's slice is zero (seen once)
+  if (a.y_direct) {
+    // The previous launch may still read / write Y until it completes.
+    pdl_wait();
+    // slices start on 128-byte lines (8 float4): a warp's 512-byte store then
+    // covers 16 whole sectors (unaligned slices cost one partial sector per
+    // warp store, +30 KB of L2 writes at B = 64)
+    const int64_t nv = static_cast<int64_t>(a.B) * (a.out_cols / 4);
+    const int64_t v0 = (nv * blockIdx.x / gridDim.x) & ~int64_t{7};
+    const int64_t v1 = blockIdx.x + 1 == gridDim.x
+                           ? nv
+                           : (nv * (blockIdx.x + 1) / gridDim.x) & ~int64_t{7};
+    const int q4 = a.out_cols / 4;
+    for (int64_t v = v0 + tid; v < v1; v += 128) {
+      const int64_t n = v / q4, j = (v % q4) * 4;
+      __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.y) + n * a.y_ld + j),
+             make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+    named_bar(1, 128);  // then one cumulative release: see down_finish_tile
+    if (tid == 0) {
+      fence_acq_rel_gpu();
+      atomicAdd(a.sched + 2, 1);
+    }
+  }
   PieceReader pi;
   Piece pc;
   while (pi.next(a, p, pq, false, pc)) {
@@ -1491,14 +1515,23 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       if (stamp && tid == 0) trace_stamp(a, 40);
       const int j = pc.tile * kDownCols + row;
       const bool jok = j < a.out_cols;
-      float* yp = down_acc(a, pc.tile) + j;
-      const int64_t ld = a.yacc_ld;
+      if (a.y_direct && !y_zeroed) {
+        // (long true by now: every CTA zeroes right after the PDL wait)
+        if (tid == 0)
+          while (static_cast<int>(ld_acquire(reinterpret_cast<const unsigned*>(a.sched + 2))) <
+                 static_cast<int>(gridDim.x)) {
+          }
+        named_bar(1, 128);
+        y_zeroed = true;
+      }
+      float* yp = a.y_direct ? reinterpret_cast<float*>(a.y) + j : down_acc(a, pc.tile) + j;
+      const int64_t ld = a.y_direct ? a.y_ld : a.yacc_ld;
       // v4 reductions over whole 4-column groups (the condition is
       // warp-uniform: the shuffles involve all 32 lanes); under the fused TP
       // all-reduce always, at system scope (the owner's workspace may be on
       // another GPU: 4x fewer NVLink reductions)
       const bool tp = a.tp_size > 1;
-      const bool vec = (a.red_v4 || tp) &&
+      const bool vec = (a.red_v4 || tp || a.y_direct) &&
                        __all_sync(0xffffffffu, j - (lane & 3) + 3 < a.out_cols);
       for (int c0 = 0; c0 < a.n_pad; c0 += 16) {
         float v[16];
@@ -1523,7 +1556,8 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
-      down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, 128, smem_flag, stamp);
+      if (!a.y_direct)
+        down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, 128, smem_flag, stamp);
     }
     if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
     ++acc_it;
@@ -1641,6 +1675,7 @@ __global__ void __launch_bounds__(kTC ? kTcThreads : kGemvThreads, 1)
       }
       a.sched[0] = 0;
       a.sched[1] = 0;
+      a.sched[2] = 0;
       fence_acq_rel_gpu();
     }
   }

@@ -63,6 +63,12 @@ struct StreamArgs {
   int64_t y_ld;
   int y_bf16;
   int y_vec4;  // fp32 Y, 16-byte aligned rows: float4 stores
+  // Direct Y (kModeBlock, dynamic queue, tcgen05, one GPU, fp32 Y in device
+  // memory): after griddepcontrol.wait every CTA's epilogue warps zero their
+  // 1/G slice of Y and count it on sched[2]; down pieces red.add their
+  // partial sums straight into Y once sched[2] == G.  No per-tile counter,
+  // no finalize pass and no workspace re-zeroing on the launch's tail.
+  int y_direct;
   // tcgen05: independent accumulators per tile (MMA k of a K block goes to
   // accumulator k % nacc), so consecutive MMAs do not serialise on one
   // accumulator; the epilogue sums them.  TMEM = 2 x nacc x n_pad columns.

@@ -6,7 +6,9 @@ v4 partial-sum reductions on full shards too (DFK_RED_V4=2) or nowhere
 (DFK_RED_V4=0), two accumulator chains (DFK_NACC=2), the full grid and
 down chunks of 8 K blocks at every N (DFK_GRID / DFK_DN_CHUNK), balanced
 stream-K pieces (DFK_BAL: tile-straddling stage-1 and down ranges, K-block
-counted tile completion).  Shapes
+counted tile completion), fp32 Y through the workspace + finalize pass
+instead of direct red.adds into Y (DFK_Y_DIRECT=0), and the stage-1 tail
+split on a 100-CTA grid (DFK_S1_TAIL=3).  Shapes
 cover a full stage-1 wave (d_ff/64 >= SMs) and a small shard, B across the
 N = 16 / 32 / 64 MMA widths.
 """
@@ -55,6 +57,8 @@ print("worst", worst)
     {"DFK_GRID": "148", "DFK_DN_CHUNK": "8"},
     {"DFK_BAL": "2"},
     {"DFK_BAL": "1", "DFK_GRID": "140"},
+    {"DFK_Y_DIRECT": "0"},
+    {"DFK_S1_TAIL": "3", "DFK_GRID": "100"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_knob_paths_match_oracle(env):
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)],

@@ -486,6 +486,31 @@ def test_stage1_stream_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, fam):
         assert rel_err(a2.download(), a2_ref) <= TOL
 
 
+@pytest.mark.parametrize("B", [1, 16, 64])
+def test_direct_y_overwrites_stale_output(rt, ctx, oracle_lib, B):
+    """Direct Y (fp32 Y in device memory): the block kernel zeroes Y after
+    the PDL wait and red.adds the down partial sums into it, so whatever Y
+    held before (NaN here, or the previous call's result) must not leak into
+    the result; back-to-back calls on different inputs stay exact."""
+    dm, df = 1024, 9600  # 150 stage-1 tiles: a full wave plus a tail
+    x, wu, wg, wd = instance(oracle_lib, 77 + B, B, dm, df)
+    x2 = instance(oracle_lib, 78 + B, B, dm, df)[0]
+    _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    _, y_ref2 = oracle_lib.forward(x2, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    xd, xd2 = ctx.array((B, dm)).upload(x), ctx.array((B, dm)).upload(x2)
+    y = ctx.array((B, dm), rt.F32)
+    y.upload(np.full((B, dm), np.nan, np.float32))
+    ctx.forward(w, xd, y)
+    assert rel_err(y.download(), y_ref) <= TOL
+    for _ in range(3):
+        ctx.forward(w, xd2, y)
+        ctx.forward(w, xd, y)
+    assert rel_err(y.download(), y_ref) <= TOL
+    ctx.forward(w, xd2, y)
+    assert rel_err(y.download(), y_ref2) <= TOL
+
+
 @pytest.mark.parametrize("fam,B", [("tc", 4), ("tc", 40), ("gemv", 4)])
 def test_stage1_tail_split_parity_and_mutant(rt, ctx, oracle_lib, fam, B):
     """Tail split (dfk_config.s1_tail): the first wave of stage-1 tiles runs
