@@ -797,7 +797,7 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     // Direct Y (stream_kernels.cuh): fp32 Y in this GPU's memory with whole
     // 16-byte row groups; not under the fused TP all-reduce (its own tile
     // owners) nor for Y in mapped host memory (no PCIe reductions).
-    if (a.dynamic && L.tc && !tp && knobs().y_direct && !y_bf16 && a.y_vec4 &&
+    if (a.dynamic && !tp && knobs().y_direct && !y_bf16 && a.y_vec4 &&
         w->d_model % 4 == 0 && device_memory(a.y))
       a.y_direct = 1;
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)

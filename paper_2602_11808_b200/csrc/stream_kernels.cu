@@ -588,6 +588,42 @@ __device__ __forceinline__ void red_rows_v4(float (&v)[16], float* col0, int64_t
   }
 }
 
+// Direct Y (StreamArgs::y_direct), run by the nthr epilogue / math threads
+// of every CTA once per launch: after griddepcontrol.wait (the previous
+// launch may still read or write Y) zero this CTA's 1/G slice of Y and count
+// it on sched[2].  Slices start on 128-byte lines (8 float4), so a warp's
+// 512-byte store covers whole sectors (unaligned slices cost a partial sector
+// per warp store: +30 KB of L2 writes at B = 64).
+__device__ __forceinline__ void direct_y_zero(const StreamArgs& a, int tid, int nthr) {
+  pdl_wait();
+  const int64_t nv = static_cast<int64_t>(a.B) * (a.out_cols / 4);
+  const int64_t v0 = (nv * blockIdx.x / gridDim.x) & ~int64_t{7};
+  const int64_t v1 =
+      blockIdx.x + 1 == gridDim.x ? nv : (nv * (blockIdx.x + 1) / gridDim.x) & ~int64_t{7};
+  const int q4 = a.out_cols / 4;
+  for (int64_t v = v0 + tid; v < v1; v += nthr) {
+    const int64_t n = v / q4, j = (v % q4) * 4;
+    __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.y) + n * a.y_ld + j),
+           make_float4(0.f, 0.f, 0.f, 0.f));
+  }
+  named_bar(1, nthr);  // then one cumulative release: see down_finish_tile
+  if (tid == 0) {
+    fence_acq_rel_gpu();
+    atomicAdd(a.sched + 2, 1);
+  }
+}
+
+// Before a CTA's first reduction into Y: every slice is zero (long true by
+// then -- every CTA zeroes right after the PDL wait, the first down piece
+// comes after stage-1 streaming).
+__device__ __forceinline__ void direct_y_wait(const StreamArgs& a, int tid, int nthr) {
+  if (tid == 0)
+    while (static_cast<int>(ld_acquire(reinterpret_cast<const unsigned*>(a.sched + 2))) <
+           static_cast<int>(gridDim.x)) {
+    }
+  named_bar(1, nthr);
+}
+
 __device__ __forceinline__ float* down_acc(const StreamArgs& a, int t) {
   return a.tp_size > 1 ? a.tp_yacc[t % a.tp_size] : a.yacc;
 }
@@ -1018,6 +1054,8 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
   const int wbytes_all = a.kbs * kBlockBytes;
   const int xblk = a.n_pad * 128;
   int64_t it = 0;
+  bool y_zeroed = false;
+  if (a.y_direct) direct_y_zero(a, tid, nthr);
   PieceReader pi;
   Piece pc;
   while (pi.next(a, p, pq, false, pc)) {
@@ -1109,13 +1147,19 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
       }
       if (a.flags) s1_publish(a, pc.tile, tid, nthr);
     } else {
+      if (a.y_direct && !y_zeroed) {
+        direct_y_wait(a, tid, nthr);
+        y_zeroed = true;
+      }
+      float* ybase = a.y_direct ? reinterpret_cast<float*>(a.y) : down_acc(a, pc.tile);
+      const int64_t ld = a.y_direct ? a.y_ld : a.yacc_ld;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int j = pc.tile * kDownCols + gemv_row(r, mw, q);
 #pragma unroll
         for (int n = 0; n < NB; ++n) {
           if (c == 0 && n < a.B && j < a.out_cols) {
-            float* dst = down_acc(a, pc.tile) + static_cast<int64_t>(n) * a.yacc_ld + j;
+            float* dst = ybase + static_cast<int64_t>(n) * ld + j;
             if (a.tp_size > 1)
               atomicAdd_system(dst, acc[r][n]);
             else
@@ -1123,7 +1167,7 @@ __device__ __forceinline__ void gemv_consume(const StreamArgs& a, const Plan& p,
           }
         }
       }
-      down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, nthr, smem_flag);
+      if (!a.y_direct) down_finish_tile(a, p, pc.tile, pc.kb1 - pc.kb0, tid, nthr, smem_flag);
     }
     if (tid == 0) trace_stamp(a, 2 + 2 * pi.i);
   }
@@ -1346,29 +1390,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
   int split_iter = 0;
   bool dn_stamped = false;
   bool y_zeroed = false;  // direct Y: every CTA's slice is zero (seen once)
-  if (a.y_direct) {
-    // The previous launch may still read / write Y until it completes.
-    pdl_wait();
-    // slices start on 128-byte lines (8 float4): a warp's 512-byte store then
-    // covers 16 whole sectors (unaligned slices cost one partial sector per
-    // warp store, +30 KB of L2 writes at B = 64)
-    const int64_t nv = static_cast<int64_t>(a.B) * (a.out_cols / 4);
-    const int64_t v0 = (nv * blockIdx.x / gridDim.x) & ~int64_t{7};
-    const int64_t v1 = blockIdx.x + 1 == gridDim.x
-                           ? nv
-                           : (nv * (blockIdx.x + 1) / gridDim.x) & ~int64_t{7};
-    const int q4 = a.out_cols / 4;
-    for (int64_t v = v0 + tid; v < v1; v += 128) {
-      const int64_t n = v / q4, j = (v % q4) * 4;
-      __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.y) + n * a.y_ld + j),
-             make_float4(0.f, 0.f, 0.f, 0.f));
-    }
-    named_bar(1, 128);  // then one cumulative release: see down_finish_tile
-    if (tid == 0) {
-      fence_acq_rel_gpu();
-      atomicAdd(a.sched + 2, 1);
-    }
-  }
+  if (a.y_direct) direct_y_zero(a, tid, 128);
   PieceReader pi;
   Piece pc;
   while (pi.next(a, p, pq, false, pc)) {
@@ -1516,12 +1538,7 @@ __device__ __forceinline__ void tc_epilogue(const StreamArgs& a, const Plan& p,
       const int j = pc.tile * kDownCols + row;
       const bool jok = j < a.out_cols;
       if (a.y_direct && !y_zeroed) {
-        // (long true by now: every CTA zeroes right after the PDL wait)
-        if (tid == 0)
-          while (static_cast<int>(ld_acquire(reinterpret_cast<const unsigned*>(a.sched + 2))) <
-                 static_cast<int>(gridDim.x)) {
-          }
-        named_bar(1, 128);
+        direct_y_wait(a, tid, 128);
         y_zeroed = true;
       }
       float* yp = a.y_direct ? reinterpret_cast<float*>(a.y) + j : down_acc(a, pc.tile) + j;
