@@ -638,6 +638,11 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     int64_t grid = cfg.down_ctas > 0 ? cfg.down_ctas : ctx->sm_count;
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, U));
     DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a, true));
+    // Direct Y as in the block kernel (every CTA zeroes its slice after the
+    // PDL wait; the first reduction comes a whole first piece later).
+    if (a.dynamic && knobs().y_direct && !y_bf16 && a.y_vec4 && w->d_model % 4 == 0 &&
+        device_memory(a.y))
+      a.y_direct = 1;
     cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
                                   static_cast<int>(grid), cfg.pdl != 0,
                                   ctx->stream, &a3m);

@@ -25,6 +25,7 @@ ap.add_argument("--shapes", default="llama8b:2,4,8;qwen7b:2,4,8;qwen32b:2,4,8;ll
 ap.add_argument("--batches", default="1,2,4,8,16,32,64")
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--json", default="")
+ap.add_argument("--cks", default="0,8,16", help="down chunk sizes (0 = heuristic)")
 a = ap.parse_args()
 ctx = rt.Context(0)
 ev0, ev1 = rt.Event(), rt.Event()
@@ -70,7 +71,7 @@ for spec in a.shapes.split(";"):
             fams = [rt.FAMILY_TC] + ([rt.FAMILY_GEMV] if B <= 8 else [])
             for fam in fams:
                 for s1k in s1ks:
-                    for ck in (0, 8, 16):
+                    for ck in (int(v) for v in a.cks.split(",")):
                         lab = f"{'gemv' if fam == rt.FAMILY_GEMV else 'tc'}_s1k{s1k}_ck{ck}"
                         cfgs[lab] = rt.Config.make(s1_family=fam, down_family=fam,
                                                    block_kernel=1, dynamic_sched=1,
