@@ -279,11 +279,13 @@ TP_SHAPES = (("Qwen2.5-32B", 5120, 27648, (1, 2, 4, 8)),
              ("Llama-3.1-70B", 8192, 28672, (2, 4, 8)))
 
 
-def tp_shards(rt, ctx, ev0, ev1, batches=(1, 16, 64), reps=20):
+def tp_shards(rt, ctx, ev0, ev1, batches=(1, 16, 64), reps=20, tune=True):
     """BASELINE configs[3] / [4] on ONE GPU: a rank of TP=P runs the block of
     its balanced_ranges(d_ff, P) shard (tp.cpp:8-29), so its kernel time is
     that block's time (the all-reduce, fused in the kernel at N > 1, is not in
-    this number).  Library default config; weight sets rotated beyond 3x L2."""
+    this number).  `us`: the library default config (what a NULL-config call
+    runs); `tuned_us`: the scheduler's pick for that shard and batch (dfk_tune,
+    tuner.cpp's profile/select).  Weight sets rotated beyond 3x L2."""
     import math
     out = {}
     for name, dm, df, Ps in TP_SHAPES:
@@ -303,17 +305,37 @@ def tp_shards(rt, ctx, ev0, ev1, batches=(1, 16, 64), reps=20):
             for B in batches:
                 x = ctx.array((B, dm)).fill_uniform(31 + B)
                 y = ctx.array((B, dm), rt.F32)
-                for i in range(4):
-                    ctx.forward(ws[i % nsets], x, y)
-                ctx.sync()
-                ev0.record(ctx)
-                for i in range(reps):
-                    ctx.forward(ws[i % nsets], x, y)
-                ev1.record(ctx)
-                ctx.sync()
-                us = ev0.elapsed_ms(ev1) * 1e3 / reps
+
+                def run(cfg):
+                    for i in range(4):
+                        ctx.forward(ws[i % nsets], x, y, cfg=cfg)
+                    ctx.sync()
+                    ev0.record(ctx)
+                    for i in range(reps):
+                        ctx.forward(ws[i % nsets], x, y, cfg=cfg)
+                    ev1.record(ctx)
+                    ctx.sync()
+                    return ev0.elapsed_ms(ev1) * 1e3 / reps
+
+                if tune:
+                    # tune first, then time default and pick alternately (the
+                    # tuning burst can leave the GPU at its power cap for a while)
+                    # (after dfk_tune a NULL config runs the pick: keep the
+                    # library default's resolved config)
+                    dcfg = ctx.resolve_config(ws[0], B)
+                    cfg, _, _ = ctx.tune(ws[0], B, None, 1, 4)
+                    time.sleep(1.0)  # let the power controller settle after the burst
+                    t = [run(dcfg), run(cfg), run(dcfg), run(cfg)]
+                    us, tus = (t[0] + t[2]) / 2, (t[1] + t[3]) / 2
+                else:
+                    us = run(None)
                 gbs = block_bytes(B, dm, dfs) / (us * 1e-6) / 1e9
                 row[str(B)] = {"us": round(us, 2), "gbs": round(gbs, 1)}
+                if tune:
+                    row[str(B)].update({
+                        "tuned_us": round(tus, 2),
+                        "tuned_gbs": round(block_bytes(B, dm, dfs) / (tus * 1e-6) / 1e9, 1),
+                        "tuned_cfg": cfg.label.decode()})
             out[f"{name} tp{P}"] = {"d_model": dm, "d_ff_shard": dfs, "per_batch": row}
             del ws
     return out
@@ -508,6 +530,7 @@ def main():
         for B in sweep:
             cfg, hit, entry = ctx.tune(sets[0], B, None, 1, 4)
             chosen[B] = cfg.label.decode()
+        time.sleep(1.0)  # let the power controller settle after the tuning burst
     cfgs = {B: ctx.select_config(sets[0], B) for B in sweep}
 
     def call(B, i, cfg=None):
@@ -691,7 +714,7 @@ def main():
         decode = decode_loop(rt, ctx, ev0, ev1)
     shards = None
     if P == 1 and not args.no_tp_shards:
-        shards = tp_shards(rt, ctx, ev0, ev1)
+        shards = tp_shards(rt, ctx, ev0, ev1, tune=not args.no_tune)
     tp_full = None
     if P > 1 and not args.no_tp_shards and not args.tp_emulate:
         tp_full = tp_configs(rt, ctx, ev0, ev1, rank, P, tp_mode, barrier, max_over_ranks)

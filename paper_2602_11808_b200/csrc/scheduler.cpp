@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kCacheFormatVersion = 1;
 constexpr double kGateTolerance = 1e-2;  // max|dY| / max|Y_ref|, bf16 path
-constexpr int kRepsPerRun = 8;
+constexpr int kRepsPerRun = 16;
 
 struct Result {
   std::string label;
@@ -120,6 +120,19 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, const ShapeTiles* w
       std::snprintf(d.label, sizeof(d.label), "%s", config_label(d).c_str());
       add(d);
     }
+  }
+  // The dynamic block kernel on every SM where the default grid is 7/8 of
+  // them (N <= 16, or shards without a full stage-1 wave): the idle eighth
+  // that starts the next PDL launch early loses to more streaming CTAs on
+  // some shards (Qwen2.5-7B / Qwen2.5-32B / Llama-70B TP4: -3 to -7 %), and
+  // the stage-1 split follows the grid (profiles/r2_tail_split.md).
+  if (B <= 16 || w->s1_tiles < ctx->sm_count) {
+    dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, 0, 1, 1);
+    c.dynamic_sched = 1;
+    c.s1_ctas = ctx->sm_count;
+    std::snprintf(c.label, sizeof(c.label), "%s", "");
+    std::snprintf(c.label, sizeof(c.label), "%s", config_label(c).c_str());
+    add(c);
   }
   // 0 = library default (every SM); 3/4 of the SMs was the default before
   // the dynamic queue and stays a candidate
