@@ -437,6 +437,32 @@ def test_forward_host_async_pipelined(rt, ctx, oracle_lib):
         assert rel_err(hy[i].arr, refs[i]) <= TOL, i
 
 
+def test_forward_host_async_zero_copy_path(rt, ctx, oracle_lib):
+    """Host-buffer calls that do not take the copy-engine path (GEMV chunks at
+    B > 8, the static block plan) run the zero-copy chain: the kernel writes Y
+    straight into the caller's pinned buffer.  Y in mapped host memory must
+    not take the direct-Y mode (no reductions over PCIe): the workspace +
+    finalize path, stale host contents overwritten."""
+    from paper_2602_11808_b200.runtime import PinnedHost, to_bf16_bits
+    dm, df = 512, 1024
+    cfgs = [rt.Config.make(block_kernel=1, dynamic_sched=1, s1_family=rt.FAMILY_GEMV,
+                           down_family=rt.FAMILY_GEMV),
+            rt.Config.make(block_kernel=1, dynamic_sched=0)]
+    for j, B in enumerate((12, 20)):
+        x, wu, wg, wd = instance(oracle_lib, 70 + j, B, dm, df)
+        w = ctx.weights(wg, wu, wd)
+        y_ref = oracle_lib.forward(x, wu, wg, wd)[1]
+        px = PinnedHost((B, dm), np.uint16)
+        px.arr[...] = to_bf16_bits(x)
+        for cfg in cfgs:
+            py = PinnedHost((B, dm), np.float32)
+            py.arr[...] = np.nan
+            for _ in range(2):
+                ctx.forward_host_async(w, px.arr, py.arr, cfg=cfg)
+            ctx.sync()
+            assert rel_err(py.arr, y_ref) <= TOL, (B, cfg.label)
+
+
 @pytest.mark.parametrize("split", [2, 4])
 def test_split_k_silu_per_chunk_mutant_fails(rt, ctx, oracle_lib, split):
     """Negative control (the reference's SiluPerKChunk mutant,
