@@ -190,7 +190,9 @@ DFK_API int dfk_stage1(dfk_context ctx, dfk_weights w, const void* x,
 DFK_API int dfk_down(dfk_context ctx, dfk_weights w, const void* a2,
                      int64_t batch, void* y, int32_t y_dtype,
                      const dfk_config* cfg);
-/* Whole block: Y = stage-2(stage-1(X)); A2 lives in context scratch. */
+/* Whole block: Y = stage-2(stage-1(X)); A2 lives in context scratch.  An
+ * fp32 Y in device memory is zeroed by the kernel and accumulated in place
+ * ("direct Y"); X may overlap Y (in-place callers get the workspace path). */
 DFK_API int dfk_forward(dfk_context ctx, dfk_weights w, const void* x,
                         int64_t batch, void* y, int32_t y_dtype,
                         const dfk_config* cfg);

@@ -523,6 +523,11 @@ int ensure_down_workspace(dfk_context_s* ctx, dfk_weights_s* w, int64_t rows) {
                     ctx->stream);
 }
 
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  const auto pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+  return pa < pb + nb && pb < pa + na;
+}
+
 // True for memory of a device (cudaMalloc / pool), false for host-mapped,
 // managed or unknown pointers.
 bool device_memory(const void* p) {
@@ -640,7 +645,10 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a, true));
     // Direct Y as in the block kernel (every CTA zeroes its slice after the
     // PDL wait; the first reduction comes a whole first piece later).
+    // (not when Y overlaps the A2 operand: Y is zeroed while A2 is read)
     if (a.dynamic && knobs().y_direct && !y_bf16 && a.y_vec4 && w->d_model % 4 == 0 &&
+        !overlaps(ap, static_cast<size_t>(B * a_ld) * 2, y,
+                  static_cast<size_t>(B * y_ld) * 4) &&
         device_memory(a.y))
       a.y_direct = 1;
     cudaError_t e = launch_stream(kModeDown, L.tc, gemv_nb(nb), tm, tm, a,
@@ -802,8 +810,12 @@ int block_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* x, int64_t B,
     // Direct Y (stream_kernels.cuh): fp32 Y in this GPU's memory with whole
     // 16-byte row groups; not under the fused TP all-reduce (its own tile
     // owners) nor for Y in mapped host memory (no PCIe reductions).
+    // Nor when Y overlaps X: Y is zeroed while X is still being loaded.
     if (a.dynamic && !tp && knobs().y_direct && !y_bf16 && a.y_vec4 &&
-        w->d_model % 4 == 0 && device_memory(a.y))
+        w->d_model % 4 == 0 &&
+        !overlaps(xp, static_cast<size_t>(B * x_ld) * 2, y,
+                  static_cast<size_t>(B * y_ld) * 4) &&
+        device_memory(a.y))
       a.y_direct = 1;
     if (a.bp_rB < 0 || a.bp_rB > grid || a.bp_rA < 0 || a.bp_rA > grid)
       return fail(DFK_ERR_CUDA, "internal: block plan remainder out of range");

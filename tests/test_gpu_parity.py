@@ -537,6 +537,25 @@ def test_direct_y_overwrites_stale_output(rt, ctx, oracle_lib, B):
     assert rel_err(y.download(), y_ref2) <= TOL
 
 
+def test_direct_y_not_taken_when_y_overlaps_x(rt, ctx, oracle_lib):
+    """X (bf16) living inside Y's own bytes (an in-place caller): the kernel
+    would zero Y while X is still being loaded, so direct Y must not be taken
+    -- the workspace path writes Y only after every X load."""
+    B, dm, df = 8, 1024, 1536
+    x, wu, wg, wd = instance(oracle_lib, 95, B, dm, df)
+    _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    y = ctx.array((B, dm), rt.F32)
+    xv = rt.DeviceArray.__new__(rt.DeviceArray)  # a non-owning bf16 view of Y's bytes
+    xv.ctx, xv.shape, xv.dtype, xv.nbytes, xv.ptr = ctx, (B, dm), rt.BF16, B * dm * 2, y.ptr
+    try:
+        xv.upload(x)
+        ctx.forward(w, xv, y)
+        assert rel_err(y.download(), y_ref) <= TOL
+    finally:
+        xv.ptr = None  # not ours to free
+
+
 @pytest.mark.parametrize("fam,B", [("tc", 4), ("tc", 40), ("gemv", 4)])
 def test_stage1_tail_split_parity_and_mutant(rt, ctx, oracle_lib, fam, B):
     """Tail split (dfk_config.s1_tail): the first wave of stage-1 tiles runs
