@@ -645,8 +645,11 @@ int down_fused(dfk_context_s* ctx, dfk_weights_s* w, const void* a2,
     DFK_TRY(fill_dynamic(ctx, w, cfg, static_cast<int>(grid), &a, true));
     // Direct Y as in the block kernel (every CTA zeroes its slice after the
     // PDL wait; the first reduction comes a whole first piece later).
-    // (not when Y overlaps the A2 operand: Y is zeroed while A2 is read)
+    // (not when Y overlaps the A2 operand: Y is zeroed while A2 is read; and
+    // only when every CTA is resident -- a CTA's first reduction waits for
+    // all slices, so a caller's down_ctas beyond the SM count would hang)
     if (a.dynamic && knobs().y_direct && !y_bf16 && a.y_vec4 && w->d_model % 4 == 0 &&
+        grid <= ctx->sm_count &&
         !overlaps(ap, static_cast<size_t>(B * a_ld) * 2, y,
                   static_cast<size_t>(B * y_ld) * 4) &&
         device_memory(a.y))

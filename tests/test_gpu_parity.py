@@ -49,6 +49,9 @@ def configs(rt, B):
                                               s1_ctas=5, chunk_kb=3, kbs=2),
         "dyn_fused_tc": rt.Config.make(dynamic_sched=1, down_ctas=148, s1_ctas=148),
         "dyn_fused_ch5": rt.Config.make(dynamic_sched=1, chunk_kb=5, s1_ctas=9, down_ctas=13),
+        # more down CTAs than SMs: not all resident, so no direct Y (its
+        # first reduction waits for every CTA's slice)
+        "dyn_fused_dn400_ch2": rt.Config.make(dynamic_sched=1, chunk_kb=2, down_ctas=400),
         "dyn_block_s1k3": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_chunk_kb=3),
         "dyn_fused_s1k2_c7": rt.Config.make(dynamic_sched=1, s1_chunk_kb=2, s1_ctas=7),
         "dyn_block_wholetiles": rt.Config.make(block_kernel=1, dynamic_sched=1,
