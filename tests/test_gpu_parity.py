@@ -727,7 +727,8 @@ def test_weight_layouts_pack_identically(rt, ctx, oracle_lib):
     ("qwen2.5-7b", 1, 3584, 18944), ("qwen2.5-7b", 16, 3584, 18944),
     ("qwen2.5-32b tp8 shard", 64, 5120, 3456), ("qwen2.5-32b tp8 shard", 2, 5120, 3456),
     ("llama-3.1-70b tp8 shard", 1, 8192, 3584), ("llama-3.1-70b tp8 shard", 32, 8192, 3584),
-    ("llama-3.1-70b tp2 shard", 8, 8192, 14336)])
+    ("llama-3.1-70b tp2 shard", 8, 8192, 14336), ("qwen2.5-32b tp2 shard", 64, 5120, 13824),
+    ("llama-3.1-70b tp4 shard", 16, 8192, 7168)])
 def test_baseline_config_shapes_parity(rt, ctx, oracle_lib, name, B, dm, df):
     """BASELINE.json configs 3-5 at full size (a TP rank's block is the block
     of its d_ff shard, balanced_ranges tp.cpp:8-29): the library default
@@ -738,12 +739,31 @@ def test_baseline_config_shapes_parity(rt, ctx, oracle_lib, name, B, dm, df):
     a2_ref, y_ref = oracle_lib.forward(x, wu, wg, wd)
     w = ctx.weights(wg, wu, wd)
     for cfg in (None, rt.Config.make(block_kernel=1, dynamic_sched=1, s1_chunk_kb=16, chunk_kb=8),
+                rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=3),
+                rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=4, kbs=3),
+                rt.Config.make(block_kernel=1, dynamic_sched=1, s1_ctas=148),
                 rt.Config.make(variant=rt.VARIANT_TWO_KERNEL)):
         xd = ctx.array((B, dm)).upload(x)
         y = ctx.array((B, dm), rt.F32)
         ctx.forward(w, xd, y, cfg=cfg)
         err = rel_err(y.download(), y_ref)
         assert err <= TOL, (name, B, cfg.label if cfg else "default", err)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dm,df,B", [(5120, 13824, 32), (8192, 7168, 1), (5120, 3456, 64)])
+def test_scheduler_pick_matches_oracle(rt, ctx, oracle_lib, dm, df, B, tmp_path):
+    """Whatever dfk_tune picks for a BASELINE shard (tail split, full grid,
+    stream-K chunks, cuBLASLt ...) is what NULL-config calls run afterwards:
+    that pick, at full size, against the fp64 oracle."""
+    x, wu, wg, wd = instance(oracle_lib, 20261017 + B, B, dm, df)
+    _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+    w = ctx.weights(wg, wu, wd)
+    cfg, _, _ = ctx.tune(w, B, str(tmp_path / "cache.json"), 1, 3)
+    xd = ctx.array((B, dm)).upload(x)
+    y = ctx.array((B, dm), rt.F32)
+    ctx.forward(w, xd, y)  # NULL config: the scheduler's decision
+    assert rel_err(y.download(), y_ref) <= TOL, cfg.label
 
 
 @pytest.mark.parametrize("B", [255, 256, 257, 300])
