@@ -329,7 +329,7 @@ struct Knobs {
   int a2_tma = env_int("DFK_A2_TMA", 1);            // A2 by one TMA store per tile
   int xrows8 = env_int("DFK_XROWS8", 1);            // 8-row activation boxes at B <= 8
   int nacc = env_int("DFK_NACC", 1);                // independent accumulator chains
-  int pf_kb = env_int("DFK_PF_KB", 12);             // K blocks prefetched to L2 before PDL wait
+  int pf_kb = env_int("DFK_PF_KB", -1);             // K blocks prefetched to L2 before PDL wait (-1 = auto)
   int trace_s0 = env_int("DFK_TRACE_S0", 24);       // first ring stage the trace records
   int dn_chunk = env_int("DFK_DN_CHUNK", 0);        // down K chunk (0 = heuristic)
   int grid = env_int("DFK_GRID", 0);                // block-kernel CTAs (0 = heuristic)
@@ -507,9 +507,11 @@ void fill_common(dfk_context_s* ctx, dfk_weights_s* w, int64_t nb, bool tc,
     int n = std::max(1, std::min(knobs().nacc, 256 / n_pad));
     a->nacc = n >= 4 ? 4 : n >= 2 ? 2 : 1;
   }
-  // 12 K blocks (192 KiB) of L2 prefetch: the measured optimum (A/B sweep
-  // 0..60, profiles/r1b_tuning.md).
-  a->pf_kb = knobs().pf_kb;
+  // 12 K blocks (192 KiB) of L2 prefetch: the measured optimum on full
+  // shards (A/B sweep 0..60, profiles/r1b_tuning.md); 8 on shards with fewer
+  // stage-1 tiles than SMs (-0.2 to -0.5 us on the TP8 shards once the down
+  // tail got shorter, profiles/r2_tail_split.md).
+  a->pf_kb = knobs().pf_kb >= 0 ? knobs().pf_kb : (w->s1_tiles < ctx->sm_count ? 8 : 12);
   const int ms = std::max(2, max_stages(ctx, n_pad, a->kbs, sk, a->a2_tma));
   a->stages = stages_req > 0 ? std::max(2, std::min(stages_req, ms)) : ms;
 }
