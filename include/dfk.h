@@ -138,7 +138,8 @@ typedef struct dfk_config {
                            tiles than CTAs: the first wave of tiles runs
                            whole, every later tile is split into s1_tail
                            K parts (stream-K), spreading the last stage-1
-                           wave over all CTAs (0/1 = off)                 */
+                           wave over all CTAs (0 = auto: 3 at batch > 16,
+                           off below; 1 = off)                            */
   char label[64];       /* scheduler label, e.g. "fused_tc_s12_pdl"        */
 } dfk_config;
 

@@ -114,7 +114,7 @@ std::string config_label(const dfk_config& c) {
   if (c.block_kernel) {
     if (c.dynamic_sched) o << "dyn" << c.chunk_kb << "_";
     if (c.dynamic_sched && c.s1_chunk_kb) o << "s1k" << c.s1_chunk_kb << "_";
-    if (c.dynamic_sched && c.s1_tail > 1) o << "s1t" << c.s1_tail << "_";
+    if (c.dynamic_sched && c.s1_tail > 0) o << "s1t" << c.s1_tail << "_";
     if (c.s1_split_k > 1) o << "sk" << c.s1_split_k << "_";
     o << "block_" << (c.s1_family == DFK_FAMILY_GEMV ? "gemv" : "tc") << "_st"
       << c.s1_stages << "_kbs" << c.kbs << "_c" << c.s1_ctas
@@ -427,7 +427,13 @@ int fill_dynamic(dfk_context_s* ctx, dfk_weights_s* w, const dfk_config& cfg,
   a->s1_chunk = s1c;
   a->s1_tail = 0;
   a->s1_whole = 0;
-  const int tail = knobs().s1_tail > 0 ? knobs().s1_tail : cfg.s1_tail;
+  // (0 = auto: 3 parts at N >= 32 -- B = 32: Llama-8B -3 %, Qwen2.5-32B TP2
+  // -8 %, Llama-70B TP2 -3 %; B = 64: -1 / -7 / -2 %, Qwen2.5-7B +1 %;
+  // neutral at N <= 16, profiles/r2_tail_split.md; 1 = off)
+  const int tail = knobs().s1_tail > 0 ? knobs().s1_tail
+                   : cfg.s1_tail > 0  ? cfg.s1_tail
+                   : a->n_pad >= 32   ? 3
+                                      : 0;
   if (block && s1c >= w->s1_kblocks && tail > 1 && w->s1_tiles > grid && a->split_k <= 1) {
     a->s1_tail = std::min(tail, w->s1_kblocks);
     a->s1_whole = knobs().s1_whole > 0 ? std::min(knobs().s1_whole, w->s1_tiles) : grid;

@@ -192,9 +192,9 @@ std::vector<dfk_config> candidates(const dfk_context_s* ctx, const ShapeTiles* w
   // 57.2 -> 54.5 us, Qwen2.5-32B TP2 69.0 -> 63.8 us; the best part count
   // differs per shape and batch, profiles/r2_tail_split.md) ...
   if (w->s1_tiles > ctx->sm_count) {
-    for (int parts : {2, 3, 4})
+    for (int parts : {1, 2, 3, 4})  // 1: whole tiles (the N >= 32 default is 3)
       for (int kbs : {0, 3}) {
-        if (B <= 16 && (parts > 2 || kbs)) continue;
+        if (B <= 16 && (parts != 2 || kbs)) continue;
         dfk_config c = make_cfg(DFK_VARIANT_FUSED, DFK_FAMILY_TC, DFK_FAMILY_TC, kbs, 1, 1);
         c.dynamic_sched = 1;
         c.s1_tail = parts;

@@ -17,7 +17,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--B", type=int, default=16)
 ap.add_argument("--dm", type=int, default=4096)
 ap.add_argument("--df", type=int, default=14336)
-ap.add_argument("--variant", default="fused", choices=["fused", "two", "four", "mutant2"])
+ap.add_argument("--variant", default="fused",
+                choices=["fused", "fused_notail", "two", "four", "mutant2"])
 a = ap.parse_args()
 ctx = rt.Context(0)
 s = 1 / np.sqrt(a.dm)
@@ -32,7 +33,10 @@ cfg = {"fused": None, "two": rt.Config.make(variant=rt.VARIANT_TWO_KERNEL),
        "four": rt.Config.make(variant=rt.VARIANT_FOUR_KERNEL),
        # the fused block kernel with SiLU(A_gate) round-tripped through global
        # memory in its epilogue (MaterializeIntermediate, verification.cpp:126-169)
-       "mutant2": rt.Config.make(block_kernel=1, dynamic_sched=1, mutant=2)}[a.variant]
+       "mutant2": rt.Config.make(block_kernel=1, dynamic_sched=1, mutant=2, s1_tail=1),
+       # the default block kernel with whole stage-1 tiles only (no tail split:
+       # every tile through the epilogue the mutant modifies)
+       "fused_notail": rt.Config.make(block_kernel=1, dynamic_sched=1, s1_tail=1)}[a.variant]
 for _ in range(3):
     ctx.forward(w, x, y, cfg=cfg)
 ctx.profiler_range(True)
