@@ -281,6 +281,28 @@ def test_decode_loop_eager_and_graph(rt, ctx, oracle_lib, B, L, steps):
         assert rel_err(y.download(), xr) <= 2 * TOL, cfg.label
 
 
+@pytest.mark.parametrize("B", [32, 64])
+def test_decode_graph_with_tail_split(rt, ctx, oracle_lib, B):
+    """Decode chains at N >= 32 on a shard with more stage-1 tiles than SMs
+    (d_ff = 9600: 150 tiles), where the default splits the tiles past the
+    first wave into K parts (stream-K partial sums, bf16 Y through the
+    finalize path): eager and graph replays against the oracle chain."""
+    dm, df, L, steps = 512, 9600, 2, 2
+    layers = [instance(oracle_lib, 400 + l, B, dm, df)[1:] for l in range(L)]
+    x0 = instance(oracle_lib, 399, B, dm, df)[0]
+    ws = [ctx.weights(wg, wu, wd) for (wu, wg, wd) in layers]
+    xr = x0
+    for _ in range(steps):
+        for (wu, wg, wd) in layers:
+            xr = oracle_lib.quantize_bf16(oracle_lib.forward(xr, wu, wg, wd)[1])[0]
+    xd = ctx.array((B, dm)).upload(x0)
+    for graph in (False, True, True):
+        y = ctx.array((B, dm))
+        ctx.decode(ws, xd, steps, y, graph=graph)
+        ctx.sync()
+        assert rel_err(y.download(), xr) <= 2 * TOL, (graph, rel_err(y.download(), xr))
+
+
 def test_decode_graph_interleaved_with_eager_calls(rt, ctx, oracle_lib):
     """Graph replays and eager block launches interleave on one context (the
     block-kernel epoch protocol, decode.cpp header)."""
