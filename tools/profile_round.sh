@@ -1,9 +1,12 @@
 #!/bin/bash
 # One GPU call: bench line, ncu launch list of a short bench, ncu --set full of
-# the default (block) kernel at every batch of the sweep.  Outputs under
-# gpurun_out/ (summarise with tools/ncu_summary.py).
+# the default (block) kernel at every batch of the sweep, summarised on the box
+# (tools/ncu_summary.py) so that only small files come back: block_traffic.json
+# (bench.py's roofline.traffic), launches.md/.csv, raw pages of B = 1/16/64.
+# The .ncu-rep files are deleted after summarising (they exceed gpurun's 64 MiB
+# transfer limit together).  Outputs under $OUT (default gpurun_out/prof).
 set -u
-OUT=${OUT:-gpurun_out}
+OUT=${OUT:-gpurun_out/prof}
 mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 if [ -z "${NOBENCH:-}" ]; then
@@ -18,3 +21,10 @@ for B in ${SWEEP:-1 2 4 8 16 32 64}; do
     -s 4 -c 1 -f -o $OUT/block_B${B} python tools/profile_block.py --B $B > $OUT/ncu_B$B.log 2>&1
   echo "ncu full B=$B rc=$?"
 done
+python tools/ncu_summary.py traffic $OUT/block_traffic.json $OUT/block_B*.ncu-rep > $OUT/summary.log 2>&1
+[ -f $OUT/launches.csv ] && python tools/ncu_summary.py launches $OUT/launches.md $OUT/launches.csv >> $OUT/summary.log 2>&1
+for B in 1 16 64; do
+  [ -f $OUT/block_B$B.ncu-rep ] && $NCU -i $OUT/block_B$B.ncu-rep --page raw --csv > $OUT/block_B${B}_raw.csv 2>/dev/null
+done
+[ -z "${KEEP_REPS:-}" ] && rm -f $OUT/*.ncu-rep
+du -sh $OUT
