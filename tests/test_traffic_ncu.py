@@ -74,7 +74,9 @@ def test_materialized_intermediates_trip_the_write_counter():
     reads it back: the counter must see at least that much more than the
     fused block (the reference's MaterializeIntermediate mutant)."""
     B, dm, df = 64, 4096, 14336
-    fused = counters(B, "fused", dm, df)["lts__t_sectors_srcunit_tex_op_write.sum"] * 32
+    # (whole stage-1 tiles: the N >= 32 tail split's workspace re-zeroing is
+    # not an intermediate and would eat into the margin)
+    fused = counters(B, "fused_notail", dm, df)["lts__t_sectors_srcunit_tex_op_write.sum"] * 32
     two = counters(B, "two", dm, df)["lts__t_sectors_srcunit_tex_op_write.sum"] * 32
     assert two - fused >= 0.9 * 2 * B * df * 2, (two, fused)
 
