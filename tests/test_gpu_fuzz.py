@@ -45,3 +45,43 @@ def test_random_shapes_default_config(oracle_lib):
             del w
     finally:
         ctx.close()
+
+
+def test_random_configs_ragged_shapes(oracle_lib):
+    """Random points of the scheduler's search space (tail split 0-4 parts,
+    CTA count, stage-1 / down chunk, stage size, kernel family at B <= 8, fp32
+    or bf16 Y) on ragged shapes, each run twice back to back against the fp64
+    oracle: every configuration dfk_tune may pick must be exact to tolerance,
+    not only the ones the default takes."""
+    from paper_2602_11808_b200 import runtime as rt
+
+    import os
+    rng = np.random.default_rng(int(os.environ.get("DFK_FUZZ_SEED", "20261018")))
+    ctx = rt.Context(0)
+    try:
+        for case in range(int(os.environ.get("DFK_FUZZ_CASES", "30"))):
+            dm = int(rng.choice([136, 520, 1000]))
+            df = int(rng.choice([1032, 4000, 9990]))
+            B = int(rng.choice([1, 5, 8, 16, 33, 64]))
+            fam = (rt.FAMILY_GEMV if B <= 8 and rng.random() < 0.3 else rt.FAMILY_TC)
+            kw = dict(block_kernel=1, dynamic_sched=1, s1_family=fam, down_family=fam,
+                      s1_tail=int(rng.integers(0, 5)),
+                      s1_ctas=int(rng.choice([0, 3, 17, 100, 148])),
+                      chunk_kb=int(rng.choice([0, 3, 8, 24])),
+                      s1_chunk_kb=int(rng.choice([0, 0, 5, 16])),
+                      kbs=int(rng.choice([0, 2, 3])) if fam == rt.FAMILY_TC else 0)
+            cfg = rt.Config.make(**kw)
+            y_dt = rt.BF16 if rng.random() < 0.3 else rt.F32
+            x, wu, wg, wd = (oracle_lib.quantize_bf16(a)[0] for a in
+                             oracle_lib.make_instance(2000 + case, B, dm, df, 1.0 / np.sqrt(dm)))
+            _, y_ref = oracle_lib.forward(x, wu, wg, wd)
+            w = ctx.weights(wg, wu, wd)
+            xd = ctx.array((B, dm)).upload(x)
+            y = ctx.array((B, dm), y_dt)
+            for _ in range(2):
+                ctx.forward(w, xd, y, cfg=cfg)
+            tol = TOL if y_dt == rt.F32 else 2 * TOL
+            assert rel_err(y.download(), y_ref) <= tol, (case, dm, df, B, kw, y_dt)
+            del w
+    finally:
+        ctx.close()
