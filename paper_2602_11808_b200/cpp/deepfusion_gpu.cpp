@@ -52,6 +52,26 @@ struct Scratch {
   }
 };
 
+// Pinned host staging for the stage-only calls' copies (pageable std::vector
+// buffers made every H2D / D2H a bounce-buffered synchronous copy: ~0.3 ms of
+// run_fused_stage1's A2 read-back at Llama-8B B = 64).  Grows geometrically;
+// used under Runtime::mu.
+struct PinnedScratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      const size_t nb = std::max(need, 2 * bytes);
+      if (p) dfk_host_free(p);
+      p = nullptr;
+      bytes = 0;
+      check(dfk_host_alloc(nb, &p));
+      bytes = nb;
+    }
+    return p;
+  }
+};
+
 // One process-wide context per device (created on first use), its scratch,
 // and an LRU cache of prepacked weight sets keyed by the matrices' exact
 // contents (Matrix id + version, see deepfusion.hpp).
@@ -59,6 +79,7 @@ struct Runtime {
   std::mutex mu;
   std::map<int, dfk_context> ctx;
   std::map<int, Scratch> x_buf, a2_buf, y_buf;
+  PinnedScratch h_in, h_out;  // host staging of the stage-only calls
 
   struct Key {
     std::uint64_t g_id, g_ver, u_id, u_ver, d_id, d_ver;
@@ -165,13 +186,14 @@ void gpu_stage1(const dfk_config* cfg, const Matrix& x, const Matrix& w_up,
   dfk_context c = r.context(0);
   void* xd = r.x_buf[0].get(c, static_cast<size_t>(B * dm) * 2);
   void* ad = r.a2_buf[0].get(c, static_cast<size_t>(B * df) * 2);
-  std::vector<std::uint16_t> xb(static_cast<size_t>(B * dm)), out(static_cast<size_t>(B * df));
-  to_bf16(x.data(), B * dm, xb.data());
-  check(dfk_memcpy_h2d(c, xd, xb.data(), xb.size() * 2));
+  auto* xb = static_cast<std::uint16_t*>(r.h_in.get(static_cast<size_t>(B * dm) * 2));
+  auto* out = static_cast<std::uint16_t*>(r.h_out.get(static_cast<size_t>(B * df) * 2));
+  to_bf16(x.data(), B * dm, xb);
+  check(dfk_memcpy_h2d(c, xd, xb, static_cast<size_t>(B * dm) * 2));
   check(dfk_stage1(c, h, xd, B, ad, cfg));
-  check(dfk_memcpy_d2h(c, out.data(), ad, out.size() * 2));
+  check(dfk_memcpy_d2h(c, out, ad, static_cast<size_t>(B * df) * 2));
   check(dfk_context_sync(c));
-  from_bf16(out.data(), a2);
+  from_bf16(out, a2);
 }
 
 Matrix gpu_forward(const dfk_config* cfg, const Matrix& x, const MlpWeights& w) {
@@ -379,15 +401,15 @@ Matrix down_projection(const Matrix& a2, const Matrix& w_down, Accounting) {
   dfk_context c = r.context(0);
   void* ad = r.a2_buf[0].get(c, static_cast<size_t>(B * df) * 2);
   void* yd = r.y_buf[0].get(c, static_cast<size_t>(B * dm) * 4);
-  std::vector<std::uint16_t> ab(static_cast<size_t>(B * df));
-  to_bf16(a2.data(), B * df, ab.data());
-  check(dfk_memcpy_h2d(c, ad, ab.data(), ab.size() * 2));
+  auto* ab = static_cast<std::uint16_t*>(r.h_in.get(static_cast<size_t>(B * df) * 2));
+  auto* out = static_cast<float*>(r.h_out.get(static_cast<size_t>(B * dm) * 4));
+  to_bf16(a2.data(), B * df, ab);
+  check(dfk_memcpy_h2d(c, ad, ab, static_cast<size_t>(B * df) * 2));
   check(dfk_down(c, h, ad, B, yd, DFK_F32, nullptr));
-  std::vector<float> out(static_cast<size_t>(B * dm));
-  check(dfk_memcpy_d2h(c, out.data(), yd, out.size() * 4));
+  check(dfk_memcpy_d2h(c, out, yd, static_cast<size_t>(B * dm) * 4));
   check(dfk_context_sync(c));
   Matrix y(B, dm);
-  check(dfk_host_from_f32(out.data(), out.size(), y.data(), DFK_F64));
+  check(dfk_host_from_f32(out, static_cast<size_t>(B * dm), y.data(), DFK_F64));
   return y;
 }
 
