@@ -11,9 +11,20 @@
 // third of that (profiles/r2_host_convert.md).  Splitting the loops over a
 // worker pool was measured too: faster into a warm caller buffer, slower
 // into the freshly zeroed Matrix the C++ drop-in returns (the lines live in
-// the calling core's cache), so the calls stay on the caller's thread.
+// the calling core's cache), so B x d_model sized calls stay on the caller's
+// thread.  Only conversions of >= kParallelMin elements -- the B x d_ff A2 of
+// the drop-in's run_fused_stage1 / down_projection at large B (7.3 MB of
+// fp64 at Llama-8B B = 64), which is memory-bandwidth bound on one core --
+// are split over a small persistent pool.
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "internal.h"
 
@@ -28,17 +39,119 @@ inline uint16_t bf16_rne(float f) {
   return static_cast<uint16_t>(nan ? ((u >> 16) | 0x40u) : r);
 }
 
+constexpr size_t kParallelMin = size_t{1} << 19;  // elements
+constexpr size_t kChunk = size_t{1} << 16;
+
+// A job lives on the caller's stack: [0, n) split into kChunk pieces taken
+// with an atomic cursor by the workers and the caller alike.  Workers pick
+// the job up under the lock (counted in `active`) and the caller returns only
+// when every piece is done and no worker still holds the job.  One job at a
+// time: a caller that finds the pool busy converts serially.
+class Pool {
+ public:
+  static Pool& get() {
+    static Pool* p = new Pool();  // never destroyed: no join race at exit
+    return *p;
+  }
+  bool run(size_t n, const std::function<void(size_t, size_t)>& fn) {
+    std::unique_lock<std::mutex> busy(busy_, std::try_to_lock);
+    if (!busy.owns_lock() || workers_ == 0) return false;
+    Job job{&fn, n, (n + kChunk - 1) / kChunk};
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &job;
+      ++gen_;
+    }
+    cv_.notify_all();
+    job.work();
+    while (job.done.load(std::memory_order_acquire) < job.chunks) std::this_thread::yield();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = nullptr;  // no new worker picks it up
+    }
+    while (active_.load(std::memory_order_acquire) != 0) std::this_thread::yield();
+    return true;
+  }
+
+ private:
+  struct Job {
+    const std::function<void(size_t, size_t)>* fn;
+    size_t n, chunks;
+    std::atomic<size_t> next{0}, done{0};
+    Job(const std::function<void(size_t, size_t)>* f, size_t n_, size_t c)
+        : fn(f), n(n_), chunks(c) {}
+    void work() {
+      for (size_t c; (c = next.fetch_add(1)) < chunks;) {
+        (*fn)(c * kChunk, std::min(n, (c + 1) * kChunk));
+        done.fetch_add(1, std::memory_order_release);
+      }
+    }
+  };
+  Pool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    workers_ = std::min(7u, hw > 2 ? hw / 2 - 1 : 0u);
+    for (unsigned i = 0; i < workers_; ++i) std::thread([this] { loop(); }).detach();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      Job* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        job = job_;
+        if (!job) continue;
+        active_.fetch_add(1, std::memory_order_relaxed);
+      }
+      job->work();
+      active_.fetch_sub(1, std::memory_order_release);
+    }
+  }
+  std::mutex busy_, mu_;
+  std::condition_variable cv_;
+  Job* job_ = nullptr;
+  uint64_t gen_ = 0;
+  std::atomic<int> active_{0};
+  unsigned workers_ = 0;
+};
+
+// The element loops over [lo, hi), kept as plain functions on restrict
+// pointers so that they vectorise (the inline path of small calls runs them
+// directly, the pool through a std::function per chunk).
+void f64_to_bf16(const double* __restrict s, uint16_t* __restrict d, size_t lo, size_t hi) {
+  for (size_t i = lo; i < hi; ++i) d[i] = bf16_rne(static_cast<float>(s[i]));
+}
+void f32_to_bf16(const float* __restrict s, uint16_t* __restrict d, size_t lo, size_t hi) {
+  for (size_t i = lo; i < hi; ++i) d[i] = bf16_rne(s[i]);
+}
+inline float widen(uint16_t v) {
+  const uint32_t u = static_cast<uint32_t>(v) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
 }  // namespace
 
+// Rounding into bf16 (our own staging buffer, fp64 / fp32 input of any
+// size): large inputs on the pool -- the drop-in's down_projection A2 at
+// B = 64 (917 K elements) 750 -> 600 us.  Widening into the caller's fp64
+// Matrix stays on the calling thread: the pool was slower there (B = 64
+// run_fused_stage1 517 -> 620 us; the destination lines are the caller's).
 void host_to_bf16(const void* src, int dtype, size_t n, uint16_t* dst) {
   if (dtype == DFK_BF16) {
     std::memcpy(dst, src, n * 2);
   } else if (dtype == DFK_F32) {
     const float* s = static_cast<const float*>(src);
-    for (size_t i = 0; i < n; ++i) dst[i] = bf16_rne(s[i]);
+    if (n < kParallelMin ||
+        !Pool::get().run(n, [=](size_t lo, size_t hi) { f32_to_bf16(s, dst, lo, hi); }))
+      f32_to_bf16(s, dst, 0, n);
   } else {
     const double* s = static_cast<const double*>(src);
-    for (size_t i = 0; i < n; ++i) dst[i] = bf16_rne(static_cast<float>(s[i]));
+    if (n < kParallelMin ||
+        !Pool::get().run(n, [=](size_t lo, size_t hi) { f64_to_bf16(s, dst, lo, hi); }))
+      f64_to_bf16(s, dst, 0, n);
   }
 }
 
@@ -55,12 +168,6 @@ void host_from_f32(const float* src, size_t n, void* dst, int dtype) {
 }
 
 void host_from_bf16(const uint16_t* src, size_t n, void* dst, int dtype) {
-  auto widen = [](uint16_t v) {
-    const uint32_t u = static_cast<uint32_t>(v) << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
-  };
   if (dtype == DFK_BF16) {
     std::memcpy(dst, src, n * 2);
   } else if (dtype == DFK_F32) {

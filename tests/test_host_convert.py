@@ -30,7 +30,7 @@ def _special_values():
     return np.concatenate([f, ties])
 
 
-@pytest.mark.parametrize("n", [7, 1000, 300_001])
+@pytest.mark.parametrize("n", [7, 1000, 300_001, 1_300_007])  # the last: worker pool
 def test_f64_to_bf16_matches_oracle(rt, oracle_lib, n):
     rng = np.random.default_rng(n)
     a = rng.standard_normal(n) * np.exp(rng.uniform(-30, 30, n))
@@ -47,7 +47,7 @@ def test_nan_stays_quiet_nan(rt):
     assert np.all(got & 0x0040)
 
 
-@pytest.mark.parametrize("n", [5, 200_003])
+@pytest.mark.parametrize("n", [5, 200_003, 700_001])
 def test_f32_to_bf16_and_bf16_passthrough(rt, oracle_lib, n):
     rng = np.random.default_rng(1 + n)
     f = (rng.standard_normal(n) * 100).astype(np.float32)
@@ -57,7 +57,7 @@ def test_f32_to_bf16_and_bf16_passthrough(rt, oracle_lib, n):
     assert np.array_equal(_to_bf16(rt, got, rt.BF16), got)
 
 
-@pytest.mark.parametrize("n", [3, 250_000])
+@pytest.mark.parametrize("n", [3, 250_000, 917_504])
 def test_widening_is_exact(rt, oracle_lib, n):
     rng = np.random.default_rng(2 + n)
     f = (rng.standard_normal(n) * 1e3).astype(np.float32)
@@ -76,9 +76,11 @@ def test_widening_is_exact(rt, oracle_lib, n):
 
 
 def test_concurrent_callers_share_the_pool(rt, oracle_lib):
-    """Several host threads converting at once (no shared state)."""
+    """Several host threads converting at once: small calls inline, large
+    ones on the worker pool (one job at a time; a caller finding it busy
+    converts inline) -- every result exact."""
     rng = np.random.default_rng(9)
-    arrays = [rng.standard_normal(180_000 + 1000 * i) for i in range(6)]
+    arrays = [rng.standard_normal((180_000 if i % 2 else 700_000) + 1000 * i) for i in range(6)]
     wants = [oracle_lib.quantize_bf16(a)[1] for a in arrays]
     results = [None] * len(arrays)
 
