@@ -12,10 +12,9 @@
 // worker pool was measured too: faster into a warm caller buffer, slower
 // into the freshly zeroed Matrix the C++ drop-in returns (the lines live in
 // the calling core's cache), so B x d_model sized calls stay on the caller's
-// thread.  Only conversions of >= kParallelMin elements -- the B x d_ff A2 of
-// the drop-in's run_fused_stage1 / down_projection at large B (7.3 MB of
-// fp64 at Llama-8B B = 64), which is memory-bandwidth bound on one core --
-// are split over a small persistent pool.
+// thread.  Only rounding to bf16 of >= kParallelMin elements (into our own
+// staging buffer: X at B >= 32, the B x d_ff A2 the drop-in's down_projection
+// receives) is split over a small persistent pool.
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -39,7 +38,7 @@ inline uint16_t bf16_rne(float f) {
   return static_cast<uint16_t>(nan ? ((u >> 16) | 0x40u) : r);
 }
 
-constexpr size_t kParallelMin = size_t{1} << 19;  // elements
+constexpr size_t kParallelMin = size_t{1} << 17;  // elements
 constexpr size_t kChunk = size_t{1} << 16;
 
 // A job lives on the caller's stack: [0, n) split into kChunk pieces taken
@@ -135,8 +134,9 @@ inline float widen(uint16_t v) {
 }  // namespace
 
 // Rounding into bf16 (our own staging buffer, fp64 / fp32 input of any
-// size): large inputs on the pool -- the drop-in's down_projection A2 at
-// B = 64 (917 K elements) 750 -> 600 us.  Widening into the caller's fp64
+// size): inputs of >= 128 K elements on the pool -- the drop-in's
+// down_projection A2 at B = 64 (917 K elements) 750 -> 620 us,
+// dfk_forward_host's X at B = 32 / 64: 227 -> 190 / 361 -> 339 us per call.  Widening into the caller's fp64
 // Matrix stays on the calling thread: the pool was slower there (B = 64
 // run_fused_stage1 517 -> 620 us; the destination lines are the caller's).
 void host_to_bf16(const void* src, int dtype, size_t n, uint16_t* dst) {
